@@ -1,0 +1,149 @@
+"""CPU oracle for the Atom W4A4 hot path (arXiv 2310.19102) -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package.  The product package ``paper_2310_19102_b200``
+never imports it and shares no code with it.
+
+The arithmetic lives in ``atom_oracle.c`` (plain C, fp32 steps pinned, int64 partials, double
+output); this module only marshals numpy arrays through ctypes.  Paper citations are in the C file.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+GROUP = 128
+_HERE = Path(__file__).resolve().parent
+_SRC = _HERE / "atom_oracle.c"
+_LIB = _HERE / "liboracle.so"
+
+ORC_OK, ORC_ERR_NULL, ORC_ERR_SHAPE, ORC_ERR_ARG, ORC_ERR_OVERFLOW = 0, 1, 2, 4, 8
+
+
+def build(force: bool = False) -> Path:
+    """Compile the oracle with pinned IEEE semantics (no contraction, no fast-math)."""
+    if force or not _LIB.exists() or _LIB.stat().st_mtime < _SRC.stat().st_mtime:
+        tmp = _LIB.with_suffix(f".so.tmp{os.getpid()}")
+        subprocess.run(
+            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+             "-fPIC", "-shared", "-o", str(tmp), str(_SRC), "-lm"],
+            check=True)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(str(build()))
+        P = ctypes.c_void_p
+        i64, i32, f32 = ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+        L.oracle_quantize_rows.argtypes = [P, i64, i64, P, i64, i32, f32, f32, P, P, P]
+        L.oracle_group_partials.argtypes = [P, P, P, P, i64, i64, i64, i32, P]
+        L.oracle_gemm_output.argtypes = [P, P, P, i64, i64, i64, P]
+        L.oracle_output_rows.argtypes = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, P]
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_max_threads.restype = ctypes.c_int
+        for f in (L.oracle_quantize_rows, L.oracle_group_partials, L.oracle_gemm_output,
+                  L.oracle_output_rows):
+            f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(st: int, what: str):
+    if st != ORC_OK:
+        raise OracleError(f"{what} failed with oracle status {st}")
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())
+
+
+def quantize_rows(x, perm, K: int, k_outlier: int = 128, clip_int4: float = 0.9,
+                  clip_int8: float = 1.0):
+    """O2-O6 (reorder, group amax, scale, code, pack) for every row of ``x``.
+
+    ``x`` is an fp16 or fp32 [rows][ldx] array (fp16 is widened exactly to fp32 first).
+    Returns (q4 uint8 [rows][(K-k_o)/2], q8 int8 [rows][k_o] or None, scales fp32 [K/128][rows]).
+    Activations use clip_int4 = 0.9, weights 0.85; outliers clip_int8 = 1.0.
+    """
+    x32 = np.ascontiguousarray(np.asarray(x).astype(np.float32))
+    rows, ldx = x32.shape
+    perm = np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    assert perm.shape == (K,)
+    q4 = np.zeros((rows, (K - k_outlier) // 2), dtype=np.uint8)
+    q8 = np.zeros((rows, k_outlier), dtype=np.int8) if k_outlier else None
+    sc = np.zeros((K // GROUP, rows), dtype=np.float32)
+    st = lib().oracle_quantize_rows(_ptr(x32), rows, ldx, _ptr(perm), K, k_outlier,
+                                    ctypes.c_float(clip_int4), ctypes.c_float(clip_int8),
+                                    _ptr(q4), _ptr(q8), _ptr(sc))
+    _check(st, "oracle_quantize_rows")
+    return q4, q8, sc
+
+
+def group_partials(a_q4, a_q8, w_q4, w_q8, M: int, N: int, K: int, k_outlier: int = 128):
+    """O7: exact int32 partials [G][M][N] (int64 accumulation, overflow-checked)."""
+    out = np.zeros((K // GROUP, M, N), dtype=np.int32)
+    st = lib().oracle_group_partials(_ptr(_c(a_q4)), _ptr(_c(a_q8)), _ptr(_c(w_q4)),
+                                     _ptr(_c(w_q8)), M, N, K, k_outlier, _ptr(out))
+    _check(st, "oracle_group_partials")
+    return out
+
+
+def gemm_output(partials, a_scales, w_scales):
+    """O8: C = sum_t s_a[t][m] s_w[t][n] P_t[m][n] in float64, t ascending."""
+    G, M, N = partials.shape
+    c = np.zeros((M, N), dtype=np.float64)
+    st = lib().oracle_gemm_output(_ptr(_c(partials)), _ptr(_c(a_scales)), _ptr(_c(w_scales)),
+                                  M, N, G, _ptr(c))
+    _check(st, "oracle_gemm_output")
+    return c
+
+
+def output_rows(a_q4, a_q8, a_scales, w_q4, w_q8, w_scales, M: int, N: int, K: int,
+                k_outlier: int, rows):
+    """O7+O8 for selected token rows only (sampled parity at full size, CPU baseline timing)."""
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    c = np.zeros((rows.size, N), dtype=np.float64)
+    st = lib().oracle_output_rows(_ptr(_c(a_q4)), _ptr(_c(a_q8)), _ptr(_c(a_scales)),
+                                  _ptr(_c(w_q4)), _ptr(_c(w_q8)), _ptr(_c(w_scales)),
+                                  M, N, K, k_outlier, _ptr(rows), rows.size, _ptr(c))
+    _check(st, "oracle_output_rows")
+    return c
+
+
+def _c(a):
+    return None if a is None else np.ascontiguousarray(a)
+
+
+def quantized_linear(x, perm, w, K: int, k_outlier: int = 128, clip_a: float = 0.9,
+                     clip_w: float = 0.85, clip_int8: float = 1.0):
+    """Whole path on the CPU: quantize W (offline, a0) and X (a1), partials (a2) and output (a3-a5
+    before the fp16 rounding).  Returns a dict of every intermediate."""
+    M, N = x.shape[0], w.shape[0]
+    a_q4, a_q8, a_s = quantize_rows(x, perm, K, k_outlier, clip_a, clip_int8)
+    w_q4, w_q8, w_s = quantize_rows(w, perm, K, k_outlier, clip_w, clip_int8)
+    P = group_partials(a_q4, a_q8, w_q4, w_q8, M, N, K, k_outlier)
+    C = gemm_output(P, a_s, w_s)
+    return dict(a_q4=a_q4, a_q8=a_q8, a_scales=a_s, w_q4=w_q4, w_q8=w_q8, w_scales=w_s,
+                partials=P, c=C)
