@@ -1,0 +1,135 @@
+/*
+ * atom.h -- C ABI of the B200-native Atom W4A4 hot path (arXiv 2310.19102).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (the paper), "S:n" = SPEC.md line n.
+ *
+ * The path:
+ *   a0  atom_quantize_weights   offline: reorder weight columns by the calibration index and
+ *                               quantize them (RTN; GPTQ is out of scope)
+ *   a1  atom_reorder_quantize   online: reorder activation channels and dynamically quantize
+ *                               them (INT4 groups of 128 + INT8 outlier block)
+ *   a2-a5 atom_w4a4_gemm        fused mixed-precision group GEMM: exact int32 partial per
+ *                               K-group on the tensor cores, dequantized with s_a*s_w and
+ *                               accumulated in fp32, outlier INT8 group fused, fp16 out
+ *                                                                                P:254, Fig 6
+ *
+ * Conventions shared by every entry point
+ *   - Pointers are DEVICE pointers owned by the caller (e.g. torch tensors' data_ptr()).  The
+ *     library never allocates, frees, retains or synchronizes; every call is asynchronous on
+ *     `stream` (a cudaStream_t passed as void*, NULL = legacy default stream).
+ *   - Arguments are validated on the host BEFORE anything is launched; on error nothing is
+ *     launched and a non-zero atom_status_t is returned.  Nothing aborts or throws across the ABI.
+ *   - Device faults (e.g. an out-of-range perm entry, which is a precondition and not checked on
+ *     the hot path) surface at the caller's next synchronization.  atom_validate_perm() checks a
+ *     perm on the device for tests.
+ *   - All base pointers must be 16-byte aligned.  Calls are reentrant; the only global state is
+ *     a per-device attribute cache.
+ *   - Group size is fixed at g = 128 ("group size of 128"); k_outlier is 0 or 128
+ *     ("128 channels ... keep them in INT8"); K counts the outlier channels (P:256 fn).
+ *
+ * Quantized formats (bit-exact with the CPU oracle in oracle/)
+ *   q4      uint8 [rows][(K - k_outlier)/2]  symmetric INT4 codes in [-8, 7], two's-complement
+ *           nibbles, low nibble = even (lower) reordered channel
+ *   q8      int8  [rows][k_outlier]          symmetric INT8 codes of the outlier block
+ *   scales  fp32  [K/128][rows]              group-major; row t < G4 = (K-k_o)/128 is INT4 group
+ *           t, the last row is the outlier scale when k_outlier == 128 (one per token / channel)
+ *   Quantizer: s = 2*max|x|*c/(2^n - 1), evaluated as alpha = fl(fl(2c)/(2^n-1)),
+ *   s = fl(amax*alpha) (s = FLT_MIN for an all-zero group), q = clamp(rint_even(fl(x*fl(1/s))),
+ *   -2^(n-1), 2^(n-1)-1).
+ */
+#ifndef ATOM_H_
+#define ATOM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ATOM_ABI_VERSION 1
+#define ATOM_GROUP 128
+
+typedef enum {
+  ATOM_OK = 0,
+  ATOM_ERR_NULL = 1,        /* a required pointer is NULL (or a forbidden one is non-NULL) */
+  ATOM_ERR_SHAPE = 2,       /* K % 128, N % 128, M < 0, ld too small, ... */
+  ATOM_ERR_ALIGN = 3,       /* a pointer or leading dimension breaks the alignment rules */
+  ATOM_ERR_ARG = 4,         /* k_outlier not in {0,128}, clip not in (0,1], bad dtype */
+  ATOM_ERR_WORKSPACE = 5,   /* workspace missing or smaller than atom_w4a4_gemm_workspace_size */
+  ATOM_ERR_UNSUPPORTED = 6, /* current device is not sm_100 (B200) */
+  ATOM_ERR_CUDA = 7         /* a CUDA runtime/driver call or the launch itself failed */
+} atom_status_t;
+
+typedef enum { ATOM_F16 = 0, ATOM_F32 = 1 } atom_dtype_t;
+
+/*
+ * a1: reorder + dynamic quantize activations ("fuses the activation matrix reordering
+ * operators", "tailoring quantization parameters for each activation matrix").
+ *   x_f16      fp16 [M][ldx] row-major; token m, source channel c at x_f16[m*ldx + c]
+ *   perm       int32 [K]: reordered channel j reads source channel perm[j] (gather).  The last
+ *              k_outlier entries are the outlier channels (Fig 4).  A K-shard passes
+ *              perm + k0 with its own K (multiple of 128) and k_outlier = 128 only on the shard
+ *              that owns the tail.  Precondition (unchecked): 0 <= perm[j] < ldx.
+ *   K          number of reordered channels, K % 128 == 0, K >= k_outlier
+ *   k_outlier  0 or 128
+ *   clip_int4  clipping factor of the INT4 groups, in (0,1]; the paper's 0.9 for activations
+ *   clip_int8  clipping factor of the INT8 outlier block, in (0,1]; 1.0
+ *   q4, q8, scales  outputs as described above (q8 must be NULL iff k_outlier == 0; q4 may be
+ *              NULL iff K == k_outlier).  ldx % 8 == 0 (16-byte rows).
+ *   M == 0 is a no-op.
+ */
+atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip_int4, float clip_int8,
+                                    uint8_t* q4, int8_t* q8, float* scales, void* stream);
+
+/*
+ * a0: offline weight reorder + quantize (Fig 4 P:237 "The weight matrix (W) is statically
+ * reordered"; P:299 RTN stands in for GPTQ, which only changes the codes offline).  Same math
+ * and formats as atom_reorder_quantize with rows = output channels n of W [N][ldw] (nn.Linear
+ * layout); the paper's clip is 0.85 for weights.  scales are fp32 [K/128][N].
+ */
+atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip_int4, float clip_int8,
+                                    uint8_t* q4, int8_t* q8, float* scales, void* stream);
+
+/*
+ * a2-a5: fused mixed-precision group GEMM (P:254 Steps 1-3, Fig 6, outliers P:230):
+ *     P_t[m][n] = sum_{j in group t} qa[m][j] * qw[n][j]            exact int32 (tensor cores)
+ *     C[m][n]   = sum_t a_scales[t][m] * w_scales[t][n] * P_t[m][n]  fp32 accumulation
+ *   written to c[m*ldc + n] as fp16 (c_dtype = ATOM_F16) or as the fp32 partial sum (ATOM_F32,
+ *   for K-sharded tensor parallelism where partials are all-reduced in fp32).
+ *   a_q4/a_q8/a_scales  activations from atom_reorder_quantize (M rows)
+ *   w_q4/w_q8/w_scales  weights from atom_quantize_weights (N rows), same perm and K
+ *   M >= 0 (M == 0 is a no-op), N % 128 == 0, K % 128 == 0, k_outlier in {0,128},
+ *   ldc >= N, ldc % 8 == 0 (an N-shard can write its column block into a wider buffer).
+ *   debug_partials  NULL, or int32 [K/128][M][N]: every exact group partial P_t (test-only).
+ *   workspace       may be NULL when atom_w4a4_gemm_workspace_size() returns 0.
+ */
+atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
+                             const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
+                             int64_t M, int64_t N, int64_t K, int32_t k_outlier,
+                             void* c, int64_t ldc, atom_dtype_t c_dtype,
+                             int32_t* debug_partials, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+/* Bytes of device workspace atom_w4a4_gemm needs for this shape (0 today: no split-K). */
+size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier);
+
+/* Test helper: on `stream`, sets *ok_flag (device int32) to 1 iff perm[0..K) is a bijection of
+ * [0,K) (ldx == K) or an injection into [0,ldx).  scratch: device int32 [ldx], clobbered. */
+atom_status_t atom_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
+                                 int32_t* ok_flag, void* stream);
+
+const char* atom_status_string(atom_status_t s);
+int atom_abi_version(void);
+/* Number of kernel launches the last successful call on this thread issued (for bench
+ * accounting of "gpu_launches"). */
+int atom_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATOM_H_ */

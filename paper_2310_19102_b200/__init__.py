@@ -1,0 +1,214 @@
+"""B200-native Atom W4A4 hot path (arXiv 2310.19102) -- thin Python binding over libatom.so.
+
+Argument marshalling only: every step of the path runs in the CUDA kernels behind the C ABI
+(include/atom.h).  PyTorch supplies device memory and streams.  There is no CPU fallback: if the
+in-tree ``libatom.so`` is missing or a call fails, an exception is raised.
+
+Names follow the ABI and the paper:
+  reorder_quantize(x, perm)        a1  online activation reorder + dynamic quantize
+  quantize_weights(w, perm)        a0  offline weight reorder + quantize
+  w4a4_gemm(a, w)                  a2-a5 fused group GEMM with INT8 outliers
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Optional
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libatom.so"
+GROUP = 128
+
+ATOM_OK = 0
+STATUS_NAMES = {0: "ATOM_OK", 1: "ATOM_ERR_NULL", 2: "ATOM_ERR_SHAPE", 3: "ATOM_ERR_ALIGN",
+                4: "ATOM_ERR_ARG", 5: "ATOM_ERR_WORKSPACE", 6: "ATOM_ERR_UNSUPPORTED",
+                7: "ATOM_ERR_CUDA"}
+ATOM_F16, ATOM_F32 = 0, 1
+
+# every symbol include/atom.h declares
+ABI_SYMBOLS = ("atom_reorder_quantize", "atom_quantize_weights", "atom_w4a4_gemm",
+               "atom_w4a4_gemm_workspace_size", "atom_validate_perm", "atom_status_string",
+               "atom_abi_version", "atom_last_launch_count")
+
+
+class AtomError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {STATUS_NAMES.get(status, status)} "
+                         f"({_lib().atom_status_string(status).decode()})")
+
+
+_L = None
+
+
+def _lib():
+    """Load the in-tree libatom.so (fail loudly if it was never built)."""
+    global _L
+    if _L is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (no CPU fallback exists)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        P, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+        q_args = [P, i64, i64, P, i64, i32, f32, f32, P, P, P, P]
+        L.atom_reorder_quantize.argtypes = q_args
+        L.atom_quantize_weights.argtypes = q_args
+        L.atom_w4a4_gemm.argtypes = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int,
+                                     P, P, ctypes.c_size_t, P]
+        L.atom_w4a4_gemm_workspace_size.argtypes = [i64, i64, i64, i32]
+        L.atom_w4a4_gemm_workspace_size.restype = ctypes.c_size_t
+        L.atom_validate_perm.argtypes = [P, i64, i64, P, P, P]
+        L.atom_status_string.argtypes = [ctypes.c_int]
+        L.atom_status_string.restype = ctypes.c_char_p
+        L.atom_abi_version.restype = ctypes.c_int
+        L.atom_last_launch_count.restype = ctypes.c_int
+        for f in (L.atom_reorder_quantize, L.atom_quantize_weights, L.atom_w4a4_gemm,
+                  L.atom_validate_perm):
+            f.restype = ctypes.c_int
+        _L = L
+    return _L
+
+
+def load():
+    """Return the ctypes handle of libatom.so (raises if it is missing)."""
+    return _lib()
+
+
+def abi_version() -> int:
+    return int(_lib().atom_abi_version())
+
+
+def last_launch_count() -> int:
+    return int(_lib().atom_last_launch_count())
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _check(st: int, what: str):
+    if st != ATOM_OK:
+        raise AtomError(st, what)
+
+
+@dataclass
+class Quantized:
+    """Packed operand: q4 uint8 [rows][(K-k_o)/2], q8 int8 [rows][k_o] (or None),
+    scales fp32 [K/128][rows] (group-major), with the reordered K and k_outlier."""
+    q4: object
+    q8: object
+    scales: object
+    K: int
+    k_outlier: int
+
+    @property
+    def rows(self) -> int:
+        return int(self.scales.shape[1])
+
+
+def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream):
+    import torch
+    if x.dtype != torch.float16 or x.dim() != 2 or not x.is_cuda:
+        raise TypeError("expected a 2-D CUDA fp16 tensor")
+    if x.stride(1) != 1:
+        raise ValueError("rows must be contiguous")
+    if perm.dtype != torch.int32 or not perm.is_cuda or not perm.is_contiguous():
+        raise TypeError("perm must be a contiguous CUDA int32 tensor")
+    rows, ld = x.shape[0], x.stride(0)
+    K = int(perm.numel()) if K is None else int(K)
+    if out is None:
+        dev = x.device
+        q4 = torch.empty((rows, (K - k_outlier) // 2), dtype=torch.uint8, device=dev) \
+            if K > k_outlier else None
+        q8 = torch.empty((rows, k_outlier), dtype=torch.int8, device=dev) if k_outlier else None
+        sc = torch.empty((K // GROUP, rows), dtype=torch.float32, device=dev)
+        out = Quantized(q4, q8, sc, K, k_outlier)
+    st = getattr(_lib(), fn_name)(_ptr(x), rows, ld, _ptr(perm), K, k_outlier,
+                                  ctypes.c_float(clip_int4), ctypes.c_float(clip_int8),
+                                  _ptr(out.q4), _ptr(out.q8), _ptr(out.scales), _stream(stream))
+    _check(st, fn_name)
+    return out
+
+
+def reorder_quantize(x, perm, K: Optional[int] = None, k_outlier: int = 128,
+                     clip_int4: float = 0.9, clip_int8: float = 1.0, out: Quantized = None,
+                     stream=None) -> Quantized:
+    """a1: reorder + dynamically quantize activations x fp16 [M][ldx] (clip 0.9)."""
+    return _quantize("atom_reorder_quantize", x, perm, K, k_outlier, clip_int4, clip_int8, out,
+                     stream)
+
+
+def quantize_weights(w, perm, K: Optional[int] = None, k_outlier: int = 128,
+                     clip_int4: float = 0.85, clip_int8: float = 1.0, out: Quantized = None,
+                     stream=None) -> Quantized:
+    """a0: offline reorder + quantize of W fp16 [N][K] (nn.Linear layout, clip 0.85)."""
+    return _quantize("atom_quantize_weights", w, perm, K, k_outlier, clip_int4, clip_int8, out,
+                     stream)
+
+
+def workspace_size(M: int, N: int, K: int, k_outlier: int = 128) -> int:
+    return int(_lib().atom_w4a4_gemm_workspace_size(M, N, K, k_outlier))
+
+
+def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partials=None,
+              workspace=None, stream=None):
+    """a2-a5: C[m][n] = sum_t s_a[t][m] s_w[t][n] P_t[m][n] (fp32 accumulate), fp16 or fp32 out.
+
+    ``out`` may be a wider [M][ldc] view (ldc >= N) to write an N-shard in place.
+    ``debug_partials``: optional int32 [K/128][M][N] CUDA tensor receiving every exact partial.
+    """
+    import torch
+    if a.K != w.K or a.k_outlier != w.k_outlier:
+        raise ValueError("activation and weight quantization disagree on K / k_outlier")
+    M, N = a.rows, w.rows
+    if out is None:
+        dt = torch.float16 if out_dtype is None else out_dtype
+        out = torch.empty((M, N), dtype=dt, device=a.scales.device)
+    if out.dtype not in (torch.float16, torch.float32) or out.stride(1) != 1:
+        raise TypeError("out must be fp16/fp32 with contiguous rows")
+    c_dtype = ATOM_F16 if out.dtype == torch.float16 else ATOM_F32
+    ws_bytes = workspace_size(M, N, a.K, a.k_outlier)
+    if ws_bytes and workspace is None:
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=out.device)
+    st = _lib().atom_w4a4_gemm(_ptr(a.q4), _ptr(a.q8), _ptr(a.scales), _ptr(w.q4), _ptr(w.q8),
+                               _ptr(w.scales), M, N, a.K, a.k_outlier, _ptr(out), out.stride(0),
+                               c_dtype, _ptr(debug_partials), _ptr(workspace),
+                               0 if workspace is None else workspace.numel(), _stream(stream))
+    _check(st, "atom_w4a4_gemm")
+    return out
+
+
+def validate_perm(perm, ldx: Optional[int] = None, stream=None) -> bool:
+    """Device check that perm is a bijection of [0,K) (ldx == K) or an injection into [0,ldx)."""
+    import torch
+    K = perm.numel()
+    ldx = K if ldx is None else ldx
+    scratch = torch.empty(ldx, dtype=torch.int32, device=perm.device)
+    ok = torch.empty(1, dtype=torch.int32, device=perm.device)
+    _check(_lib().atom_validate_perm(_ptr(perm), K, ldx, _ptr(scratch), _ptr(ok),
+                                     _stream(stream)), "atom_validate_perm")
+    return bool(ok.item())
+
+
+class QuantizedLinear:
+    """Convenience wrapper: one Atom W4A4 linear layer (weights quantized once, offline)."""
+
+    def __init__(self, weight_f16, perm, k_outlier: int = 128, clip_w: float = 0.85,
+                 clip_a: float = 0.9, clip_int8: float = 1.0):
+        self.perm = perm
+        self.k_outlier = k_outlier
+        self.clip_a, self.clip_int8 = clip_a, clip_int8
+        self.w = quantize_weights(weight_f16, perm, k_outlier=k_outlier, clip_int4=clip_w,
+                                  clip_int8=clip_int8)
+
+    def __call__(self, x, out=None, stream=None):
+        a = reorder_quantize(x, self.perm, k_outlier=self.k_outlier, clip_int4=self.clip_a,
+                             clip_int8=self.clip_int8, stream=stream)
+        return w4a4_gemm(a, self.w, out=out, stream=stream)

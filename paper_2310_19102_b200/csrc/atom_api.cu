@@ -1,0 +1,199 @@
+// atom_api.cu -- the C ABI (include/atom.h): host-side validation, device checks, launches.
+//
+// Nothing here computes the method; it validates arguments exactly as documented in atom.h
+// (SPEC S:152 / S:283 "shape error" conventions), then calls the launchers in quantize.cu and
+// gemm.cu on the caller's stream.  No allocation, no synchronization, no exceptions.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <mutex>
+
+#include "atom.h"
+#include "internal.h"
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+struct DeviceInfo {
+  bool ok = false;
+  bool is_sm100 = false;
+  int num_sms = 0;
+};
+
+constexpr int kMaxDevices = 64;
+DeviceInfo g_dev[kMaxDevices];
+std::once_flag g_dev_once[kMaxDevices];
+
+// Per-device attribute cache (the only global state; initialised once per device).
+atom_status_t current_device(DeviceInfo* out) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return ATOM_ERR_CUDA;
+  std::call_once(g_dev_once[dev], [dev]() {
+    int major = 0, minor = 0, sms = 0;
+    DeviceInfo d;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) {
+      d.ok = true;
+      d.is_sm100 = (major == 10 && minor == 0);
+      d.num_sms = sms;
+    }
+    g_dev[dev] = d;
+  });
+  *out = g_dev[dev];
+  if (!out->ok) return ATOM_ERR_CUDA;
+  if (!out->is_sm100) return ATOM_ERR_UNSUPPORTED;
+  return ATOM_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool clip_ok(float c) { return c > 0.0f && c <= 1.0f; }
+
+atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
+                               int64_t K, int32_t k_o, float clip4, float clip8,
+                               const uint8_t* q4, const int8_t* q8, const float* scales) {
+  if (rows < 0) return ATOM_ERR_SHAPE;
+  if (!(k_o == 0 || k_o == ATOM_GROUP)) return ATOM_ERR_ARG;
+  if (K <= 0 || K % ATOM_GROUP != 0 || K < k_o) return ATOM_ERR_SHAPE;
+  if (!clip_ok(clip4) || !clip_ok(clip8)) return ATOM_ERR_ARG;
+  if (rows > 0x7fffffffLL || K > (1LL << 30)) return ATOM_ERR_SHAPE;
+  if (ld <= 0 || ld % 8 != 0 || ld > (1LL << 30)) return ATOM_ERR_SHAPE;
+  if (ld * 2 > 227 * 1024) return ATOM_ERR_SHAPE;  // the source row is staged in shared memory
+  if (rows == 0) return ATOM_OK;
+  if (!x || !perm || !scales) return ATOM_ERR_NULL;
+  if ((K > k_o) != (q4 != nullptr)) return ATOM_ERR_NULL;
+  if ((k_o > 0) != (q8 != nullptr)) return ATOM_ERR_NULL;
+  if (!aligned16(x) || !aligned16(perm) || !aligned16(scales) || (q4 && !aligned16(q4)) ||
+      (q8 && !aligned16(q8)))
+    return ATOM_ERR_ALIGN;
+  return ATOM_OK;
+}
+
+atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
+                              int64_t K, int32_t k_o, float clip4, float clip8, uint8_t* q4,
+                              int8_t* q8, float* scales, void* stream) {
+  g_last_launches = 0;
+  atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, scales);
+  if (st != ATOM_OK || rows == 0) return st;
+  DeviceInfo dev;
+  if ((st = current_device(&dev)) != ATOM_OK) return st;
+  cudaError_t e = atom::launch_reorder_quantize(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8,
+                                                scales, static_cast<cudaStream_t>(stream),
+                                                dev.num_sms);
+  if (e != cudaSuccess) return ATOM_ERR_CUDA;
+  g_last_launches = 1;
+  return ATOM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
+                                    float* scales, void* stream) {
+  return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, scales,
+                         stream);
+}
+
+atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
+                                    float* scales, void* stream) {
+  return quantize_common(w_f16, N, ldw, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, scales,
+                         stream);
+}
+
+size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
+  (void)M;
+  (void)N;
+  (void)K;
+  (void)k_outlier;
+  return 0;
+}
+
+atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
+                             const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
+                             int64_t M, int64_t N, int64_t K, int32_t k_outlier, void* c,
+                             int64_t ldc, atom_dtype_t c_dtype, int32_t* debug_partials,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  if (M < 0 || N <= 0 || N % 128 != 0) return ATOM_ERR_SHAPE;
+  if (!(k_outlier == 0 || k_outlier == ATOM_GROUP)) return ATOM_ERR_ARG;
+  if (K <= 0 || K % ATOM_GROUP != 0 || K < k_outlier) return ATOM_ERR_SHAPE;
+  if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > (1LL << 30)) return ATOM_ERR_SHAPE;
+  if (ldc < N || ldc % 8 != 0) return ATOM_ERR_SHAPE;
+  if (!(c_dtype == ATOM_F16 || c_dtype == ATOM_F32)) return ATOM_ERR_ARG;
+  const size_t ws = atom_w4a4_gemm_workspace_size(M, N, K, k_outlier);
+  if (ws > 0 && (workspace == nullptr || workspace_bytes < ws)) return ATOM_ERR_WORKSPACE;
+  if (M == 0) return ATOM_OK;
+  if (!a_scales || !w_scales || !c) return ATOM_ERR_NULL;
+  const bool has4 = K > k_outlier, has8 = k_outlier > 0;
+  if (has4 != (a_q4 != nullptr) || has4 != (w_q4 != nullptr)) return ATOM_ERR_NULL;
+  if (has8 != (a_q8 != nullptr) || has8 != (w_q8 != nullptr)) return ATOM_ERR_NULL;
+  if (!aligned16(a_scales) || !aligned16(w_scales) || !aligned16(c) ||
+      (a_q4 && !aligned16(a_q4)) || (w_q4 && !aligned16(w_q4)) || (a_q8 && !aligned16(a_q8)) ||
+      (w_q8 && !aligned16(w_q8)) || (debug_partials && !aligned16(debug_partials)))
+    return ATOM_ERR_ALIGN;
+  DeviceInfo dev;
+  atom_status_t st = current_device(&dev);
+  if (st != ATOM_OK) return st;
+  atom::GemmArgs a;
+  a.a_q4 = a_q4;
+  a.a_q8 = a_q8;
+  a.a_scales = a_scales;
+  a.w_q4 = w_q4;
+  a.w_q8 = w_q8;
+  a.w_scales = w_scales;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.k_outlier = k_outlier;
+  a.c = c;
+  a.ldc = ldc;
+  a.c_f32 = c_dtype == ATOM_F32;
+  a.debug_partials = debug_partials;
+  int launches = 0;
+  cudaError_t e =
+      atom::launch_w4a4_gemm(a, static_cast<cudaStream_t>(stream), dev.num_sms, &launches);
+  if (e != cudaSuccess) return ATOM_ERR_CUDA;
+  g_last_launches = launches;
+  return ATOM_OK;
+}
+
+atom_status_t atom_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
+                                 int32_t* ok_flag, void* stream) {
+  g_last_launches = 0;
+  if (!perm || !scratch || !ok_flag) return ATOM_ERR_NULL;
+  if (K <= 0 || ldx < K) return ATOM_ERR_SHAPE;
+  DeviceInfo dev;
+  atom_status_t st = current_device(&dev);
+  if (st != ATOM_OK) return st;
+  if (atom::launch_validate_perm(perm, K, ldx, scratch, ok_flag,
+                                 static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return ATOM_ERR_CUDA;
+  g_last_launches = 2;
+  return ATOM_OK;
+}
+
+const char* atom_status_string(atom_status_t s) {
+  switch (s) {
+    case ATOM_OK: return "ATOM_OK";
+    case ATOM_ERR_NULL: return "ATOM_ERR_NULL: required pointer missing or forbidden pointer given";
+    case ATOM_ERR_SHAPE: return "ATOM_ERR_SHAPE: invalid shape or leading dimension";
+    case ATOM_ERR_ALIGN: return "ATOM_ERR_ALIGN: pointer not 16-byte aligned";
+    case ATOM_ERR_ARG: return "ATOM_ERR_ARG: invalid k_outlier, clip factor or dtype";
+    case ATOM_ERR_WORKSPACE: return "ATOM_ERR_WORKSPACE: workspace missing or too small";
+    case ATOM_ERR_UNSUPPORTED: return "ATOM_ERR_UNSUPPORTED: device is not sm_100 (B200)";
+    case ATOM_ERR_CUDA: return "ATOM_ERR_CUDA: CUDA call or kernel launch failed";
+  }
+  return "ATOM_ERR_UNKNOWN";
+}
+
+int atom_abi_version(void) { return ATOM_ABI_VERSION; }
+
+int atom_last_launch_count(void) { return g_last_launches; }
+
+}  // extern "C"

@@ -1,0 +1,378 @@
+// gemm.cu -- a2-a5: fused W4A4 mixed-precision group GEMM on sm_100a tensor cores.
+//
+// Paper (Fig 6): per (activation group, weight group) compute the low-bit product on
+// the tensor cores (Step 1), dequantize each temporary result with its two group scales (Step 2)
+// and sum (Step 3), all fused in the MMA pipeline; the 128 INT8 outlier channels are one more
+// group of the same K loop (mixed precision via reordering P:242).
+//
+// B200 design:
+//   * swap-AB: the MMA M side (128 TMEM lanes) is 128 output channels n of W, the MMA N side is a
+//     tile of BT tokens.  D[n][m] = sum_k W'[n][k] A'[m][k].
+//   * TMA streams the PACKED INT4 tiles (64 B per row per group) into a 4-stage ring; the INT8
+//     outlier group arrives as two 64-byte halves through the same ring.
+//   * 4 unpack warps expand nibbles to int8 *16 (q << 4: one LOP per 4 codes, exact two's
+//     complement) directly into the 128B-swizzled K-major layout the UMMA descriptor reads, using
+//     the same intra-group channel permutation for both operands (the dot product is
+//     order-invariant).  tcgen05 has no s4 kind, so this is the INT4 -> INT8 step.
+//   * 1 MMA thread issues 4 x tcgen05.mma.kind::i8 (K = 32) per group into a TMEM int32
+//     accumulator that is double-buffered ACROSS groups, so group t+1 multiplies while the
+//     epilogue drains group t.  INT4 partials come out as 256*P_t (exact, |256 P| <= 2^21).
+//   * 8 epilogue warps (thread = output channel, TMEM lane) tcgen05.ld the partial, scale it by
+//     s_w[t][n] * s_a[t][m] (1/256 folded into s_w, exact) and accumulate in fp32 registers;
+//     after the last group they write fp16 (or fp32 for K-sharded TP).
+//   * persistent CTAs (one per SM) walk output tiles; consecutive CTAs share the weight tile.
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace atom {
+
+constexpr int kStages = 4;      // packed-tile TMA ring depth
+constexpr int kUbuf = 2;        // unpacked int8 operand buffers
+constexpr int kThreads = 448;   // 14 warps
+constexpr int kUnpackWarp0 = 2; // warps 2..5
+constexpr int kNumUnpackWarps = 4;
+constexpr int kEpiWarp0 = 6;    // warps 6..13
+constexpr int kNumEpiWarps = 8;
+constexpr int kTileN = 128;     // output channels per tile (MMA M)
+
+struct GemmParams {
+  const float* a_scales;
+  const float* w_scales;
+  void* c;
+  int64_t ldc;
+  int32_t* debug;
+  int M, N, G, G4, k_o, c_f32;
+  int m_tiles, num_tiles;
+};
+
+template <int BT>
+struct __align__(1024) GemmSmem {
+  uint8_t ubuf_w[kUbuf][kTileN * 128];  // unpacked weight group, SW128 K-major
+  uint8_t ubuf_a[kUbuf][BT * 128];      // unpacked activation group, SW128 K-major
+  uint8_t stage_w[kStages][kTileN * 64];// packed weight group (or half of the INT8 group)
+  uint8_t stage_a[kStages][BT * 64];    // packed activation group
+  float sa[kNumEpiWarps][BT / 2];       // per-epilogue-warp staged activation scales
+  uint64_t full[kStages], empty[kStages];
+  uint64_t ufull[kUbuf], uempty[kUbuf];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+template <int BT>
+__host__ __device__ constexpr uint32_t tmem_cols() {
+  return (2 * BT) <= 32 ? 32 : (2 * BT) <= 64 ? 64 : (2 * BT) <= 128 ? 128 : (2 * BT) <= 256 ? 256 : 512;
+}
+
+__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk) {
+  return row * 128u + (((chunk ^ (row & 7u)) & 7u) << 4);
+}
+
+template <int BT>
+__global__ void __launch_bounds__(kThreads, 1)
+w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
+                 const __grid_constant__ CUtensorMap tm_aq4,
+                 const __grid_constant__ CUtensorMap tm_wq8,
+                 const __grid_constant__ CUtensorMap tm_aq8, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  GemmSmem<BT>& sm = *reinterpret_cast<GemmSmem<BT>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  constexpr uint32_t kTmemCols = tmem_cols<BT>();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kNumUnpackWarps);
+    }
+    for (int u = 0; u < kUbuf; ++u) {
+      mbar_init(&sm.ufull[u], kNumUnpackWarps);
+      mbar_init(&sm.uempty[u], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.tfull[b], 1);
+      mbar_init(&sm.tempty[b], kNumEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_wq4);
+    tma_prefetch_desc(&tm_aq4);
+    tma_prefetch_desc(&tm_wq8);
+    tma_prefetch_desc(&tm_aq8);
+  }
+  if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  const int G = p.G, G4 = p.G4;
+  const int loads_per_tile = G4 + (p.k_o ? 2 : 0);
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int n0 = (tile / p.m_tiles) * kTileN;
+        const int m0 = (tile % p.m_tiles) * BT;
+        for (int l = 0; l < loads_per_tile; ++l, ++it) {
+          const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+          mbar_wait(&sm.empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&sm.full[s], kTileN * 64 + BT * 64);
+          if (l < G4) {
+            tma_load_2d(sm.stage_w[s], &tm_wq4, &sm.full[s], l * 64, n0);
+            tma_load_2d(sm.stage_a[s], &tm_aq4, &sm.full[s], l * 64, m0);
+          } else {
+            const int h = l - G4;
+            tma_load_2d(sm.stage_w[s], &tm_wq8, &sm.full[s], h * 64, n0);
+            tma_load_2d(sm.stage_a[s], &tm_aq8, &sm.full[s], h * 64, m0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (single thread) =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_i8(kTileN, BT);
+      uint32_t g_it = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (int t = 0; t < G; ++t, ++g_it) {
+          const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
+          const uint32_t b = g_it & 1, bph = (g_it >> 1) & 1;
+          mbar_wait(&sm.ufull[u], uph);
+          mbar_wait(&sm.tempty[b], bph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + b * BT;
+          const uint32_t a_base = smem_u32(sm.ubuf_w[u]);
+          const uint32_t b_base = smem_u32(sm.ubuf_a[u]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_i8(d, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
+                    k > 0 ? 1u : 0u);
+          umma_commit(&sm.uempty[u]);
+          umma_commit(&sm.tfull[b]);
+        }
+      }
+    }
+  } else if (warp < kEpiWarp0) {
+    // ===================== unpack warps: packed INT4 -> int8 (16*q), SW128 =====================
+    const int ut = threadIdx.x - kUnpackWarp0 * 32;  // 0..127
+    uint32_t it = 0, g_it = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int t = 0; t < G; ++t, ++g_it) {
+        const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
+        mbar_wait(&sm.uempty[u], uph ^ 1);
+        const bool int4 = t < G4;
+        const int nh = int4 ? 1 : 2;
+        for (int h = 0; h < nh; ++h, ++it) {
+          const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+          mbar_wait(&sm.full[s], ph);
+#pragma unroll 2
+          for (int i = ut; i < (kTileN + BT) * 4; i += kNumUnpackWarps * 32) {
+            const uint32_t row = i >> 2, c = i & 3;
+            const bool is_w = row < kTileN;
+            const uint32_t r = is_w ? row : row - kTileN;
+            const uint8_t* src = (is_w ? sm.stage_w[s] : sm.stage_a[s]) + r * 64 + c * 16;
+            uint8_t* dst = is_w ? sm.ubuf_w[u] : sm.ubuf_a[u];
+            const uint4 v = *reinterpret_cast<const uint4*>(src);
+            if (int4) {
+              uint4 lo, hi;
+              lo.x = (v.x << 4) & 0xF0F0F0F0u; hi.x = v.x & 0xF0F0F0F0u;
+              lo.y = (v.y << 4) & 0xF0F0F0F0u; hi.y = v.y & 0xF0F0F0F0u;
+              lo.z = (v.z << 4) & 0xF0F0F0F0u; hi.z = v.z & 0xF0F0F0F0u;
+              lo.w = (v.w << 4) & 0xF0F0F0F0u; hi.w = v.w & 0xF0F0F0F0u;
+              *reinterpret_cast<uint4*>(dst + sw128_off(r, 2 * c)) = lo;
+              *reinterpret_cast<uint4*>(dst + sw128_off(r, 2 * c + 1)) = hi;
+            } else {
+              *reinterpret_cast<uint4*>(dst + sw128_off(r, 4 * h + c)) = v;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.empty[s]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ufull[u]);
+      }
+    }
+  } else {
+    // ===================== epilogue warps =====================
+    constexpr int COLS = BT / 2;  // tokens per thread
+    const int e = warp - kEpiWarp0;
+    const int q = warp & 3;       // TMEM lane quarter this warp may access
+    const int half = e >> 2;
+    const int n_local = q * 32 + lane;
+    float* sa = sm.sa[e];
+    uint32_t g_it = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int n0 = (tile / p.m_tiles) * kTileN;
+      const int m0 = (tile % p.m_tiles) * BT;
+      const int n = n0 + n_local;
+      const int mc0 = m0 + half * COLS;
+      float acc[COLS];
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) acc[j] = 0.0f;
+      for (int t = 0; t < G; ++t, ++g_it) {
+        const uint32_t b = g_it & 1, bph = (g_it >> 1) & 1;
+        const bool int4 = t < G4;
+        for (int j = lane; j < COLS; j += 32) {
+          const int m = mc0 + j;
+          sa[j] = (m < p.M) ? __ldg(p.a_scales + static_cast<int64_t>(t) * p.M + m) : 0.0f;
+        }
+        float sw = __ldg(p.w_scales + static_cast<int64_t>(t) * p.N + n);
+        if (int4) sw *= (1.0f / 256.0f);  // undo the 16*16 operand pre-scaling (exact)
+        __syncwarp();
+        mbar_wait(&sm.tfull[b], bph);
+        tc_fence_after();
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * BT + half * COLS;
+#pragma unroll
+        for (int ch = 0; ch < COLS / 16; ++ch) {
+          uint32_t r[16];
+          tmem_ld16(taddr + ch * 16, r);
+          tmem_ld_wait();
+          if (ch == COLS / 16 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.tempty[b]);
+          }
+          if (p.debug != nullptr) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int m = mc0 + ch * 16 + k;
+              const int v = static_cast<int>(r[k]);
+              if (m < p.M)
+                p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const float scale = sw * sa[ch * 16 + k];
+            acc[ch * 16 + k] = fmaf(scale, __int2float_rn(static_cast<int>(r[k])), acc[ch * 16 + k]);
+          }
+        }
+        __syncwarp();
+      }
+      // ---- tile output ----
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) {
+        const int m = mc0 + j;
+        if (m < p.M) {
+          if (p.c_f32)
+            static_cast<float*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = acc[j];
+          else
+            static_cast<__half*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = __float2half_rn(acc[j]);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side: tensor maps + launch
+// ---------------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+  }
+  return fn;
+}
+
+// 2D uint8 tensor [rows][cols] (row stride = cols bytes), box [box_rows][64 bytes].
+static bool make_map_u8(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                        uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BT>
+static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms) {
+  const int M = static_cast<int>(a.M), N = static_cast<int>(a.N), K = static_cast<int>(a.K);
+  const int k_o = a.k_outlier;
+  const uint64_t kp = static_cast<uint64_t>(K - k_o) / 2;
+  CUtensorMap m_wq4, m_aq4, m_wq8, m_aq8;
+  // A map is always encoded (a valid descriptor is required as a kernel parameter); the unused
+  // INT4 or INT8 maps alias the other operand and are never read.
+  const void* w4 = kp ? static_cast<const void*>(a.w_q4) : static_cast<const void*>(a.w_q8);
+  const void* a4 = kp ? static_cast<const void*>(a.a_q4) : static_cast<const void*>(a.a_q8);
+  const void* w8 = k_o ? static_cast<const void*>(a.w_q8) : static_cast<const void*>(a.w_q4);
+  const void* a8 = k_o ? static_cast<const void*>(a.a_q8) : static_cast<const void*>(a.a_q4);
+  const uint64_t c4 = kp ? kp : 128, c8 = k_o ? 128 : kp;
+  if (!make_map_u8(&m_wq4, w4, c4, N, kTileN) || !make_map_u8(&m_aq4, a4, c4, M, BT) ||
+      !make_map_u8(&m_wq8, w8, c8, N, kTileN) || !make_map_u8(&m_aq8, a8, c8, M, BT))
+    return cudaErrorInvalidValue;
+
+  GemmParams p;
+  p.a_scales = a.a_scales;
+  p.w_scales = a.w_scales;
+  p.c = a.c;
+  p.ldc = a.ldc;
+  p.debug = a.debug_partials;
+  p.M = M;
+  p.N = N;
+  p.G = K / 128;
+  p.G4 = (K - k_o) / 128;
+  p.k_o = k_o;
+  p.c_f32 = a.c_f32;
+  p.m_tiles = (M + BT - 1) / BT;
+  p.num_tiles = p.m_tiles * (N / kTileN);
+
+  const size_t smem = sizeof(GemmSmem<BT>) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(w4a4_gemm_kernel<BT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+  w4a4_gemm_kernel<BT><<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_w4a4_gemm(const GemmArgs& a, cudaStream_t stream, int num_sms,
+                             int* launches) {
+  *launches = 0;
+  if (a.M == 0) return cudaSuccess;
+  const int64_t n_tiles = a.N / kTileN;
+  auto tiles = [&](int bt) { return n_tiles * ((a.M + bt - 1) / bt); };
+  cudaError_t e;
+  if (tiles(128) >= num_sms) e = launch_bt<128>(a, stream, num_sms);
+  else if (tiles(64) >= num_sms) e = launch_bt<64>(a, stream, num_sms);
+  else e = launch_bt<32>(a, stream, num_sms);
+  if (e == cudaSuccess) *launches = 1;
+  return e;
+}
+
+}  // namespace atom

@@ -1,0 +1,37 @@
+// internal.h -- launchers shared between the kernel translation units and the C-ABI layer.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace atom {
+
+cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip4, float clip8, uint8_t* q4, int8_t* q8,
+                                    float* scales, cudaStream_t stream, int num_sms);
+
+cudaError_t launch_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
+                                 int32_t* ok, cudaStream_t stream);
+
+struct GemmArgs {
+  const uint8_t* a_q4;
+  const int8_t* a_q8;
+  const float* a_scales;
+  const uint8_t* w_q4;
+  const int8_t* w_q8;
+  const float* w_scales;
+  int64_t M, N, K;
+  int32_t k_outlier;
+  void* c;
+  int64_t ldc;
+  int c_f32;
+  int32_t* debug_partials;
+};
+
+// Returns the number of kernel launches issued through *launches.
+cudaError_t launch_w4a4_gemm(const GemmArgs& a, cudaStream_t stream, int num_sms,
+                             int* launches);
+
+}  // namespace atom

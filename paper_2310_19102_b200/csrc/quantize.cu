@@ -1,0 +1,157 @@
+// quantize.cu -- a0/a1: fused channel reorder + dynamic symmetric quantization (sm_100a).
+//
+// Paper: reorder activations by the offline calibration index so the outlier channels sit at the
+// tail (Fig 4), keep the last 128 reordered channels in INT8, quantize the
+// rest to INT4 in groups of 128, with dynamically computed symmetric scales
+// s = 2*max|X|*c/(2^n-1) and codes clamp(round(X/s)).  The same kernel
+// quantizes weights offline (rows = output channels, clip 0.85).
+//
+// B200 design: HBM-bound gather.  One CTA per (row, group-chunk); the fp16 row is staged once in
+// shared memory with 128-bit streaming loads (coalesced), the gather x'[j] = x[perm[j]] then
+// reads shared memory.  One warp per 128-channel group: each lane owns 4 reordered channels
+// (one 128-bit perm load), the group |max| is a 5-step warp-shuffle reduction, codes are packed
+// in registers and written as 64 contiguous bytes per warp (INT4) or 128 bytes (INT8).
+// Numerics are pinned to the oracle's binary32 steps: __fdiv_rn / __fmul_rn / __frcp_rn are
+// IEEE round-to-nearest and never contracted; cvt.rni gives round-half-to-even.
+#include <cfloat>
+#include <cstdint>
+#include <cuda_fp16.h>
+
+#include "internal.h"
+
+namespace atom {
+
+constexpr int kQuantThreads = 256;
+constexpr int kQuantWarps = kQuantThreads / 32;
+
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ int quant_code(float x, float inv, int lo, int hi) {
+  int q = __float2int_rn(__fmul_rn(x, inv));  // single RN multiply, then round-half-even
+  return min(max(q, lo), hi);
+}
+
+__global__ void __launch_bounds__(kQuantThreads)
+reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
+                        const int32_t* __restrict__ perm, int32_t G, int32_t G4,
+                        int32_t groups_per_cta, float clip4, float clip8,
+                        uint8_t* __restrict__ q4, int8_t* __restrict__ q8,
+                        float* __restrict__ scales) {
+  extern __shared__ uint4 srow4[];
+  const __half* srow = reinterpret_cast<const __half*>(srow4);
+  const int64_t row = blockIdx.x;
+  const int g_begin = blockIdx.y * groups_per_cta;
+  const int g_end = min(G, g_begin + groups_per_cta);
+
+  // Stage the whole source row (the gather may touch any channel).
+  const uint4* src = reinterpret_cast<const uint4*>(x + row * ldx);
+  const int n16 = static_cast<int>(ldx / 8);
+  for (int i = threadIdx.x; i < n16; i += kQuantThreads) srow4[i] = ld_stream_u4(src + i);
+  __syncthreads();
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // alpha = fl(fl(2c) / (2^n - 1))
+  const float alpha4 = __fdiv_rn(__fmul_rn(2.0f, clip4), 15.0f);
+  const float alpha8 = __fdiv_rn(__fmul_rn(2.0f, clip8), 255.0f);
+  const int64_t row4 = static_cast<int64_t>(G4) * 64;
+
+  for (int t = g_begin + warp; t < g_end; t += kQuantWarps) {
+    const int4 p = __ldg(reinterpret_cast<const int4*>(perm + t * 128 + 4 * lane));
+    const float v0 = __half2float(srow[p.x]);
+    const float v1 = __half2float(srow[p.y]);
+    const float v2 = __half2float(srow[p.z]);
+    const float v3 = __half2float(srow[p.w]);
+    float amax = fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3)));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    const bool is_int4 = t < G4;
+    const float s = (amax == 0.0f) ? FLT_MIN : __fmul_rn(amax, is_int4 ? alpha4 : alpha8);
+    const float inv = __frcp_rn(s);
+    if (is_int4) {
+      const int c0 = quant_code(v0, inv, -8, 7), c1 = quant_code(v1, inv, -8, 7);
+      const int c2 = quant_code(v2, inv, -8, 7), c3 = quant_code(v3, inv, -8, 7);
+      const uint16_t packed = static_cast<uint16_t>((c0 & 0xF) | ((c1 & 0xF) << 4) |
+                                                    ((c2 & 0xF) << 8) | ((c3 & 0xF) << 12));
+      reinterpret_cast<uint16_t*>(q4 + row * row4 + t * 64)[lane] = packed;
+    } else {
+      const int c0 = quant_code(v0, inv, -128, 127), c1 = quant_code(v1, inv, -128, 127);
+      const int c2 = quant_code(v2, inv, -128, 127), c3 = quant_code(v3, inv, -128, 127);
+      const uint32_t packed = (c0 & 0xFF) | ((c1 & 0xFF) << 8) | ((c2 & 0xFF) << 16) |
+                              (static_cast<uint32_t>(c3 & 0xFF) << 24);
+      reinterpret_cast<uint32_t*>(q8 + row * 128)[lane] = packed;
+    }
+    if (lane == 0) scales[static_cast<int64_t>(t) * rows + row] = s;
+  }
+}
+
+cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip4, float clip8, uint8_t* q4, int8_t* q8,
+                                    float* scales, cudaStream_t stream, int num_sms) {
+  const int G = static_cast<int>(K / 128);
+  const int G4 = static_cast<int>((K - k_outlier) / 128);
+  // Enough CTAs to cover the SMs a few times over; each CTA re-stages the row from L2.
+  int splits = static_cast<int>((4LL * 2 * num_sms + rows - 1) / rows);
+  const int max_splits = (G + kQuantWarps - 1) / kQuantWarps;
+  splits = max(1, min(splits, max_splits));
+  const int gpc = (G + splits - 1) / splits;
+  splits = (G + gpc - 1) / gpc;
+  const size_t smem = static_cast<size_t>(ldx) * sizeof(__half);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(reorder_quantize_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
+  reorder_quantize_kernel<<<grid, kQuantThreads, smem, stream>>>(
+      static_cast<const __half*>(x), rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, scales);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// perm validation (test helper)
+// ---------------------------------------------------------------------------------------------
+__global__ void perm_count_kernel(const int32_t* perm, int64_t K, int64_t ldx, int32_t* counts,
+                                  int32_t* bad) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < K;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = perm[j];
+    if (p < 0 || p >= ldx) atomicOr(bad, 1);
+    else atomicAdd(counts + p, 1);
+  }
+}
+
+__global__ void perm_check_kernel(const int32_t* counts, int64_t K, int64_t ldx, int32_t* bad,
+                                  int32_t* ok) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = *bad;
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < ldx; c += blockDim.x) {
+    const int32_t n = counts[c];
+    if (n > 1 || (ldx == K && n != 1)) atomicOr(&any, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ok = any ? 0 : 1;
+}
+
+cudaError_t launch_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
+                                 int32_t* ok, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(int32_t) * ldx, stream);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ok, 0, sizeof(int32_t), stream);
+  if (e != cudaSuccess) return e;
+  perm_count_kernel<<<64, 256, 0, stream>>>(perm, K, ldx, scratch, ok);
+  // `ok` doubles as the `bad` accumulator until the check kernel overwrites it.
+  perm_check_kernel<<<1, 1024, 0, stream>>>(scratch, K, ldx, ok, ok);
+  return cudaGetLastError();
+}
+
+}  // namespace atom

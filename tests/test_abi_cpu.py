@@ -1,0 +1,92 @@
+"""CPU-side checks of the C ABI: the library builds for sm_100a, loads, exports every symbol that
+include/atom.h declares, and its host-side validation rejects bad arguments before touching a
+device (no compute call is made here)."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2310_19102_b200 import build
+    build.build()
+    import paper_2310_19102_b200 as atom
+    return atom.load()
+
+
+def declared_symbols():
+    h = (ROOT / "include" / "atom.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:atom_status_t|size_t|const char\*|int)\s+(atom_\w+)\(",
+                                 h, re.M)))
+
+
+def test_header_declares_the_three_calls():
+    syms = declared_symbols()
+    for s in ("atom_reorder_quantize", "atom_quantize_weights", "atom_w4a4_gemm"):
+        assert s in syms
+
+
+def test_every_declared_symbol_exported(lib):
+    import paper_2310_19102_b200 as atom
+    syms = declared_symbols()
+    assert set(syms) == set(atom.ABI_SYMBOLS)
+    for s in syms:
+        assert hasattr(lib, s), s
+
+
+def test_sm100a_only_cubin():
+    import subprocess
+    so = ROOT / "paper_2310_19102_b200" / "libatom.so"
+    out = subprocess.run(["cuobjdump", "--list-elf", str(so)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out and "sm_90" not in out
+    sass = subprocess.run(["cuobjdump", "-sass", str(so)], capture_output=True, text=True).stdout
+    assert "UTCIMMA" in sass       # tcgen05.mma kind::i8
+    assert "UTMALDG" in sass       # TMA tile loads
+    assert "LDTM" in sass          # tcgen05.ld
+
+
+def test_version_and_status_strings(lib):
+    assert lib.atom_abi_version() == 1
+    for s in range(8):
+        assert lib.atom_status_string(s).startswith(b"ATOM_")
+
+
+def test_host_validation_without_device(lib):
+    f = ctypes.c_float
+    # shape / argument errors are detected before any device query
+    assert lib.atom_reorder_quantize(None, -1, 256, None, 256, 128, f(0.9), f(1.0), None, None,
+                                     None, None) == 2
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 200, 128, f(0.9), f(1.0), None, None,
+                                     None, None) == 2
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 64, f(0.9), f(1.0), None, None,
+                                     None, None) == 4
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(1.5), f(1.0), None, None,
+                                     None, None) == 4
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(0.9), f(1.0), None, None,
+                                     None, None) == 1
+    assert lib.atom_quantize_weights(None, 4, 250, None, 256, 128, f(0.85), f(1.0), None, None,
+                                     None, None) == 2
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 4, 100, 256, 128, None, 128, 0,
+                              None, None, 0, None) == 2
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 4, 128, 256, 128, None, 128, 3,
+                              None, None, 0, None) == 4
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 4, 128, 256, 128, None, 128, 0,
+                              None, None, 0, None) == 1
+    assert lib.atom_w4a4_gemm_workspace_size(1024, 28672, 8192, 128) == 0
+    # M == 0 is a no-op that succeeds without a device
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
+                              None, None, 0, None) == 0
+    assert lib.atom_last_launch_count() == 0
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = ROOT / "paper_2310_19102_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + \
+            list(pkg.rglob("*.h")):
+        txt = f.read_text()
+        assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("oracle/", ""), f

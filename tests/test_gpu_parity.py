@@ -1,0 +1,370 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bars (BASELINE north_star): packed INT4/INT8 codes, scales and per-group int32 partials
+bit-exact; fp16 output within 2^-10 absolute + 1e-3 relative of the oracle's double result.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 2.0 ** -10, 1e-3
+
+
+@pytest.fixture(scope="module")
+def atom():
+    import torch
+    import paper_2310_19102_b200 as atom
+    from paper_2310_19102_b200 import build
+    build.build()
+    atom.load()
+    torch.cuda.init()
+    return atom
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return None if t is None else t.cpu().numpy()
+
+
+def assert_close_tol(c_gpu, c_ref, what=""):
+    c = c_gpu.astype(np.float64)
+    err = np.abs(c - c_ref)
+    tol = ATOL + RTOL * np.abs(c_ref)
+    bad = err > tol
+    assert not bad.any(), (f"{what}: {bad.sum()} outputs out of tolerance, max err/tol "
+                           f"{np.max(err / tol):.3f}")
+    return float(np.max(err / tol))
+
+
+def quant_both(atom, x, perm, K, k_o, clip4, weights=False):
+    fn = atom.quantize_weights if weights else atom.reorder_quantize
+    q = fn(dev(x), dev(perm), K=K, k_outlier=k_o, clip_int4=clip4)
+    o4, o8, osc = oracle.quantize_rows(x, perm, K, k_o, clip4, 1.0)
+    return q, (o4, o8, osc)
+
+
+def assert_quant_equal(q, ref):
+    o4, o8, osc = ref
+    if o4.size:
+        np.testing.assert_array_equal(host(q.q4), o4)
+    if o8 is not None:
+        np.testing.assert_array_equal(host(q.q8), o8)
+    got = host(q.scales)
+    np.testing.assert_array_equal(got.view(np.uint32), osc.view(np.uint32))
+
+
+# ----------------------------------------------------------------------------------------------
+# a1 / a0: reorder + quantize, bit-exact
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("K", [1024, 4096, 5120, 8192, 11008])
+@pytest.mark.parametrize("M", [1, 7, 8, 127, 128, 129, 256])
+def test_reorder_quantize_bitexact(atom, M, K):
+    x = synth.activations(M, K, seed=M + K)
+    perm = synth.perm_for(K, seed=M + K)
+    q, ref = quant_both(atom, x, perm, K, 128, 0.9)
+    assert_quant_equal(q, ref)
+
+
+@pytest.mark.parametrize("k_o", [0, 128])
+@pytest.mark.parametrize("clip4", [0.9, 0.85, 1.0, 0.5])
+def test_quantize_weights_bitexact(atom, k_o, clip4):
+    N, K = 384, 1024
+    w = synth.weights(N, K, seed=3)
+    perm = synth.perm_for(K, seed=3, n_outliers=k_o)
+    q, ref = quant_both(atom, w, perm, K, k_o, clip4, weights=True)
+    assert_quant_equal(q, ref)
+
+
+def test_quantize_11008_down_proj(atom):
+    M, K = 64, 11008
+    K = 11008                     # 86 groups
+    x = synth.activations(M, K, seed=5)
+    perm = synth.perm_for(K, seed=5)
+    q, ref = quant_both(atom, x, perm, K, 128, 0.9)
+    assert_quant_equal(q, ref)
+
+
+def adversarial_rows(K):
+    rows = []
+    z = np.zeros(K, np.float16)
+    rows.append(z.copy())                                     # all-zero row
+    r = z.copy(); r[::128] = 3.0; rows.append(r)              # single nonzero per group
+    r = np.full(K, 65504, np.float16); r[1::2] = -65504; rows.append(r)   # fp16 extremes
+    rows.append(np.full(K, np.float16(2.0 ** -24)))           # fp16 subnormal
+    r = z.copy(); r[7] = -5.0; rows.append(r)                 # negative group max
+    # exact .5 ties with clip = 1: x = 7.5 s and 127.5 s  (s = 1)
+    r = z.copy(); r[:K - 128] = np.tile(np.array([7.5, -7.5, 6.5, -6.5, 0.5, -0.5, 1.5, -2.5],
+                                                 np.float16), (K - 128) // 8)
+    r[K - 128:] = np.tile(np.array([127.5, -127.5, 0.5, -1.5], np.float16), 32)
+    rows.append(r)
+    rng = np.random.default_rng(0)
+    rows.append((rng.standard_normal(K) * 1e-4).astype(np.float16))   # tiny values
+    rows.append((rng.standard_normal(K) * 3e3).astype(np.float16))    # large values
+    return np.stack(rows)
+
+
+@pytest.mark.parametrize("clip4,clip8", [(0.9, 1.0), (1.0, 1.0)])
+@pytest.mark.parametrize("perm_kind", ["identity", "reversal", "calibrated"])
+def test_quantize_adversarial(atom, clip4, clip8, perm_kind):
+    K = 1024
+    x = adversarial_rows(K)
+    perm = {"identity": np.arange(K), "reversal": np.arange(K)[::-1],
+            "calibrated": synth.perm_for(K, 1)}[perm_kind].astype(np.int32)
+    q = atom.reorder_quantize(dev(x), dev(perm), K=K, k_outlier=128, clip_int4=clip4,
+                              clip_int8=clip8)
+    ref = oracle.quantize_rows(x, perm, K, 128, clip4, clip8)
+    assert_quant_equal(q, ref)
+
+
+def test_quantize_shard_slice(atom):
+    """K-shard: perm + k0, own K, k_outlier only on the tail shard; ldx > K."""
+    M, K = 33, 2048
+    x = synth.activations(M, K, seed=8)
+    perm = synth.perm_for(K, seed=8)
+    for k0, Ks, ko in [(0, 1024, 0), (1024, 1024, 128)]:
+        sl = np.ascontiguousarray(perm[k0:k0 + Ks])
+        q = atom.reorder_quantize(dev(x), dev(sl), K=Ks, k_outlier=ko)
+        assert_quant_equal(q, oracle.quantize_rows(x, sl, Ks, ko, 0.9, 1.0))
+
+
+def test_quantize_strided_rows(atom):
+    """ldx > K with a row-strided view."""
+    import torch
+    M, K, ld = 20, 1024, 1536
+    big = synth.activations(M, ld, seed=2)
+    perm = synth.perm_for(K, seed=2)
+    xt = dev(big)
+    q = atom.reorder_quantize(xt, dev(perm), K=K)
+    assert_quant_equal(q, oracle.quantize_rows(big, perm, K, 128, 0.9, 1.0))
+
+
+# ----------------------------------------------------------------------------------------------
+# a2-a5: GEMM -- exact partials (debug mode) and tolerance outputs
+# ----------------------------------------------------------------------------------------------
+def run_gemm(atom, X, W, perm, K, k_o, debug=False, out_dtype=None):
+    import torch
+    pd = dev(perm)
+    wq = atom.quantize_weights(dev(W), pd, K=K, k_outlier=k_o)
+    aq = atom.reorder_quantize(dev(X), pd, K=K, k_outlier=k_o)
+    dbg = torch.full((K // 128, X.shape[0], W.shape[0]), -7, dtype=torch.int32,
+                     device="cuda") if debug else None
+    c = atom.w4a4_gemm(aq, wq, debug_partials=dbg, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return aq, wq, c, dbg
+
+
+@pytest.mark.parametrize("M,N,K,k_o", [
+    (1, 128, 128, 128),      # single INT8 group (textbook W8A8)
+    (7, 128, 256, 128),
+    (16, 256, 1024, 128),    # config 1 geometry (N reduced)
+    (33, 128, 512, 0),       # pure INT4 (k_o = 0)
+    (100, 256, 384, 128),
+    (129, 128, 1024, 128),   # ragged token tail across two tiles
+    (256, 256, 1024, 128),
+    (300, 384, 640, 128),
+])
+def test_gemm_partials_bitexact(atom, M, N, K, k_o):
+    X, W, perm = synth.problem(M, N, K, seed=M * 7 + N, k_outlier=k_o)
+    aq, wq, c, dbg = run_gemm(atom, X, W, perm, K, k_o, debug=True)
+    ref = oracle.quantized_linear(X, perm, W, K, k_o)
+    np.testing.assert_array_equal(host(dbg), ref["partials"])
+    assert_close_tol(host(c.float()), ref["c"], "C")
+
+
+@pytest.mark.parametrize("M", [1, 8, 16, 31, 64, 127, 128, 129, 256, 513])
+def test_gemm_output_config1_family(atom, M):
+    N, K = 1024, 1024
+    X, W, perm = synth.problem(M, N, K, seed=M)
+    _, _, c, _ = run_gemm(atom, X, W, perm, K, 128)
+    ref = oracle.quantized_linear(X, perm, W, K)
+    assert_close_tol(host(c.float()), ref["c"], f"M={M}")
+
+
+def test_gemm_unit_scale_exact_integer(atom):
+    """P3 on the GPU: clip 1 and integer-valued groups -> C is the exact integer GEMM."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).parent))
+    from test_oracle_pins import scatter, unit_scale_block
+    rng = np.random.default_rng(1)
+    M, N, K = 40, 256, 1024
+    perm = rng.permutation(K).astype(np.int32)
+    av, ac = unit_scale_block(rng, M, K, 128)
+    wv, wc = unit_scale_block(rng, N, K, 128)
+    X, W = scatter(av, perm).astype(np.float16), scatter(wv, perm).astype(np.float16)
+    pd = dev(perm)
+    wq = atom.quantize_weights(dev(W), pd, clip_int4=1.0)
+    aq = atom.reorder_quantize(dev(X), pd, clip_int4=1.0)
+    c = atom.w4a4_gemm(aq, wq, out_dtype=__import__("torch").float32)
+    exact = (ac @ wc.T).astype(np.float64)
+    assert np.abs(exact).max() < 2 ** 24
+    np.testing.assert_array_equal(host(c).astype(np.float64), exact)
+
+
+def test_gemm_fp32_output(atom):
+    import torch
+    M, N, K = 64, 256, 1024
+    X, W, perm = synth.problem(M, N, K, seed=4)
+    _, _, c, _ = run_gemm(atom, X, W, perm, K, 128, out_dtype=torch.float32)
+    ref = oracle.quantized_linear(X, perm, W, K)
+    # fp32 output: only accumulation-order error
+    np.testing.assert_allclose(host(c), ref["c"], rtol=1e-5, atol=1e-5)
+
+
+CONFIGS = {
+    "cfg2_7b_qkvo": (256, 4096, 4096),
+    "cfg3_up_m8": (8, 11008, 4096),
+    "cfg3_up_m64": (64, 11008, 4096),
+    "cfg3_up_m256": (256, 11008, 4096),
+    "cfg3_down_m256": (256, 4096, 11008),
+    "cfg3_up_m1024": (1024, 11008, 4096),
+    "cfg4_13b": (512, 13824, 5120),
+    "cfg5_70b_mlp": (1024, 28672, 8192),
+}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_gemm_baseline_configs_sampled(atom, name):
+    """Full BASELINE sizes in the launch configuration bench.py times: codes and scales in full,
+    C on a deterministic row sample (first, last and 14 random rows) against the oracle."""
+    M, N, K = CONFIGS[name]
+    X, W, perm = synth.problem(M, N, K, seed=0)
+    pd = dev(perm)
+    wq = atom.quantize_weights(dev(W), pd)
+    aq = atom.reorder_quantize(dev(X), pd)
+    c = atom.w4a4_gemm(aq, wq)
+    w4, w8, ws = oracle.quantize_rows(W, perm, K, 128, 0.85, 1.0)
+    a4, a8, as_ = oracle.quantize_rows(X, perm, K, 128, 0.9, 1.0)
+    assert_quant_equal(wq, (w4, w8, ws))
+    assert_quant_equal(aq, (a4, a8, as_))
+    rng = np.random.default_rng(123)
+    rows = np.unique(np.concatenate([[0, M - 1], rng.integers(0, M, size=min(14, M))]))
+    ref = oracle.output_rows(a4, a8, as_, w4, w8, ws, M, N, K, 128, rows)
+    assert_close_tol(host(c.float())[rows], ref, name)
+
+
+# ----------------------------------------------------------------------------------------------
+# tensor-parallel shard algebra on one device (the "fake backend" of SURVEY §4 T3)
+# ----------------------------------------------------------------------------------------------
+def test_n_shard_bit_identical(atom):
+    import torch
+    M, N, K, P = 96, 1024, 2048, 4
+    X, W, perm = synth.problem(M, N, K, seed=6)
+    pd = dev(perm)
+    aq = atom.reorder_quantize(dev(X), pd)
+    full = atom.w4a4_gemm(aq, atom.quantize_weights(dev(W), pd))
+    out = torch.empty((M, N), dtype=torch.float16, device="cuda")
+    for r in range(P):
+        sl = slice(r * N // P, (r + 1) * N // P)
+        wq = atom.quantize_weights(dev(W[sl]), pd)
+        atom.w4a4_gemm(aq, wq, out=out[:, sl])
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
+
+
+def test_k_shard_partials_and_sum(atom):
+    import torch
+    M, N, K, P = 64, 512, 2048, 2
+    X, W, perm = synth.problem(M, N, K, seed=7)
+    ref = oracle.quantized_linear(X, perm, W, K)
+    G = K // 128
+    acc = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+    for r in range(P):
+        g0, g1 = r * G // P, (r + 1) * G // P
+        sl = np.ascontiguousarray(perm[g0 * 128:g1 * 128])
+        ko = 128 if r == P - 1 else 0
+        Ks = (g1 - g0) * 128
+        pd = dev(sl)
+        aq = atom.reorder_quantize(dev(X), pd, K=Ks, k_outlier=ko)
+        wq = atom.quantize_weights(dev(W), pd, K=Ks, k_outlier=ko)
+        dbg = torch.empty((g1 - g0, M, N), dtype=torch.int32, device="cuda")
+        part = atom.w4a4_gemm(aq, wq, out_dtype=torch.float32, debug_partials=dbg)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(host(dbg), ref["partials"][g0:g1])
+        acc += part
+    assert_close_tol(host(acc.half().float()), ref["c"], "K-shard sum")
+
+
+# ----------------------------------------------------------------------------------------------
+# ABI behaviour on the device
+# ----------------------------------------------------------------------------------------------
+def test_validate_perm(atom):
+    import torch
+    K = 1024
+    assert atom.validate_perm(dev(synth.perm_for(K, 0)))
+    bad = synth.perm_for(K, 0).copy()
+    bad[3] = bad[4]
+    assert not atom.validate_perm(dev(bad))
+    assert atom.validate_perm(dev(np.arange(0, 2 * K, 2, dtype=np.int32)), ldx=2 * K)
+
+
+def test_non_default_stream(atom):
+    import torch
+    M, N, K = 64, 256, 1024
+    X, W, perm = synth.problem(M, N, K, seed=10)
+    ref = oracle.quantized_linear(X, perm, W, K)
+    s = torch.cuda.Stream()
+    xd, wd, pd = dev(X), dev(W), dev(perm)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        wq = atom.quantize_weights(wd, pd, stream=s)
+        aq = atom.reorder_quantize(xd, pd, stream=s)
+        c = atom.w4a4_gemm(aq, wq, stream=s)
+    s.synchronize()
+    assert_close_tol(host(c.float()), ref["c"], "stream")
+
+
+def test_error_codes_launch_nothing(atom):
+    import ctypes
+    import torch
+    L = atom.load()
+    x = torch.zeros((4, 256), dtype=torch.float16, device="cuda")
+    perm = torch.arange(256, dtype=torch.int32, device="cuda")
+    q4 = torch.full((4, 64), 0xAB, dtype=torch.uint8, device="cuda")
+    q8 = torch.full((4, 128), 5, dtype=torch.int8, device="cuda")
+    sc = torch.full((2, 4), 3.0, dtype=torch.float32, device="cuda")
+    f = ctypes.c_float
+    cases = [
+        (2, (x.data_ptr(), 4, 256, perm.data_ptr(), 200, 128, f(0.9), f(1.0))),   # K % 128
+        (4, (x.data_ptr(), 4, 256, perm.data_ptr(), 256, 64, f(0.9), f(1.0))),    # k_o
+        (4, (x.data_ptr(), 4, 256, perm.data_ptr(), 256, 128, f(0.0), f(1.0))),   # clip
+        (1, (None, 4, 256, perm.data_ptr(), 256, 128, f(0.9), f(1.0))),           # null x
+        (3, (x.data_ptr() + 2, 4, 256, perm.data_ptr(), 256, 128, f(0.9), f(1.0))),  # misaligned
+    ]
+    for want, args in cases:
+        st = L.atom_reorder_quantize(*args, q4.data_ptr(), q8.data_ptr(), sc.data_ptr(), None)
+        assert st == want, (want, st)
+        assert atom.last_launch_count() == 0
+    torch.cuda.synchronize()
+    assert torch.all(q4 == 0xAB) and torch.all(q8 == 5) and torch.all(sc == 3.0)
+    # GEMM: N % 128, ldc < N, bad dtype
+    args = [q4.data_ptr(), q8.data_ptr(), sc.data_ptr(), q4.data_ptr(), q8.data_ptr(),
+            sc.data_ptr()]
+    out = torch.zeros((4, 256), dtype=torch.float16, device="cuda")
+    assert L.atom_w4a4_gemm(*args, 4, 200, 256, 128, out.data_ptr(), 256, 0, None, None, 0,
+                            None) == 2
+    assert L.atom_w4a4_gemm(*args, 4, 256, 256, 128, out.data_ptr(), 128, 0, None, None, 0,
+                            None) == 2
+    assert L.atom_w4a4_gemm(*args, 4, 128, 256, 128, out.data_ptr(), 256, 5, None, None, 0,
+                            None) == 4
+    assert L.atom_w4a4_gemm(*args, 4, 128, 256, 0, out.data_ptr(), 256, 0, None, None, 0,
+                            None) == 1     # k_o = 0 but q8 pointers given
+    torch.cuda.synchronize()
+    assert torch.all(out == 0)
+
+
+def test_empty_m_is_noop(atom):
+    import torch
+    L = atom.load()
+    assert L.atom_reorder_quantize(None, 0, 256, None, 256, 128, 0.9, 1.0, None, None, None,
+                                   None) == 0
+    assert L.atom_w4a4_gemm(None, None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
+                            None, None, 0, None) == 0
