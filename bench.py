@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""Benchmark of the Atom W4A4 hot path on B200 (one JSON line on rank 0).
+
+A step = one pass of the whole hot path over one batch: a1 atom_reorder_quantize of the
+activations + a2-a5 atom_w4a4_gemm (+ the tensor-parallel collective when N > 1).  Weights are
+quantized once, offline (a0), outside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--shard n|k]
+  python bench.py --impl reference ...     # the CPU oracle as the reference arm
+
+Metric (BASELINE.json): W4A4 mixed GEMM effective TOPS = 2*M*N*K / t_step, K counting the 128
+outlier channels.  Multi-GPU (torchrun, one rank per GPU, NCCL): tensor parallel, N-shard
+(all-gather of fp16 column blocks) or K-shard (all-reduce of fp32 partials), strong scaling;
+time = max over ranks of the device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import synth  # noqa: E402
+
+CONFIGS = {
+    # name: (M tokens, N out features, K in features incl. 128 outliers, description)
+    "cfg1": (16, 1024, 1024, "single W4A4 linear, M=16, K=1024, N=1024"),
+    "cfg2": (256, 4096, 4096, "Llama-7B q/k/v/o projection, M=256, K=N=4096"),
+    "cfg3_up": (1024, 11008, 4096, "Llama-7B MLP up/gate, M=1024, K=4096, N=11008"),
+    "cfg3_down": (1024, 4096, 11008, "Llama-7B MLP down, M=1024, K=11008, N=4096"),
+    "cfg4": (512, 13824, 5120, "Llama-13B linear, M=512, K=5120, N=13824"),
+    "cfg5": (1024, 28672, 8192, "Llama-70B MLP, M=1024, K=8192, N=28672"),
+}
+METRIC = "W4A4 mixed GEMM effective TOPS and % roofline at Llama-7B/70B shapes, 1/2/4/8 B200"
+UNIT = "TOPS"
+K_OUT = 128
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def algorithmic_bytes(M, N, K, c_bytes=2):
+    """Bytes the method must move: packed W + packed A (INT4 + INT8 + fp32
+    scales) + C."""
+    per_row = (K - K_OUT) // 2 + K_OUT + (K // 128) * 4
+    return N * per_row + M * per_row + M * N * c_bytes
+
+
+def quant_bytes(M, K):
+    per_row = (K - K_OUT) // 2 + K_OUT + (K // 128) * 4
+    return M * K * 2 + K * 4 + M * per_row
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks (NVML, sampled during the timed region)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle baseline (bounded sample)
+# ------------------------------------------------------------------------------------------------
+def oracle_setup(M, N, K, seed=0):
+    import oracle
+    X, perm = synth.activations(M, K, seed), synth.perm_for(K, seed)
+    W = synth.weights(N, K, seed)
+    w4, w8, ws = oracle.quantize_rows(W, perm, K, K_OUT, 0.85, 1.0)      # offline (a0), untimed
+    return X, perm, (w4, w8, ws)
+
+
+def oracle_step(X, perm, wpack, N, K, rows):
+    """One oracle step on a sample of token rows: a1 quantize + a2-a5 outputs for those rows."""
+    import oracle
+    a4, a8, as_ = oracle.quantize_rows(X[rows], perm, K, K_OUT, 0.9, 1.0)
+    w4, w8, ws = wpack
+    return oracle.output_rows(a4, a8, as_, w4, w8, ws, len(rows), N, K, K_OUT,
+                              np.arange(len(rows)))
+
+
+def cpu_baseline(M, N, K, target_s=12.0, setup=None):
+    import oracle
+    X, perm, wpack = setup if setup is not None else oracle_setup(M, N, K)
+    cores = oracle.max_threads()
+    # calibrate on a small sample, then size the sample to ~target_s
+    t0 = time.perf_counter()
+    oracle_step(X, perm, wpack, N, K, np.arange(min(2, M)))
+    dt = (time.perf_counter() - t0) / min(2, M)
+    R = int(max(1, min(M, target_s / max(dt, 1e-6))))
+    R = max(cores, (R // cores) * cores) if R >= cores else R
+    R = min(R, M)
+    rows = np.linspace(0, M - 1, R).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle_step(X, perm, wpack, N, K, rows)
+    t = time.perf_counter() - t0
+    return {"value": 2.0 * R * N * K / t / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{R} of {M} token rows of the workload (quantize those rows + their full "
+                      f"output rows, N={N}, K={K}); {t:.2f} s on {cores} host threads"}
+
+
+# ------------------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands
+# ------------------------------------------------------------------------------------------------
+def run_reference(args, M, N, K, cfg_name, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    setup = oracle_setup(M, N, K)
+    X, perm, wpack = setup
+    cores = oracle.max_threads()
+    t0 = time.perf_counter()
+    oracle_step(X, perm, wpack, N, K, np.arange(1))
+    t_row = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.steps + args.warmup)      # whole run within a few minutes
+    R = int(max(1, min(M, budget / max(t_row, 1e-6))))
+    rows_all = [np.sort(np.random.default_rng(i).choice(M, R, replace=False))
+                for i in range(args.steps + args.warmup)]
+    for i in range(args.warmup):
+        oracle_step(X, perm, wpack, N, K, rows_all[i])
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        oracle_step(X, perm, wpack, N, K, rows_all[args.warmup + i])
+        times.append(time.perf_counter() - t0)
+    step_s = sum(times) / len(times)
+    value = 2.0 * R * N * K / step_s / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (synth/: Llama-like activations with 128 x100 outlier channels, "
+                "N(0,0.02^2) weights, seed 0)",
+        "config": {"workload": cfg_name, "M": M, "N": N, "K": K, "k_outlier": K_OUT,
+                   "group": 128, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"each step: {R} random token rows of {M} (quantize + full "
+                                   f"output rows), N={N}, K={K}, {cores} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# the CUDA path
+# ------------------------------------------------------------------------------------------------
+def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_19102_b200 as atom
+    from paper_2310_19102_b200 import build
+    if rank == 0 or not (ROOT / "paper_2310_19102_b200" / "libatom.so").exists():
+        build.build()
+    if world > 1:
+        dist.barrier()
+    atom.load()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    P, shard = world, args.shard
+    G = K // 128
+
+    # ---------------- inputs (synthetic, seeded; identical bytes on every rank) ----------------
+    X = synth.activations(M, K, args.seed)
+    perm = synth.perm_for(K, args.seed)
+    if shard == "n":
+        n0, n1 = rank * N // P, (rank + 1) * N // P
+        assert (n1 - n0) % 128 == 0, "N-shard must be a multiple of 128 columns"
+        W = synth.weights(N, K, args.seed, rows=(n0, n1))
+        perm_r, K_r, ko_r = perm, K, K_OUT
+        Wd = torch.from_numpy(W).to(dev)
+    else:  # K-shard along group boundaries; INT8 outlier group on the last rank
+        g0, g1 = rank * G // P, (rank + 1) * G // P
+        perm_r = np.ascontiguousarray(perm[g0 * 128:g1 * 128])
+        K_r, ko_r = (g1 - g0) * 128, (K_OUT if rank == P - 1 else 0)
+        W = synth.weights(N, K, args.seed)
+        Wd = torch.from_numpy(W).to(dev)
+        n0, n1 = 0, N
+    Nr = n1 - n0
+    pd = torch.from_numpy(perm_r).to(dev)
+    xd = torch.from_numpy(X).to(dev)
+    wq = atom.quantize_weights(Wd, pd, K=K_r, k_outlier=ko_r)          # a0, offline
+    del Wd
+    aq = atom.reorder_quantize(xd, pd, K=K_r, k_outlier=ko_r)          # output buffers reused
+    if shard == "n":
+        c_loc = torch.empty((M, Nr), dtype=torch.float16, device=dev)
+        c_all = torch.empty((P, M, Nr), dtype=torch.float16, device=dev) if P > 1 else None
+    else:
+        c_loc = torch.empty((M, N), dtype=torch.float32, device=dev)
+        c_all = torch.empty((M, N), dtype=torch.float16, device=dev)
+    torch.cuda.synchronize()
+
+    launches = [0]
+
+    def step(x_in):
+        atom.reorder_quantize(x_in, pd, K=K_r, k_outlier=ko_r, out=aq)
+        launches[0] += atom.last_launch_count()
+        atom.w4a4_gemm(aq, wq, out=c_loc)
+        launches[0] += atom.last_launch_count()
+
+    def collective():
+        if P == 1:
+            return c_loc
+        if shard == "n":
+            dist.all_gather_into_tensor(c_all, c_loc)
+            return c_all
+        dist.all_reduce(c_loc)
+        c_all.copy_(c_loc)
+        return c_all
+
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(2 * l2 + (64 << 20), dtype=torch.uint8, device=dev)
+
+    def flush_l2():
+        flush.zero_()
+
+    # spin up clocks (untimed), then W warm-up steps
+    t_end = time.perf_counter() + args.spinup
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            step(xd)
+        torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        flush_l2()
+        step(xd)
+        collective()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: exactly K steps ----------------
+    E = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    launches[0] = 0
+    sampler = ClockSampler(torch.cuda.current_device())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for i in range(args.steps):
+            if not args.no_flush:
+                flush_l2()
+            E[i][0].record()
+            atom.reorder_quantize(xd, pd, K=K_r, k_outlier=ko_r, out=aq)
+            launches[0] += atom.last_launch_count()
+            E[i][1].record()
+            atom.w4a4_gemm(aq, wq, out=c_loc)
+            launches[0] += atom.last_launch_count()
+            E[i][2].record()
+            collective()
+            E[i][3].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [E[i][0].elapsed_time(E[i][3]) for i in range(args.steps)]
+    q_ms = [E[i][0].elapsed_time(E[i][1]) for i in range(args.steps)]
+    g_ms = [E[i][1].elapsed_time(E[i][2]) for i in range(args.steps)]
+    c_ms = [E[i][2].elapsed_time(E[i][3]) for i in range(args.steps)]
+    stats = torch.tensor([sum(step_ms) / args.steps, sum(q_ms) / args.steps,
+                          sum(g_ms) / args.steps, sum(c_ms) / args.steps], device=dev,
+                         dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    step_avg, q_avg, g_avg, c_avg = stats.tolist()
+    gpu_launches = launches[0]
+
+    # ---------------- e2e through the public API with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        x_h = torch.from_numpy(X).pin_memory()
+        out_shape = c_all.shape if (P > 1) else c_loc.shape
+        out_dtype = torch.float16
+        c_h = torch.empty(out_shape, dtype=out_dtype).pin_memory()
+        xin = torch.empty_like(xd)
+        EE = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        for i in range(max(1, args.warmup)):
+            xin.copy_(x_h, non_blocking=True)
+            step(xin)
+            c = collective()
+            c_h.copy_(c if c.dtype == out_dtype else c.half(), non_blocking=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            if not args.no_flush:
+                flush_l2()
+            EE[i][0].record()
+            xin.copy_(x_h, non_blocking=True)
+            step(xin)
+            c = collective()
+            c_h.copy_(c if c.dtype == out_dtype else c.half(), non_blocking=True)
+            EE[i][1].record()
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([sum(EE[i][0].elapsed_time(EE[i][1]) for i in range(args.steps))
+                             / args.steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        e2e = {"value": 2.0 * M * N * K / (e_ms * 1e-3) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int(P * X.nbytes),
+               "d2h_bytes_per_step": int(P * c_h.numel() * c_h.element_size()),
+               "ms_per_step": e_ms}
+
+    if rank != 0:
+        return
+    peaks, peak_src = load_peaks()
+    ops = 2.0 * M * N * K
+    value = ops / (step_avg * 1e-3) / 1e12
+    # dominant kernel: the GEMM (int8 tensor-core contraction).  Peak for its own dtype: the
+    # measured bf16 burst peak x the nominal int8/bf16 ratio (4.5 / 2.25 = 2).
+    gemm_ops_launch = 2.0 * M * Nr * K_r
+    achieved = gemm_ops_launch / (g_avg * 1e-3) / 1e12
+    peak_int8 = 2.0 * peaks["bf16_tflops"]
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(f"{cfg_name}:gemm:P{P}{shard}")
+    t_roof_spec = max(2.0 * M * Nr * K_r / 4.5e15, algorithmic_bytes(M, Nr, K_r) / 8e12)
+    qb = quant_bytes(M, K_r)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_avg, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (synth/: Llama-like activations with 128 x100 outlier channels, "
+                "N(0,0.02^2) weights, seed 0)",
+        "config": {"workload": cfg_name, "desc": CONFIGS[cfg_name][3], "M": M, "N": N, "K": K,
+                   "k_outlier": K_OUT, "group": 128,
+                   "parallelism": "single" if P == 1 else f"tp{P}-{shard}shard",
+                   "l2": "flushed before every timed step (write of 2xL2+64MiB)"
+                         if not args.no_flush else "warm"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_int8,
+                     "unit": "TFLOP/s", "frac": achieved / peak_int8, "traffic": traffic,
+                     "kernel": "atom::w4a4_gemm_kernel",
+                     "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} x 2 "
+                                    f"(int8/bf16 nominal ratio)"},
+        "roofline_spec": {"t_roof_us": t_roof_spec * 1e6, "t_gemm_us": g_avg * 1e3,
+                          "frac": t_roof_spec / (g_avg * 1e-3),
+                          "model": "max(2MNK/4.5e15, bytes/8e12) per GPU (BASELINE.json)"},
+        "kernels": {
+            "reorder_quantize": {"us": q_avg * 1e3, "GB/s": qb / (q_avg * 1e-3) / 1e9,
+                                 "frac_hbm": qb / (q_avg * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "w4a4_gemm": {"us": g_avg * 1e3, "TOPS": achieved},
+            "collective": {"us": c_avg * 1e3},
+        },
+        "gpu_launches": gpu_launches,
+        "clocks": sampler.summary(),
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(M, N, K, target_s=args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["atom", "reference"], default="atom")
+    ap.add_argument("--config", choices=list(CONFIGS), default="cfg5")
+    ap.add_argument("--shard", choices=["n", "k"], default="n")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--spinup", type=float, default=0.5, help="seconds of untimed clock spin-up")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    M, N, K, _ = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, M, N, K, args.config, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_atom(args, M, N, K, args.config, world, rank, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -44,10 +44,22 @@ def activations(M: int, K: int, seed: int, n_outliers: int = N_OUTLIERS,
     return x.astype(np.float16)
 
 
-def weights(N: int, K: int, seed: int, std: float = 0.02) -> np.ndarray:
-    """fp16 [N][K] random-init weights, N(0, std^2)."""
-    g = _rng(seed + 104729)
-    return (std * g.standard_normal((N, K))).astype(np.float16)
+W_BLOCK = 1024   # weight rows per independently seeded block
+
+
+def weights(N: int, K: int, seed: int, std: float = 0.02, rows: tuple | None = None) -> np.ndarray:
+    """fp16 [N][K] random-init weights, N(0, std^2).  Rows come in blocks of W_BLOCK, each from
+    its own PCG64 stream (SeedSequence([seed, block])), so a tensor-parallel rank can generate
+    exactly its row range ``rows = (r0, r1)`` of the same matrix without the rest."""
+    r0, r1 = (0, N) if rows is None else rows
+    out = np.empty((r1 - r0, K), dtype=np.float16)
+    for b in range(r0 // W_BLOCK, (r1 + W_BLOCK - 1) // W_BLOCK):
+        b0, b1 = b * W_BLOCK, min(N, (b + 1) * W_BLOCK)
+        g = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 104729, b])))
+        blk = (np.float32(std) * g.standard_normal((b1 - b0, K), dtype=np.float32))
+        lo, hi = max(b0, r0), min(b1, r1)
+        out[lo - r0:hi - r0] = blk[lo - b0:hi - b0].astype(np.float16)
+    return out
 
 
 def calibration_perm(calib: np.ndarray, n_outliers: int = N_OUTLIERS) -> np.ndarray:
