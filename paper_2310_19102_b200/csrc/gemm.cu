@@ -39,6 +39,13 @@ constexpr int kNumUnpackWarps = 4;
 constexpr int kEpiWarp0 = 6;    // warps 6..13
 constexpr int kNumEpiWarps = 8;
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
+constexpr int kSRing = 8;       // group-scale ring depth
+
+// The TMEM accumulator of every group starts from the int32 bit pattern of 1.5*2^23 (tcgen05.mma
+// always accumulates), so the MMA leaves float(1.5*2^23 + P) bit-exactly (|P| <= 2^21 < 2^22)
+// and the epilogue recovers P with one exact FADD instead of an int->float conversion.
+constexpr uint32_t kMagicBits = 0x4B400000u;
+constexpr float kMagic = 12582912.0f;
 
 struct GemmParams {
   const float* a_scales;
@@ -56,10 +63,12 @@ struct __align__(1024) GemmSmem {
   uint8_t ubuf_a[kUbuf][BT * 128];      // unpacked activation group, SW128 K-major
   uint8_t stage_w[kStages][kTileN * 64];// packed weight group (or half of the INT8 group)
   uint8_t stage_a[kStages][BT * 64];    // packed activation group
-  float sa[kNumEpiWarps][BT / 2];       // per-epilogue-warp staged activation scales
+  float ssw[kSRing][kTileN];             // weight scales of a group (ring, filled by cp.async)
+  float ssa[kSRing][BT];                 // activation scales of a group
   uint64_t full[kStages], empty[kStages];
   uint64_t ufull[kUbuf], uempty[kUbuf];
   uint64_t tfull[2], tempty[2];
+  uint64_t sready[kSRing], sfree[kSRing];
   uint32_t tmem_base;
 };
 
@@ -80,7 +89,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                  const __grid_constant__ CUtensorMap tm_aq8, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   GemmSmem<BT>& sm = *reinterpret_cast<GemmSmem<BT>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+      smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   constexpr uint32_t kTmemCols = tmem_cols<BT>();
@@ -97,6 +106,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.tfull[b], 1);
       mbar_init(&sm.tempty[b], kNumEpiWarps);
+    }
+    for (int r = 0; r < kSRing; ++r) {
+      mbar_init(&sm.sready[r], kNumUnpackWarps * 32);  // one cp.async-arrive per unpack thread
+      mbar_init(&sm.sfree[r], kNumEpiWarps);
     }
     fence_mbar_init();
   }
@@ -147,7 +160,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
           const uint32_t b = g_it & 1, bph = (g_it >> 1) & 1;
           mbar_wait(&sm.ufull[u], uph);
-          mbar_wait(&sm.tempty[b], bph ^ 1);
+          mbar_wait(&sm.tempty[b], bph);   // buffer drained AND re-filled with the magic
           tc_fence_after();
           const uint32_t d = tmem + b * BT;
           const uint32_t a_base = smem_u32(sm.ubuf_w[u]);
@@ -155,7 +168,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             umma_i8(d, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
-                    k > 0 ? 1u : 0u);
+                    1u);
           umma_commit(&sm.uempty[u]);
           umma_commit(&sm.tfull[b]);
         }
@@ -163,10 +176,26 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     }
   } else if (warp < kEpiWarp0) {
     // ===================== unpack warps: packed INT4 -> int8 (16*q), SW128 =====================
+    // They also stage each group's scales into the scale ring with cp.async (4-byte copies, any
+    // M), signalling sready through cp.async.mbarrier.arrive; the epilogue frees the slot.
     const int ut = threadIdx.x - kUnpackWarp0 * 32;  // 0..127
     uint32_t it = 0, g_it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int n0 = (tile / p.m_tiles) * kTileN;
+      const int m0 = (tile % p.m_tiles) * BT;
       for (int t = 0; t < G; ++t, ++g_it) {
+        {
+          const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
+          mbar_wait(&sm.sfree[sr], sph ^ 1);
+          cp_async_4(&sm.ssw[sr][ut], p.w_scales + static_cast<int64_t>(t) * p.N + n0 + ut);
+          for (int j = ut; j < BT; j += kNumUnpackWarps * 32) {
+            // rows past M: any finite scale works, their partials are exactly zero (TMA
+            // zero-fills out-of-range activation rows) and they are never stored
+            const int m = min(m0 + j, p.M - 1);
+            cp_async_4(&sm.ssa[sr][j], p.a_scales + static_cast<int64_t>(t) * p.M + m);
+          }
+          cp_async_mbar_arrive(&sm.sready[sr]);
+        }
         const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
         mbar_wait(&sm.uempty[u], uph ^ 1);
         const bool int4 = t < G4;
@@ -209,35 +238,53 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     const int q = warp & 3;       // TMEM lane quarter this warp may access
     const int half = e >> 2;
     const int n_local = q * 32 + lane;
-    float* sa = sm.sa[e];
+    const uint32_t tlane = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * COLS;
+    // pre-fill both accumulator buffers with the magic, then hand them to the MMA warp
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int ch = 0; ch < COLS / 16; ++ch) tmem_st16_const(tlane + b * BT + ch * 16, kMagicBits);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&sm.tempty[0]);
+      mbar_arrive(&sm.tempty[1]);
+    }
     uint32_t g_it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int n0 = (tile / p.m_tiles) * kTileN;
       const int m0 = (tile % p.m_tiles) * BT;
       const int n = n0 + n_local;
       const int mc0 = m0 + half * COLS;
-      float acc[COLS];
+      float2 acc[COLS / 2];
 #pragma unroll
-      for (int j = 0; j < COLS; ++j) acc[j] = 0.0f;
+      for (int j = 0; j < COLS / 2; ++j) acc[j] = make_float2(0.0f, 0.0f);
       for (int t = 0; t < G; ++t, ++g_it) {
         const uint32_t b = g_it & 1, bph = (g_it >> 1) & 1;
+        const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
         const bool int4 = t < G4;
-        for (int j = lane; j < COLS; j += 32) {
-          const int m = mc0 + j;
-          sa[j] = (m < p.M) ? __ldg(p.a_scales + static_cast<int64_t>(t) * p.M + m) : 0.0f;
-        }
-        float sw = __ldg(p.w_scales + static_cast<int64_t>(t) * p.N + n);
+        mbar_wait(&sm.sready[sr], sph);
+        float sw = sm.ssw[sr][n_local];
         if (int4) sw *= (1.0f / 256.0f);  // undo the 16*16 operand pre-scaling (exact)
-        __syncwarp();
+        // Dequantize T = float(1.5*2^23 + R) with ONE fma: g = T*sw' - 1.5*2^23*sw' = sw'*R,
+        // rounded once.  sw' = sw with its 2 lowest mantissa bits cleared (relative change
+        // < 2^-22) so that 1.5*2^23*sw' is exact; see DESIGN.md "Epilogue arithmetic".
+        const float swh = __uint_as_float(__float_as_uint(sw) & 0xFFFFFFFCu);
+        const float2 sw2 = make_float2(swh, swh);
+        const float2 nc2 = make_float2(-kMagic * swh, -kMagic * swh);
+        const float4* sa4 = reinterpret_cast<const float4*>(&sm.ssa[sr][half * COLS]);
         mbar_wait(&sm.tfull[b], bph);
         tc_fence_after();
-        const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * BT + half * COLS;
+        const uint32_t taddr = tlane + b * BT;
 #pragma unroll
         for (int ch = 0; ch < COLS / 16; ++ch) {
           uint32_t r[16];
           tmem_ld16(taddr + ch * 16, r);
           tmem_ld_wait();
+          tmem_st16_const(taddr + ch * 16, kMagicBits);   // re-arm for the group after next
           if (ch == COLS / 16 - 1) {
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.tempty[b]);
@@ -246,28 +293,36 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
               const int m = mc0 + ch * 16 + k;
-              const int v = static_cast<int>(r[k]);
+              const int v = static_cast<int>(r[k] - kMagicBits);
               if (m < p.M)
                 p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
             }
           }
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float scale = sw * sa[ch * 16 + k];
-            acc[ch * 16 + k] = fmaf(scale, __int2float_rn(static_cast<int>(r[k])), acc[ch * 16 + k]);
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const float4 s = sa4[ch * 4 + k4];
+            const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
+                                                     __uint_as_float(r[4 * k4 + 1])), sw2, nc2);
+            const float2 g1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 2]),
+                                                     __uint_as_float(r[4 * k4 + 3])), sw2, nc2);
+            acc[ch * 8 + 2 * k4] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[ch * 8 + 2 * k4]);
+            acc[ch * 8 + 2 * k4 + 1] =
+                __ffma2_rn(make_float2(s.z, s.w), g1, acc[ch * 8 + 2 * k4 + 1]);
           }
         }
         __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.sfree[sr]);
       }
       // ---- tile output ----
 #pragma unroll
       for (int j = 0; j < COLS; ++j) {
         const int m = mc0 + j;
+        const float v = (j & 1) ? acc[j >> 1].y : acc[j >> 1].x;
         if (m < p.M) {
           if (p.c_f32)
-            static_cast<float*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = acc[j];
+            static_cast<float*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = v;
           else
-            static_cast<__half*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = __float2half_rn(acc[j]);
+            static_cast<__half*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = __float2half_rn(v);
         }
       }
     }
