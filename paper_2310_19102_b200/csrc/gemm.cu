@@ -5,21 +5,23 @@
 // and sum (Step 3), all fused in the MMA pipeline; the 128 INT8 outlier channels are one more
 // group of the same K loop (mixed precision via reordering P:242).
 //
-// B200 design (DESIGN.md "GEMM kernel"):
+// B200 design (DESIGN.md section 7.2):
 //   * swap-AB: the MMA M side (128 TMEM lanes) is 128 output channels n of W, the MMA N side is a
 //     tile of BT tokens.  D[n][m] = sum_k W'[n][k] A'[m][k].
 //   * TMA streams the PACKED INT4 tiles (64 B per row per group) into a 4-stage ring; the INT8
 //     outlier group arrives as two 64-byte halves through the same ring.
-//   * 4 unpack warps expand nibbles to int8 *16 (q << 4: one LOP per 4 codes, exact two's
-//     complement) directly into the 128B-swizzled K-major layout the UMMA descriptor reads, using
-//     the same intra-group channel permutation for both operands (the dot product is
-//     order-invariant).  tcgen05 has no s4 kind, so this is the INT4 -> INT8 step.
-//   * 1 MMA thread issues 4 x tcgen05.mma.kind::i8 (K = 32) per group into a TMEM int32
-//     accumulator that is double-buffered ACROSS groups, so group t+1 multiplies while the
-//     epilogue drains group t.  INT4 partials come out as 256*P_t (exact, |256 P| <= 2^21).
-//   * 8 epilogue warps (thread = output channel, TMEM lane) tcgen05.ld the partial, scale it by
-//     s_w[t][n] * s_a[t][m] (1/256 folded into s_w, exact) and accumulate in fp32 registers;
-//     after the last group they write fp16 (or fp32 for K-sharded TP).
+//   * 4 unpack warps expand nibbles to int8 16*q (high nibbles: one LOP per 4 codes; low nibbles:
+//     SHL + LOP; exact two's complement) directly into the 128B-swizzled K-major layout the UMMA
+//     descriptor reads, with the same intra-group channel permutation for both operands (the dot
+//     product is order-invariant).  tcgen05 has no s4 kind, so this is the INT4 -> INT8 step.
+//   * 1 MMA thread per group: one kind::f16 MMA writes the constant 1.5*2^23 (16 x 768 x 1024,
+//     exact in fp32) into the TMEM accumulator, then 4 x kind::i8 (K = 32) accumulate the int32
+//     partial on top of its bit pattern, leaving float(1.5*2^23 + R) bit-exactly (|R| <= 2^21).
+//     Accumulators are double-buffered ACROSS groups so group t+1 multiplies while the epilogue
+//     drains group t.  INT4 partials come out as R = 256*P_t (exact).
+//   * 8 epilogue warps (thread = output channel = TMEM lane) tcgen05.ld the biased partials and
+//     dequantize with two FFMA2 per column pair; fp32
+//     accumulators live in registers; after the last group they write fp16 (or fp32 for K-shards).
 //   * persistent CTAs (one per SM) walk output tiles; consecutive CTAs share the weight tile.
 #include <cstdint>
 #include <cuda.h>
@@ -32,20 +34,18 @@
 namespace atom {
 
 constexpr int kStages = 4;      // packed-tile TMA ring depth
-constexpr int kUbuf = 2;        // unpacked int8 operand buffers
+constexpr int kUbuf = 3;        // unpacked int8 operand buffers
 constexpr int kThreads = 448;   // 14 warps
 constexpr int kUnpackWarp0 = 2; // warps 2..5
 constexpr int kNumUnpackWarps = 4;
+constexpr int kUnpackThreads = kNumUnpackWarps * 32;
 constexpr int kEpiWarp0 = 6;    // warps 6..13
 constexpr int kNumEpiWarps = 8;
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
 constexpr int kSRing = 8;       // group-scale ring depth
 
-// The TMEM accumulator of every group starts from the int32 bit pattern of 1.5*2^23 (tcgen05.mma
-// always accumulates), so the MMA leaves float(1.5*2^23 + P) bit-exactly (|P| <= 2^21 < 2^22)
-// and the epilogue recovers P with one exact FADD instead of an int->float conversion.
-constexpr uint32_t kMagicBits = 0x4B400000u;
-constexpr float kMagic = 12582912.0f;
+constexpr uint32_t kMagicBits = 0x4B400000u;   // bit pattern of 1.5*2^23
+constexpr float kMagic = 12582912.0f;          // 1.5*2^23 = 16 * 768 * 1024
 
 struct GemmParams {
   const float* a_scales;
@@ -63,8 +63,10 @@ struct __align__(1024) GemmSmem {
   uint8_t ubuf_a[kUbuf][BT * 128];      // unpacked activation group, SW128 K-major
   uint8_t stage_w[kStages][kTileN * 64];// packed weight group (or half of the INT8 group)
   uint8_t stage_a[kStages][BT * 64];    // packed activation group
-  float ssw[kSRing][kTileN];             // weight scales of a group (ring, filled by cp.async)
-  float ssa[kSRing][BT];                 // activation scales of a group
+  __half bias_a[kTileN * 16];           // f16 operands of the bias MMA: all 768 / all 1024
+  __half bias_b[BT * 16];
+  float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
+  float ssa[kSRing][BT];                // activation scales of a group
   uint64_t full[kStages], empty[kStages];
   uint64_t ufull[kUbuf], uempty[kUbuf];
   uint64_t tfull[2], tempty[2];
@@ -77,8 +79,40 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
   return (2 * BT) <= 32 ? 32 : (2 * BT) <= 64 ? 64 : (2 * BT) <= 128 ? 128 : (2 * BT) <= 256 ? 256 : 512;
 }
 
-__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t chunk) {
-  return row * 128u + (((chunk ^ (row & 7u)) & 7u) << 4);
+__device__ __forceinline__ uint4 unpack_lo(uint4 v) {  // even channels -> 16*q bytes
+  return make_uint4((v.x << 4) & 0xF0F0F0F0u, (v.y << 4) & 0xF0F0F0F0u,
+                    (v.z << 4) & 0xF0F0F0F0u, (v.w << 4) & 0xF0F0F0F0u);
+}
+__device__ __forceinline__ uint4 unpack_hi(uint4 v) {  // odd channels -> 16*q bytes
+  return make_uint4(v.x & 0xF0F0F0F0u, v.y & 0xF0F0F0F0u, v.z & 0xF0F0F0F0u, v.w & 0xF0F0F0F0u);
+}
+
+// One operand tile of ROWS rows: packed stage [ROWS][64 B] -> unpacked SW128 [ROWS][128 B].
+// Thread ut owns the 16-byte packed chunk (ut & 3) of rows (ut >> 2) + 32k; rows 32 apart share
+// their swizzle phase, so every address below is a per-thread base plus an immediate.
+template <int ROWS>
+__device__ __forceinline__ void unpack_tile(const uint8_t* stage, uint8_t* ubuf, int ut,
+                                            bool int4, int h) {
+  constexpr int KR = ROWS / 32;
+  const uint32_t r0 = static_cast<uint32_t>(ut) >> 2, c = static_cast<uint32_t>(ut) & 3u;
+  const uint32_t r7 = r0 & 7u;
+  const uint8_t* src = stage + ut * 16;
+  uint4 v[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) v[k] = *reinterpret_cast<const uint4*>(src + k * 32 * 64);
+  uint8_t* dst = ubuf + r0 * 128;
+  if (int4) {
+    const uint32_t olo = ((2 * c) ^ r7) << 4, ohi = ((2 * c + 1) ^ r7) << 4;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      *reinterpret_cast<uint4*>(dst + k * 32 * 128 + olo) = unpack_lo(v[k]);
+      *reinterpret_cast<uint4*>(dst + k * 32 * 128 + ohi) = unpack_hi(v[k]);
+    }
+  } else {
+    const uint32_t o = ((4 * h + c) ^ r7) << 4;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) *reinterpret_cast<uint4*>(dst + k * 32 * 128 + o) = v[k];
+  }
 }
 
 template <int BT>
@@ -87,6 +121,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                  const __grid_constant__ CUtensorMap tm_aq4,
                  const __grid_constant__ CUtensorMap tm_wq8,
                  const __grid_constant__ CUtensorMap tm_aq8, const GemmParams p) {
+  static_assert(BT % 32 == 0 && BT >= 32 && BT <= 128, "token tile");
   extern __shared__ uint8_t smem_raw[];
   GemmSmem<BT>& sm = *reinterpret_cast<GemmSmem<BT>*>(
       smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -108,7 +143,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       mbar_init(&sm.tempty[b], kNumEpiWarps);
     }
     for (int r = 0; r < kSRing; ++r) {
-      mbar_init(&sm.sready[r], kNumUnpackWarps * 32);  // one cp.async-arrive per unpack thread
+      mbar_init(&sm.sready[r], kUnpackThreads);  // one cp.async-arrive per unpack thread
       mbar_init(&sm.sfree[r], kNumEpiWarps);
     }
     fence_mbar_init();
@@ -119,6 +154,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     tma_prefetch_desc(&tm_wq8);
     tma_prefetch_desc(&tm_aq8);
   }
+  // bias-MMA operands: every element 768 (A) / 1024 (B) -> each output = 16*768*1024 = 1.5*2^23
+  for (int i = threadIdx.x; i < kTileN * 16; i += kThreads) sm.bias_a[i] = __float2half_rn(768.0f);
+  for (int i = threadIdx.x; i < BT * 16; i += kThreads) sm.bias_b[i] = __float2half_rn(1024.0f);
+  fence_proxy_async_smem();
   if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
   tc_fence_before();
   __syncthreads();
@@ -154,15 +193,20 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     // ===================== MMA issuer (single thread) =====================
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_i8(kTileN, BT);
+      constexpr uint32_t idesc_bias = umma_idesc_f16_f32(kTileN, BT);
+      const uint64_t bias_a = umma_desc_noswz(smem_u32(sm.bias_a), kTileN);
+      const uint64_t bias_b = umma_desc_noswz(smem_u32(sm.bias_b), BT);
       uint32_t g_it = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         for (int t = 0; t < G; ++t, ++g_it) {
           const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
           const uint32_t b = g_it & 1, bph = (g_it >> 1) & 1;
-          mbar_wait(&sm.ufull[u], uph);
-          mbar_wait(&sm.tempty[b], bph);   // buffer drained AND re-filled with the magic
+          mbar_wait(&sm.tempty[b], bph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + b * BT;
+          umma_f16(d, bias_a, bias_b, idesc_bias, 0u);   // D = 1.5*2^23 (fp32 bits 0x4B400000)
+          mbar_wait(&sm.ufull[u], uph);
+          tc_fence_after();
           const uint32_t a_base = smem_u32(sm.ubuf_w[u]);
           const uint32_t b_base = smem_u32(sm.ubuf_a[u]);
 #pragma unroll
@@ -188,7 +232,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
           mbar_wait(&sm.sfree[sr], sph ^ 1);
           cp_async_4(&sm.ssw[sr][ut], p.w_scales + static_cast<int64_t>(t) * p.N + n0 + ut);
-          for (int j = ut; j < BT; j += kNumUnpackWarps * 32) {
+          for (int j = ut; j < BT; j += kUnpackThreads) {
             // rows past M: any finite scale works, their partials are exactly zero (TMA
             // zero-fills out-of-range activation rows) and they are never stored
             const int m = min(m0 + j, p.M - 1);
@@ -203,26 +247,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         for (int h = 0; h < nh; ++h, ++it) {
           const uint32_t s = it % kStages, ph = (it / kStages) & 1;
           mbar_wait(&sm.full[s], ph);
-#pragma unroll 2
-          for (int i = ut; i < (kTileN + BT) * 4; i += kNumUnpackWarps * 32) {
-            const uint32_t row = i >> 2, c = i & 3;
-            const bool is_w = row < kTileN;
-            const uint32_t r = is_w ? row : row - kTileN;
-            const uint8_t* src = (is_w ? sm.stage_w[s] : sm.stage_a[s]) + r * 64 + c * 16;
-            uint8_t* dst = is_w ? sm.ubuf_w[u] : sm.ubuf_a[u];
-            const uint4 v = *reinterpret_cast<const uint4*>(src);
-            if (int4) {
-              uint4 lo, hi;
-              lo.x = (v.x << 4) & 0xF0F0F0F0u; hi.x = v.x & 0xF0F0F0F0u;
-              lo.y = (v.y << 4) & 0xF0F0F0F0u; hi.y = v.y & 0xF0F0F0F0u;
-              lo.z = (v.z << 4) & 0xF0F0F0F0u; hi.z = v.z & 0xF0F0F0F0u;
-              lo.w = (v.w << 4) & 0xF0F0F0F0u; hi.w = v.w & 0xF0F0F0F0u;
-              *reinterpret_cast<uint4*>(dst + sw128_off(r, 2 * c)) = lo;
-              *reinterpret_cast<uint4*>(dst + sw128_off(r, 2 * c + 1)) = hi;
-            } else {
-              *reinterpret_cast<uint4*>(dst + sw128_off(r, 4 * h + c)) = v;
-            }
-          }
+          unpack_tile<kTileN>(sm.stage_w[s], sm.ubuf_w[u], ut, int4, h);
+          unpack_tile<BT>(sm.stage_a[s], sm.ubuf_a[u], ut, int4, h);
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[s]);
         }
@@ -234,23 +260,12 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   } else {
     // ===================== epilogue warps =====================
     constexpr int COLS = BT / 2;  // tokens per thread
+    constexpr int CH = COLS >= 32 ? 32 : 16;
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;       // TMEM lane quarter this warp may access
     const int half = e >> 2;
     const int n_local = q * 32 + lane;
     const uint32_t tlane = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * COLS;
-    // pre-fill both accumulator buffers with the magic, then hand them to the MMA warp
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int ch = 0; ch < COLS / 16; ++ch) tmem_st16_const(tlane + b * BT + ch * 16, kMagicBits);
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&sm.tempty[0]);
-      mbar_arrive(&sm.tempty[1]);
-    }
     uint32_t g_it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int n0 = (tile / p.m_tiles) * kTileN;
@@ -278,36 +293,34 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         tc_fence_after();
         const uint32_t taddr = tlane + b * BT;
 #pragma unroll
-        for (int ch = 0; ch < COLS / 16; ++ch) {
-          uint32_t r[16];
-          tmem_ld16(taddr + ch * 16, r);
+        for (int ch = 0; ch < COLS / CH; ++ch) {
+          uint32_t r[CH];
+          tmem_ld<CH>(taddr + ch * CH, r);
           tmem_ld_wait();
-          tmem_st16_const(taddr + ch * 16, kMagicBits);   // re-arm for the group after next
-          if (ch == COLS / 16 - 1) {
-            tmem_st_wait();
+          if (ch == COLS / CH - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.tempty[b]);
           }
           if (p.debug != nullptr) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const int m = mc0 + ch * 16 + k;
+            for (int k = 0; k < CH; ++k) {
+              const int m = mc0 + ch * CH + k;
               const int v = static_cast<int>(r[k] - kMagicBits);
               if (m < p.M)
                 p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
             }
           }
 #pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
-            const float4 s = sa4[ch * 4 + k4];
+          for (int k4 = 0; k4 < CH / 4; ++k4) {
+            const float4 s = sa4[ch * (CH / 4) + k4];
+            const int j = ch * (CH / 2) + 2 * k4;
             const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
                                                      __uint_as_float(r[4 * k4 + 1])), sw2, nc2);
             const float2 g1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 2]),
                                                      __uint_as_float(r[4 * k4 + 3])), sw2, nc2);
-            acc[ch * 8 + 2 * k4] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[ch * 8 + 2 * k4]);
-            acc[ch * 8 + 2 * k4 + 1] =
-                __ffma2_rn(make_float2(s.z, s.w), g1, acc[ch * 8 + 2 * k4 + 1]);
+            acc[j] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[j]);
+            acc[j + 1] = __ffma2_rn(make_float2(s.z, s.w), g1, acc[j + 1]);
           }
         }
         __syncwarp();
