@@ -34,7 +34,7 @@
 namespace atom {
 
 constexpr int kStages = 4;      // packed-tile TMA ring depth
-constexpr int kUbuf = 3;        // unpacked int8 operand buffers
+constexpr int kUbuf = 4;        // unpacked int8 operand buffers
 constexpr int kThreads = 448;   // 14 warps
 constexpr int kUnpackWarp0 = 2; // warps 2..5
 constexpr int kNumUnpackWarps = 4;
@@ -79,9 +79,13 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
   return (2 * BT) <= 32 ? 32 : (2 * BT) <= 64 ? 64 : (2 * BT) <= 128 ? 128 : (2 * BT) <= 256 ? 256 : 512;
 }
 
+// rotl(v, 4) & 0xF0F0F0F0 == (v << 4) & 0xF0F0F0F0, but as SHF.L.W + LOP3 on the integer pipe
+// (a plain shift is compiled to IMAD.SHL on the FMA pipe, which the epilogue saturates).
+__device__ __forceinline__ uint32_t lo_nib(uint32_t v) {
+  return __funnelshift_l(v, v, 4) & 0xF0F0F0F0u;
+}
 __device__ __forceinline__ uint4 unpack_lo(uint4 v) {  // even channels -> 16*q bytes
-  return make_uint4((v.x << 4) & 0xF0F0F0F0u, (v.y << 4) & 0xF0F0F0F0u,
-                    (v.z << 4) & 0xF0F0F0F0u, (v.w << 4) & 0xF0F0F0F0u);
+  return make_uint4(lo_nib(v.x), lo_nib(v.y), lo_nib(v.z), lo_nib(v.w));
 }
 __device__ __forceinline__ uint4 unpack_hi(uint4 v) {  // odd channels -> 16*q bytes
   return make_uint4(v.x & 0xF0F0F0F0u, v.y & 0xF0F0F0F0u, v.z & 0xF0F0F0F0u, v.w & 0xF0F0F0F0u);
@@ -115,7 +119,7 @@ __device__ __forceinline__ void unpack_tile(const uint8_t* stage, uint8_t* ubuf,
   }
 }
 
-template <int BT>
+template <int BT, bool kDebug>
 __global__ void __launch_bounds__(kThreads, 1)
 w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                  const __grid_constant__ CUtensorMap tm_aq4,
@@ -302,7 +306,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.tempty[b]);
           }
-          if (p.debug != nullptr) {
+          if constexpr (kDebug) {
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
               const int m = mc0 + ch * CH + k;
@@ -420,12 +424,12 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
   p.num_tiles = p.m_tiles * (N / kTileN);
 
   const size_t smem = sizeof(GemmSmem<BT>) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(w4a4_gemm_kernel<BT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = p.debug ? w4a4_gemm_kernel<BT, true> : w4a4_gemm_kernel<BT, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
-  w4a4_gemm_kernel<BT><<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
+  kern<<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
   return cudaGetLastError();
 }
 
