@@ -24,6 +24,7 @@
 //     accumulators live in registers; after the last group they write fp16 (or fp32 for K-shards).
 //   * persistent CTAs (one per SM) walk output tiles; consecutive CTAs share the weight tile.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -43,6 +44,7 @@ constexpr int kEpiWarp0 = 6;    // warps 6..13
 constexpr int kNumEpiWarps = 8;
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
 constexpr int kSRing = 8;       // group-scale ring depth
+constexpr int kTBuf = 4;        // TMEM accumulator buffers (4 x BT <= 512 columns)
 
 constexpr uint32_t kMagicBits = 0x4B400000u;   // bit pattern of 1.5*2^23
 constexpr float kMagic = 12582912.0f;          // 1.5*2^23 = 16 * 768 * 1024
@@ -69,14 +71,15 @@ struct __align__(1024) GemmSmem {
   float ssa[kSRing][BT];                // activation scales of a group
   uint64_t full[kStages], empty[kStages];
   uint64_t ufull[kUbuf], uempty[kUbuf];
-  uint64_t tfull[2], tempty[2];
+  uint64_t tfull[kTBuf], tempty[kTBuf];
   uint64_t sready[kSRing], sfree[kSRing];
   uint32_t tmem_base;
 };
 
 template <int BT>
 __host__ __device__ constexpr uint32_t tmem_cols() {
-  return (2 * BT) <= 32 ? 32 : (2 * BT) <= 64 ? 64 : (2 * BT) <= 128 ? 128 : (2 * BT) <= 256 ? 256 : 512;
+  return (kTBuf * BT) <= 32 ? 32 : (kTBuf * BT) <= 64 ? 64 : (kTBuf * BT) <= 128 ? 128
+       : (kTBuf * BT) <= 256 ? 256 : 512;
 }
 
 // rotl(v, 4) & 0xF0F0F0F0 == (v << 4) & 0xF0F0F0F0, but as SHF.L.W + LOP3 on the integer pipe
@@ -119,13 +122,21 @@ __device__ __forceinline__ void unpack_tile(const uint8_t* stage, uint8_t* ubuf,
   }
 }
 
-template <int BT, bool kDebug>
+// kMode (development timing probes, never used for results): bit 0 = epilogue skips its
+// arithmetic; bit 1 = unpack skips its data movement; bit 2 = producer skips the TMA loads;
+// bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint;
+// bit 5 = no bias MMA.
+template <int BT, bool kDebug, int kMode = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                  const __grid_constant__ CUtensorMap tm_aq4,
                  const __grid_constant__ CUtensorMap tm_wq8,
                  const __grid_constant__ CUtensorMap tm_aq8, const GemmParams p) {
-  static_assert(BT % 32 == 0 && BT >= 32 && BT <= 128, "token tile");
+  static_assert(BT % 32 == 0 && BT >= 32 && BT * kTBuf <= 512, "token tile");
+  auto wait = [](uint64_t* bar, uint32_t parity) {
+    if constexpr ((kMode & 16) != 0) mbar_wait_spin(bar, parity);
+    else mbar_wait(bar, parity);
+  };
   extern __shared__ uint8_t smem_raw[];
   GemmSmem<BT>& sm = *reinterpret_cast<GemmSmem<BT>*>(
       smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -142,7 +153,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       mbar_init(&sm.ufull[u], kNumUnpackWarps);
       mbar_init(&sm.uempty[u], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kTBuf; ++b) {
       mbar_init(&sm.tfull[b], 1);
       mbar_init(&sm.tempty[b], kNumEpiWarps);
     }
@@ -180,7 +191,11 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         const int m0 = (tile % p.m_tiles) * BT;
         for (int l = 0; l < loads_per_tile; ++l, ++it) {
           const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-          mbar_wait(&sm.empty[s], ph ^ 1);
+          wait(&sm.empty[s], ph ^ 1);
+          if constexpr ((kMode & 4) != 0) {   // probe: no TMA traffic
+            mbar_arrive(&sm.full[s]);
+            continue;
+          }
           mbar_arrive_expect_tx(&sm.full[s], kTileN * 64 + BT * 64);
           if (l < G4) {
             tma_load_2d(sm.stage_w[s], &tm_wq4, &sm.full[s], l * 64, n0);
@@ -204,12 +219,13 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         for (int t = 0; t < G; ++t, ++g_it) {
           const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
-          const uint32_t b = g_it & 1, bph = (g_it >> 1) & 1;
-          mbar_wait(&sm.tempty[b], bph ^ 1);
+          const uint32_t b = g_it % kTBuf, bph = (g_it / kTBuf) & 1;
+          wait(&sm.tempty[b], bph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + b * BT;
-          umma_f16(d, bias_a, bias_b, idesc_bias, 0u);   // D = 1.5*2^23 (fp32 bits 0x4B400000)
-          mbar_wait(&sm.ufull[u], uph);
+          if constexpr ((kMode & 32) == 0)
+            umma_f16(d, bias_a, bias_b, idesc_bias, 0u);   // D = 1.5*2^23 (fp32 bits 0x4B400000)
+          wait(&sm.ufull[u], uph);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sm.ubuf_w[u]);
           const uint32_t b_base = smem_u32(sm.ubuf_a[u]);
@@ -234,7 +250,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       for (int t = 0; t < G; ++t, ++g_it) {
         {
           const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
-          mbar_wait(&sm.sfree[sr], sph ^ 1);
+          wait(&sm.sfree[sr], sph ^ 1);
           cp_async_4(&sm.ssw[sr][ut], p.w_scales + static_cast<int64_t>(t) * p.N + n0 + ut);
           for (int j = ut; j < BT; j += kUnpackThreads) {
             // rows past M: any finite scale works, their partials are exactly zero (TMA
@@ -245,14 +261,16 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           cp_async_mbar_arrive(&sm.sready[sr]);
         }
         const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
-        mbar_wait(&sm.uempty[u], uph ^ 1);
+        wait(&sm.uempty[u], uph ^ 1);
         const bool int4 = t < G4;
         const int nh = int4 ? 1 : 2;
         for (int h = 0; h < nh; ++h, ++it) {
           const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-          mbar_wait(&sm.full[s], ph);
-          unpack_tile<kTileN>(sm.stage_w[s], sm.ubuf_w[u], ut, int4, h);
-          unpack_tile<BT>(sm.stage_a[s], sm.ubuf_a[u], ut, int4, h);
+          wait(&sm.full[s], ph);
+          if constexpr ((kMode & 2) == 0) {
+            unpack_tile<kTileN>(sm.stage_w[s], sm.ubuf_w[u], ut, int4, h);
+            unpack_tile<BT>(sm.stage_a[s], sm.ubuf_a[u], ut, int4, h);
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[s]);
         }
@@ -280,10 +298,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 #pragma unroll
       for (int j = 0; j < COLS / 2; ++j) acc[j] = make_float2(0.0f, 0.0f);
       for (int t = 0; t < G; ++t, ++g_it) {
-        const uint32_t b = g_it & 1, bph = (g_it >> 1) & 1;
+        const uint32_t b = g_it % kTBuf, bph = (g_it / kTBuf) & 1;
         const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
         const bool int4 = t < G4;
-        mbar_wait(&sm.sready[sr], sph);
+        wait(&sm.sready[sr], sph);
         float sw = sm.ssw[sr][n_local];
         if (int4) sw *= (1.0f / 256.0f);  // undo the 16*16 operand pre-scaling (exact)
         // Dequantize T = float(1.5*2^23 + R) with ONE fma: g = T*sw' - 1.5*2^23*sw' = sw'*R,
@@ -293,14 +311,19 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         const float2 sw2 = make_float2(swh, swh);
         const float2 nc2 = make_float2(-kMagic * swh, -kMagic * swh);
         const float4* sa4 = reinterpret_cast<const float4*>(&sm.ssa[sr][half * COLS]);
-        mbar_wait(&sm.tfull[b], bph);
+        wait(&sm.tfull[b], bph);
         tc_fence_after();
         const uint32_t taddr = tlane + b * BT;
 #pragma unroll
         for (int ch = 0; ch < COLS / CH; ++ch) {
           uint32_t r[CH];
-          tmem_ld<CH>(taddr + ch * CH, r);
-          tmem_ld_wait();
+          if constexpr ((kMode & 8) == 0) {
+            tmem_ld<CH>(taddr + ch * CH, r);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int k = 0; k < CH; ++k) r[k] = 0;
+          }
           if (ch == COLS / CH - 1) {
             tc_fence_before();
             __syncwarp();
@@ -316,7 +339,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             }
           }
 #pragma unroll
-          for (int k4 = 0; k4 < CH / 4; ++k4) {
+          for (int k4 = 0; k4 < ((kMode & 1) ? 0 : CH / 4); ++k4) {
             const float4 s = sa4[ch * (CH / 4) + k4];
             const int j = ch * (CH / 2) + 2 * k4;
             const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
@@ -425,6 +448,20 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
 
   const size_t smem = sizeof(GemmSmem<BT>) + 1024;
   auto kern = p.debug ? w4a4_gemm_kernel<BT, true> : w4a4_gemm_kernel<BT, false>;
+  if constexpr (BT == 128) {
+    static const char* mode_env = getenv("ATOM_GEMM_PROBE_MODE");   // development probe only
+    const int mode = mode_env ? atoi(mode_env) : 0;
+    if (mode == 1) kern = w4a4_gemm_kernel<BT, false, 1>;
+    if (mode == 2) kern = w4a4_gemm_kernel<BT, false, 2>;
+    if (mode == 3) kern = w4a4_gemm_kernel<BT, false, 3>;
+    if (mode == 4) kern = w4a4_gemm_kernel<BT, false, 4>;
+    if (mode == 7) kern = w4a4_gemm_kernel<BT, false, 7>;
+    if (mode == 15) kern = w4a4_gemm_kernel<BT, false, 15>;
+    if (mode == 16) kern = w4a4_gemm_kernel<BT, false, 16>;
+    if (mode == 23) kern = w4a4_gemm_kernel<BT, false, 23>;
+    if (mode == 47) kern = w4a4_gemm_kernel<BT, false, 47>;
+    if (mode == 32) kern = w4a4_gemm_kernel<BT, false, 32>;
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -1,0 +1,39 @@
+"""Time the GEMM kernel alone (CUDA events, L2 flushed) for a config, optionally in a probe mode
+(ATOM_GEMM_PROBE_MODE: 1 = no epilogue math, 2 = no unpack, 3 = neither).  Development tool."""
+import os
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import torch  # noqa: E402
+
+import paper_2310_19102_b200 as atom  # noqa: E402
+import synth  # noqa: E402
+from bench import CONFIGS  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
+M, N, K, _ = CONFIGS[cfg]
+X, perm = synth.activations(M, K, 0), synth.perm_for(K, 0)
+W = synth.weights(N, K, 0)
+pd = torch.from_numpy(perm).cuda()
+wq = atom.quantize_weights(torch.from_numpy(W).cuda(), pd)
+aq = atom.reorder_quantize(torch.from_numpy(X).cuda(), pd)
+c = torch.empty((M, N), dtype=torch.float16, device="cuda")
+flush = torch.empty(300 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(3):
+    atom.w4a4_gemm(aq, wq, out=c)
+ts = []
+for _ in range(10):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    atom.w4a4_gemm(aq, wq, out=c)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+ts.sort()
+us = ts[len(ts) // 2] * 1e3
+print(f"{cfg} mode={os.environ.get('ATOM_GEMM_PROBE_MODE', '0')} gemm {us:.1f} us  "
+      f"{2 * M * N * K / us / 1e6:.0f} TOPS")
