@@ -14,16 +14,17 @@
 //     SHL + LOP; exact two's complement) directly into the 128B-swizzled K-major layout the UMMA
 //     descriptor reads, with the same intra-group channel permutation for both operands (the dot
 //     product is order-invariant).  tcgen05 has no s4 kind, so this is the INT4 -> INT8 step.
-//   * 1 MMA thread per group: one kind::f16 MMA writes the constant 1.5*2^23 (16 x 768 x 1024,
-//     exact in fp32) into the TMEM accumulator, then 4 x kind::i8 (K = 32) accumulate the int32
-//     partial on top of its bit pattern, leaving float(1.5*2^23 + R) bit-exactly (|R| <= 2^21).
-//     Accumulators are double-buffered ACROSS groups so group t+1 multiplies while the epilogue
-//     drains group t.  INT4 partials come out as R = 256*P_t (exact).
-//   * 8 epilogue warps (thread = output channel = TMEM lane) tcgen05.ld the biased partials and
-//     dequantize with two FFMA2 per column pair; fp32
+//   * 1 MMA thread per group: 4 x kind::i8 (K = 32) into a fresh TMEM int32 accumulator (4 TMEM
+//     buffers rotate ACROSS groups so later groups multiply while the epilogue drains earlier
+//     ones) and ONE tcgen05.commit that both frees the unpacked operands and publishes the
+//     partial.  INT4 partials come out as R = 256*P_t (exact, |R| <= 2^21).
+//   * 8 epilogue warps (thread = output channel = TMEM lane) tcgen05.ld the partials, turn R into
+//     the float 1.5*2^23 + R with one LOP3 ((R & 0x7FFFFF) ^ 0x4B400000, exact for |R| < 2^22)
+//     and dequantize with two FFMA2 per column pair; fp32
 //     accumulators live in registers; after the last group they write fp16 (or fp32 for K-shards).
 //   * persistent CTAs (one per SM) walk output tiles; consecutive CTAs share the weight tile.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -39,15 +40,15 @@ constexpr int kUbuf = 4;        // unpacked int8 operand buffers
 constexpr int kThreads = 448;   // 14 warps
 constexpr int kUnpackWarp0 = 2; // warps 2..5
 constexpr int kNumUnpackWarps = 4;
-constexpr int kUnpackThreads = kNumUnpackWarps * 32;
 constexpr int kEpiWarp0 = 6;    // warps 6..13
 constexpr int kNumEpiWarps = 8;
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
-constexpr int kSRing = 8;       // group-scale ring depth
+constexpr int kSRing = 16;      // group-scale ring depth
 constexpr int kTBuf = 4;        // TMEM accumulator buffers (4 x BT <= 512 columns)
+static_assert(kTBuf == kUbuf, "one mdone barrier ring serves both the operand and TMEM rings");
 
 constexpr uint32_t kMagicBits = 0x4B400000u;   // bit pattern of 1.5*2^23
-constexpr float kMagic = 12582912.0f;          // 1.5*2^23 = 16 * 768 * 1024
+constexpr float kMagic = 12582912.0f;          // 1.5*2^23
 
 struct GemmParams {
   const float* a_scales;
@@ -57,6 +58,7 @@ struct GemmParams {
   int32_t* debug;
   int M, N, G, G4, k_o, c_f32;
   int m_tiles, num_tiles;
+  long long* trace;   // development timeline probe (CTA 0): [3][256] clock64 stamps, or null
 };
 
 template <int BT>
@@ -65,13 +67,12 @@ struct __align__(1024) GemmSmem {
   uint8_t ubuf_a[kUbuf][BT * 128];      // unpacked activation group, SW128 K-major
   uint8_t stage_w[kStages][kTileN * 64];// packed weight group (or half of the INT8 group)
   uint8_t stage_a[kStages][BT * 64];    // packed activation group
-  __half bias_a[kTileN * 16];           // f16 operands of the bias MMA: all 768 / all 1024
-  __half bias_b[BT * 16];
   float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
   float ssa[kSRing][BT];                // activation scales of a group
   uint64_t full[kStages], empty[kStages];
-  uint64_t ufull[kUbuf], uempty[kUbuf];
-  uint64_t tfull[kTBuf], tempty[kTBuf];
+  uint64_t ufull[kUbuf];
+  uint64_t mdone[kUbuf];                // MMAs of a group done: operands free + partial ready
+  uint64_t tempty[kTBuf];
   uint64_t sready[kSRing], sfree[kSRing];
   uint32_t tmem_base;
 };
@@ -90,6 +91,12 @@ __device__ __forceinline__ uint32_t lo_nib(uint32_t v) {
 __device__ __forceinline__ uint4 unpack_lo(uint4 v) {  // even channels -> 16*q bytes
   return make_uint4(lo_nib(v.x), lo_nib(v.y), lo_nib(v.z), lo_nib(v.w));
 }
+// float(1.5*2^23 + R) from the int32 partial R, |R| < 2^22: the low 23 bits of R with bit 22
+// flipped are R + 2^22 in [0, 2^23); OR-ing the exponent of 2^23 gives 2^23 + 2^22 + R exactly.
+__device__ __forceinline__ float biased(uint32_t r) {
+  return __uint_as_float((r & 0x007FFFFFu) ^ kMagicBits);
+}
+
 __device__ __forceinline__ uint4 unpack_hi(uint4 v) {  // odd channels -> 16*q bytes
   return make_uint4(v.x & 0xF0F0F0F0u, v.y & 0xF0F0F0F0u, v.z & 0xF0F0F0F0u, v.w & 0xF0F0F0F0u);
 }
@@ -124,8 +131,7 @@ __device__ __forceinline__ void unpack_tile(const uint8_t* stage, uint8_t* ubuf,
 
 // kMode (development timing probes, never used for results): bit 0 = epilogue skips its
 // arithmetic; bit 1 = unpack skips its data movement; bit 2 = producer skips the TMA loads;
-// bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint;
-// bit 5 = no bias MMA.
+// bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint.
 template <int BT, bool kDebug, int kMode = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
@@ -151,14 +157,13 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     }
     for (int u = 0; u < kUbuf; ++u) {
       mbar_init(&sm.ufull[u], kNumUnpackWarps);
-      mbar_init(&sm.uempty[u], 1);
+      mbar_init(&sm.mdone[u], 1);
     }
     for (int b = 0; b < kTBuf; ++b) {
-      mbar_init(&sm.tfull[b], 1);
       mbar_init(&sm.tempty[b], kNumEpiWarps);
     }
     for (int r = 0; r < kSRing; ++r) {
-      mbar_init(&sm.sready[r], kUnpackThreads);  // one cp.async-arrive per unpack thread
+      mbar_init(&sm.sready[r], 32);  // one cp.async-arrive per producer-warp thread
       mbar_init(&sm.sfree[r], kNumEpiWarps);
     }
     fence_mbar_init();
@@ -169,10 +174,6 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     tma_prefetch_desc(&tm_wq8);
     tma_prefetch_desc(&tm_aq8);
   }
-  // bias-MMA operands: every element 768 (A) / 1024 (B) -> each output = 16*768*1024 = 1.5*2^23
-  for (int i = threadIdx.x; i < kTileN * 16; i += kThreads) sm.bias_a[i] = __float2half_rn(768.0f);
-  for (int i = threadIdx.x; i < BT * 16; i += kThreads) sm.bias_b[i] = __float2half_rn(1024.0f);
-  fence_proxy_async_smem();
   if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
   tc_fence_before();
   __syncthreads();
@@ -183,38 +184,55 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   const int loads_per_tile = G4 + (p.k_o ? 2 : 0);
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int n0 = (tile / p.m_tiles) * kTileN;
-        const int m0 = (tile % p.m_tiles) * BT;
-        for (int l = 0; l < loads_per_tile; ++l, ++it) {
-          const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-          wait(&sm.empty[s], ph ^ 1);
+    // ===================== producer warp: group scales (cp.async) + TMA =====================
+    // The scales of a group are staged into the scale ring when its first stage is loaded, i.e.
+    // kStages + kUbuf + kTBuf groups ahead of the epilogue, which hides the L2 latency of the
+    // 4-byte copies (cp.async works for any M; TMA would need 16-byte aligned rows).
+    uint32_t it = 0, g_it = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      const int n0 = (tile / p.m_tiles) * kTileN;
+      const int m0 = (tile % p.m_tiles) * BT;
+      for (int l = 0; l < loads_per_tile; ++l, ++it) {
+        if (l <= G4) {   // first load of group t = l (the outlier group's 2nd half is l = G4+1)
+          const int t = l;
+          const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
+          wait(&sm.sfree[sr], sph ^ 1);
+          const float* ws = p.w_scales + static_cast<int64_t>(t) * p.N + n0;
+          const float* as = p.a_scales + static_cast<int64_t>(t) * p.M;
+#pragma unroll
+          for (int j = lane; j < kTileN; j += 32) cp_async_4(&sm.ssw[sr][j], ws + j);
+#pragma unroll
+          for (int j = lane; j < BT; j += 32)
+            // rows past M: any finite scale works, their partials are exactly zero (TMA
+            // zero-fills out-of-range activation rows) and they are never stored
+            cp_async_4(&sm.ssa[sr][j], as + min(m0 + j, p.M - 1));
+          cp_async_mbar_arrive(&sm.sready[sr]);
+          ++g_it;
+        }
+        const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+        wait(&sm.empty[s], ph ^ 1);
+        if (lane == 0) {
           if constexpr ((kMode & 4) != 0) {   // probe: no TMA traffic
             mbar_arrive(&sm.full[s]);
-            continue;
-          }
-          mbar_arrive_expect_tx(&sm.full[s], kTileN * 64 + BT * 64);
-          if (l < G4) {
-            tma_load_2d(sm.stage_w[s], &tm_wq4, &sm.full[s], l * 64, n0);
-            tma_load_2d(sm.stage_a[s], &tm_aq4, &sm.full[s], l * 64, m0);
           } else {
-            const int h = l - G4;
-            tma_load_2d(sm.stage_w[s], &tm_wq8, &sm.full[s], h * 64, n0);
-            tma_load_2d(sm.stage_a[s], &tm_aq8, &sm.full[s], h * 64, m0);
+            mbar_arrive_expect_tx(&sm.full[s], kTileN * 64 + BT * 64);
+            if (l < G4) {
+              tma_load_2d(sm.stage_w[s], &tm_wq4, &sm.full[s], l * 64, n0);
+              tma_load_2d(sm.stage_a[s], &tm_aq4, &sm.full[s], l * 64, m0);
+            } else {
+              const int h = l - G4;
+              tma_load_2d(sm.stage_w[s], &tm_wq8, &sm.full[s], h * 64, n0);
+              tma_load_2d(sm.stage_a[s], &tm_aq8, &sm.full[s], h * 64, m0);
+            }
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (single thread) =====================
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_i8(kTileN, BT);
-      constexpr uint32_t idesc_bias = umma_idesc_f16_f32(kTileN, BT);
-      const uint64_t bias_a = umma_desc_noswz(smem_u32(sm.bias_a), kTileN);
-      const uint64_t bias_b = umma_desc_noswz(smem_u32(sm.bias_b), BT);
       uint32_t g_it = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         for (int t = 0; t < G; ++t, ++g_it) {
@@ -223,45 +241,27 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           wait(&sm.tempty[b], bph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + b * BT;
-          if constexpr ((kMode & 32) == 0)
-            umma_f16(d, bias_a, bias_b, idesc_bias, 0u);   // D = 1.5*2^23 (fp32 bits 0x4B400000)
           wait(&sm.ufull[u], uph);
           tc_fence_after();
+          if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256) p.trace[g_it] = clock64();
           const uint32_t a_base = smem_u32(sm.ubuf_w[u]);
           const uint32_t b_base = smem_u32(sm.ubuf_a[u]);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             umma_i8(d, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
-                    1u);
-          umma_commit(&sm.uempty[u]);
-          umma_commit(&sm.tfull[b]);
+                    k > 0 ? 1u : 0u);
+          umma_commit(&sm.mdone[u]);
         }
       }
     }
   } else if (warp < kEpiWarp0) {
     // ===================== unpack warps: packed INT4 -> int8 (16*q), SW128 =====================
-    // They also stage each group's scales into the scale ring with cp.async (4-byte copies, any
-    // M), signalling sready through cp.async.mbarrier.arrive; the epilogue frees the slot.
     const int ut = threadIdx.x - kUnpackWarp0 * 32;  // 0..127
     uint32_t it = 0, g_it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int n0 = (tile / p.m_tiles) * kTileN;
-      const int m0 = (tile % p.m_tiles) * BT;
       for (int t = 0; t < G; ++t, ++g_it) {
-        {
-          const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
-          wait(&sm.sfree[sr], sph ^ 1);
-          cp_async_4(&sm.ssw[sr][ut], p.w_scales + static_cast<int64_t>(t) * p.N + n0 + ut);
-          for (int j = ut; j < BT; j += kUnpackThreads) {
-            // rows past M: any finite scale works, their partials are exactly zero (TMA
-            // zero-fills out-of-range activation rows) and they are never stored
-            const int m = min(m0 + j, p.M - 1);
-            cp_async_4(&sm.ssa[sr][j], p.a_scales + static_cast<int64_t>(t) * p.M + m);
-          }
-          cp_async_mbar_arrive(&sm.sready[sr]);
-        }
         const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
-        wait(&sm.uempty[u], uph ^ 1);
+        wait(&sm.mdone[u], uph ^ 1);   // MMAs of group g - kUbuf finished with this buffer
         const bool int4 = t < G4;
         const int nh = int4 ? 1 : 2;
         for (int h = 0; h < nh; ++h, ++it) {
@@ -276,6 +276,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         }
         fence_proxy_async_smem();
         __syncwarp();
+        if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256 && ut == 0)
+          p.trace[256 + g_it] = clock64();
         if (lane == 0) mbar_arrive(&sm.ufull[u]);
       }
     }
@@ -311,8 +313,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         const float2 sw2 = make_float2(swh, swh);
         const float2 nc2 = make_float2(-kMagic * swh, -kMagic * swh);
         const float4* sa4 = reinterpret_cast<const float4*>(&sm.ssa[sr][half * COLS]);
-        wait(&sm.tfull[b], bph);
+        wait(&sm.mdone[b], bph);
         tc_fence_after();
+        if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256 && e == 0 && lane == 0)
+          p.trace[512 + g_it] = clock64();
         const uint32_t taddr = tlane + b * BT;
 #pragma unroll
         for (int ch = 0; ch < COLS / CH; ++ch) {
@@ -333,7 +337,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
               const int m = mc0 + ch * CH + k;
-              const int v = static_cast<int>(r[k] - kMagicBits);
+              const int v = static_cast<int>(r[k]);
               if (m < p.M)
                 p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
             }
@@ -342,10 +346,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           for (int k4 = 0; k4 < ((kMode & 1) ? 0 : CH / 4); ++k4) {
             const float4 s = sa4[ch * (CH / 4) + k4];
             const int j = ch * (CH / 2) + 2 * k4;
-            const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
-                                                     __uint_as_float(r[4 * k4 + 1])), sw2, nc2);
-            const float2 g1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 2]),
-                                                     __uint_as_float(r[4 * k4 + 3])), sw2, nc2);
+            const float2 g0 = __ffma2_rn(make_float2(biased(r[4 * k4 + 0]), biased(r[4 * k4 + 1])),
+                                         sw2, nc2);
+            const float2 g1 = __ffma2_rn(make_float2(biased(r[4 * k4 + 2]), biased(r[4 * k4 + 3])),
+                                         sw2, nc2);
             acc[j] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[j]);
             acc[j + 1] = __ffma2_rn(make_float2(s.z, s.w), g1, acc[j + 1]);
           }
@@ -459,14 +463,24 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
     if (mode == 15) kern = w4a4_gemm_kernel<BT, false, 15>;
     if (mode == 16) kern = w4a4_gemm_kernel<BT, false, 16>;
     if (mode == 23) kern = w4a4_gemm_kernel<BT, false, 23>;
-    if (mode == 47) kern = w4a4_gemm_kernel<BT, false, 47>;
-    if (mode == 32) kern = w4a4_gemm_kernel<BT, false, 32>;
+
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+  static long long* trace = nullptr;
+  static const bool want_trace = getenv("ATOM_GEMM_TRACE") != nullptr;   // development probe only
+  if (want_trace && trace == nullptr) cudaMalloc(&trace, 3 * 256 * sizeof(long long));
+  p.trace = want_trace ? trace : nullptr;
   kern<<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
+  if (want_trace) {
+    long long h[768];
+    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "trace g: ufull_arrive mma_issue epi_seen (clk rel. to mma_issue[0])\n");
+    for (int g = 0; g < 256 && g < p.G * 2; ++g)
+      fprintf(stderr, "%3d %9lld %9lld %9lld\n", g, h[256 + g] - h[0], h[g] - h[0], h[512 + g] - h[0]);
+  }
   return cudaGetLastError();
 }
 
