@@ -225,52 +225,37 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
     G = K // 128
 
     # ---------------- inputs (synthetic, seeded; identical bytes on every rank) ----------------
+    from paper_2310_19102_b200 import tp
     X = synth.activations(M, K, args.seed)
     perm = synth.perm_for(K, args.seed)
     if shard == "n":
-        n0, n1 = rank * N // P, (rank + 1) * N // P
-        assert (n1 - n0) % 128 == 0, "N-shard must be a multiple of 128 columns"
-        W = synth.weights(N, K, args.seed, rows=(n0, n1))
-        perm_r, K_r, ko_r = perm, K, K_OUT
-        Wd = torch.from_numpy(W).to(dev)
-    else:  # K-shard along group boundaries; INT8 outlier group on the last rank
-        g0, g1 = rank * G // P, (rank + 1) * G // P
-        perm_r = np.ascontiguousarray(perm[g0 * 128:g1 * 128])
-        K_r, ko_r = (g1 - g0) * 128, (K_OUT if rank == P - 1 else 0)
+        n0, n1 = tp.n_shard_rows(N, P, rank)
+        W = synth.weights(N, K, args.seed, rows=(n0, n1))   # this rank's rows only
+    else:
         W = synth.weights(N, K, args.seed)
-        Wd = torch.from_numpy(W).to(dev)
         n0, n1 = 0, N
     Nr = n1 - n0
-    pd = torch.from_numpy(perm_r).to(dev)
     xd = torch.from_numpy(X).to(dev)
-    wq = atom.quantize_weights(Wd, pd, K=K_r, k_outlier=ko_r)          # a0, offline
-    del Wd
-    aq = atom.reorder_quantize(xd, pd, K=K_r, k_outlier=ko_r)          # output buffers reused
-    if shard == "n":
-        c_loc = torch.empty((M, Nr), dtype=torch.float16, device=dev)
-        c_all = torch.empty((P, M, Nr), dtype=torch.float16, device=dev) if P > 1 else None
-    else:
-        c_loc = torch.empty((M, N), dtype=torch.float32, device=dev)
-        c_all = torch.empty((M, N), dtype=torch.float16, device=dev)
+    layer = tp.TensorParallelLinear(torch.from_numpy(W).to(dev), torch.from_numpy(perm).to(dev),
+                                    K, shard)                  # a0: weights quantized offline
+    K_r = layer.K
+    del W
+    aq = layer.quantize(xd)                                    # output buffers reused below
+    c_loc = layer.gemm(aq)
+    c_all = (torch.empty((P, M, Nr), dtype=torch.float16, device=dev) if shard == "n"
+             else torch.empty((M, N), dtype=torch.float16, device=dev)) if P > 1 else None
     torch.cuda.synchronize()
 
     launches = [0]
 
     def step(x_in):
-        atom.reorder_quantize(x_in, pd, K=K_r, k_outlier=ko_r, out=aq)
+        layer.quantize(x_in, out=aq)
         launches[0] += atom.last_launch_count()
-        atom.w4a4_gemm(aq, wq, out=c_loc)
+        layer.gemm(aq, out=c_loc)
         launches[0] += atom.last_launch_count()
 
     def collective():
-        if P == 1:
-            return c_loc
-        if shard == "n":
-            dist.all_gather_into_tensor(c_all, c_loc)
-            return c_all
-        dist.all_reduce(c_loc)
-        c_all.copy_(c_loc)
-        return c_all
+        return layer.combine(c_loc, c_all)
 
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(2 * l2 + (64 << 20), dtype=torch.uint8, device=dev)
@@ -302,10 +287,10 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
             if not args.no_flush:
                 flush_l2()
             E[i][0].record()
-            atom.reorder_quantize(xd, pd, K=K_r, k_outlier=ko_r, out=aq)
+            layer.quantize(xd, out=aq)
             launches[0] += atom.last_launch_count()
             E[i][1].record()
-            atom.w4a4_gemm(aq, wq, out=c_loc)
+            layer.gemm(aq, out=c_loc)
             launches[0] += atom.last_launch_count()
             E[i][2].record()
             collective()

@@ -35,17 +35,29 @@
 
 namespace atom {
 
-constexpr int kStages = 4;      // packed-tile TMA ring depth
-constexpr int kUbuf = 4;        // unpacked int8 operand buffers
-constexpr int kThreads = 448;   // 14 warps
-constexpr int kUnpackWarp0 = 2; // warps 2..5
-constexpr int kNumUnpackWarps = 4;
-constexpr int kEpiWarp0 = 6;    // warps 6..13
+// Warp roles (16 warps, 4 warpgroups):
+//   WG0: warp 0 producer (scales via cp.async + TMA), warp 1 MMA issuer, warps 2-3 unpack
+//   WG1: warps 4-7 unpack
+//   WG2, WG3: warps 8-15 epilogue (warp % 4 = TMEM lane quarter; WG2 = token columns [0, BT/2),
+//             WG3 = [BT/2, BT))
+// setmaxnreg moves registers from WG0/WG1 (72 each) to the epilogue warpgroups (184 each), which
+// hold the fp32 accumulators of a 128 x BT tile (BT/2 per thread).
+constexpr int kThreads = 512;
+constexpr int kUnpackWarp0 = 2;
+constexpr int kNumUnpackWarps = 6;
+constexpr int kEpiWarp0 = 8;
 constexpr int kNumEpiWarps = 8;
+constexpr int kRegsLow = 64, kRegsHigh = 192;           // 8*32*64 + 8*32*192 = 65536
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
-constexpr int kSRing = 16;      // group-scale ring depth
-constexpr int kTBuf = 4;        // TMEM accumulator buffers (4 x BT <= 512 columns)
-static_assert(kTBuf == kUbuf, "one mdone barrier ring serves both the operand and TMEM rings");
+constexpr int kStages = 4;      // packed-tile TMA ring depth
+constexpr int kSRing = 8;       // group-scale ring depth
+
+template <int BT> struct Cfg {
+  static constexpr int kRing = BT >= 256 ? 2 : 4;       // unpacked operands == TMEM accumulators
+  static constexpr uint32_t kTmemCols = kRing * BT <= 32 ? 32 : kRing * BT <= 64 ? 64
+                                      : kRing * BT <= 128 ? 128 : kRing * BT <= 256 ? 256 : 512;
+  static_assert(kRing * BT <= 512, "TMEM holds at most 512 columns");
+};
 
 constexpr uint32_t kMagicBits = 0x4B400000u;   // bit pattern of 1.5*2^23
 constexpr float kMagic = 12582912.0f;          // 1.5*2^23
@@ -63,25 +75,21 @@ struct GemmParams {
 
 template <int BT>
 struct __align__(1024) GemmSmem {
-  uint8_t ubuf_w[kUbuf][kTileN * 128];  // unpacked weight group, SW128 K-major
-  uint8_t ubuf_a[kUbuf][BT * 128];      // unpacked activation group, SW128 K-major
+  static constexpr int R = Cfg<BT>::kRing;
+  uint8_t ubuf_w[R][kTileN * 128];      // unpacked weight group, SW128 K-major
+  uint8_t ubuf_a[R][BT * 128];          // unpacked activation group, SW128 K-major
   uint8_t stage_w[kStages][kTileN * 64];// packed weight group (or half of the INT8 group)
   uint8_t stage_a[kStages][BT * 64];    // packed activation group
   float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
   float ssa[kSRing][BT];                // activation scales of a group
+  float oscr[kNumEpiWarps][4][72];      // per-warp 8x8 transpose scratch for the tile output
   uint64_t full[kStages], empty[kStages];
-  uint64_t ufull[kUbuf];
-  uint64_t mdone[kUbuf];                // MMAs of a group done: operands free + partial ready
-  uint64_t tempty[kTBuf];
+  uint64_t ufull[R];
+  uint64_t mdone[R];                    // MMAs of a group done: operands free + partial ready
+  uint64_t tempty[R];
   uint64_t sready[kSRing], sfree[kSRing];
   uint32_t tmem_base;
 };
-
-template <int BT>
-__host__ __device__ constexpr uint32_t tmem_cols() {
-  return (kTBuf * BT) <= 32 ? 32 : (kTBuf * BT) <= 64 ? 64 : (kTBuf * BT) <= 128 ? 128
-       : (kTBuf * BT) <= 256 ? 256 : 512;
-}
 
 // rotl(v, 4) & 0xF0F0F0F0 == (v << 4) & 0xF0F0F0F0, but as SHF.L.W + LOP3 on the integer pipe
 // (a plain shift is compiled to IMAD.SHL on the FMA pipe, which the epilogue saturates).
@@ -91,54 +99,56 @@ __device__ __forceinline__ uint32_t lo_nib(uint32_t v) {
 __device__ __forceinline__ uint4 unpack_lo(uint4 v) {  // even channels -> 16*q bytes
   return make_uint4(lo_nib(v.x), lo_nib(v.y), lo_nib(v.z), lo_nib(v.w));
 }
-// float(1.5*2^23 + R) from the int32 partial R, |R| < 2^22: the low 23 bits of R with bit 22
-// flipped are R + 2^22 in [0, 2^23); OR-ing the exponent of 2^23 gives 2^23 + 2^22 + R exactly.
-__device__ __forceinline__ float biased(uint32_t r) {
-  return __uint_as_float((r & 0x007FFFFFu) ^ kMagicBits);
-}
-
 __device__ __forceinline__ uint4 unpack_hi(uint4 v) {  // odd channels -> 16*q bytes
   return make_uint4(v.x & 0xF0F0F0F0u, v.y & 0xF0F0F0F0u, v.z & 0xF0F0F0F0u, v.w & 0xF0F0F0F0u);
 }
+// float(1.5*2^23 + R) from the int32 partial R, |R| < 2^22: the low 23 bits of R with bit 22
+// flipped are R + 2^22 in [0, 2^23); OR-ing the exponent of 2^23 gives 2^23 + 2^22 + R exactly.
+// One LOP3; `magic` holds kMagicBits in a register.
+__device__ __forceinline__ float biased(uint32_t r, uint32_t magic) {
+  return __uint_as_float(and_xor(r, 0x007FFFFFu, magic));
+}
 
-// One operand tile of ROWS rows: packed stage [ROWS][64 B] -> unpacked SW128 [ROWS][128 B].
-// Thread ut owns the 16-byte packed chunk (ut & 3) of rows (ut >> 2) + 32k; rows 32 apart share
-// their swizzle phase, so every address below is a per-thread base plus an immediate.
-template <int ROWS>
-__device__ __forceinline__ void unpack_tile(const uint8_t* stage, uint8_t* ubuf, int ut,
-                                            bool int4, int h) {
-  constexpr int KR = ROWS / 32;
-  const uint32_t r0 = static_cast<uint32_t>(ut) >> 2, c = static_cast<uint32_t>(ut) & 3u;
+// KR rows of an operand tile, ROW_STEP apart (a multiple of 8, so all share one swizzle phase):
+// packed stage [rows][64 B] -> unpacked SW128 [rows][128 B].  This thread owns the 16-byte
+// packed chunk c of rows r0 + k*ROW_STEP; every address is a per-thread base plus an immediate.
+template <int KR, int ROW_STEP>
+__device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf, uint32_t r0,
+                                            uint32_t c, bool int4, int h) {
+  static_assert(ROW_STEP % 8 == 0, "rows must share the swizzle phase");
   const uint32_t r7 = r0 & 7u;
-  const uint8_t* src = stage + ut * 16;
+  const uint8_t* src = stage + r0 * 64 + c * 16;
   uint4 v[KR];
 #pragma unroll
-  for (int k = 0; k < KR; ++k) v[k] = *reinterpret_cast<const uint4*>(src + k * 32 * 64);
+  for (int k = 0; k < KR; ++k) v[k] = *reinterpret_cast<const uint4*>(src + k * ROW_STEP * 64);
   uint8_t* dst = ubuf + r0 * 128;
   if (int4) {
     const uint32_t olo = ((2 * c) ^ r7) << 4, ohi = ((2 * c + 1) ^ r7) << 4;
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
-      *reinterpret_cast<uint4*>(dst + k * 32 * 128 + olo) = unpack_lo(v[k]);
-      *reinterpret_cast<uint4*>(dst + k * 32 * 128 + ohi) = unpack_hi(v[k]);
+      *reinterpret_cast<uint4*>(dst + k * ROW_STEP * 128 + olo) = unpack_lo(v[k]);
+      *reinterpret_cast<uint4*>(dst + k * ROW_STEP * 128 + ohi) = unpack_hi(v[k]);
     }
   } else {
     const uint32_t o = ((4 * h + c) ^ r7) << 4;
 #pragma unroll
-    for (int k = 0; k < KR; ++k) *reinterpret_cast<uint4*>(dst + k * 32 * 128 + o) = v[k];
+    for (int k = 0; k < KR; ++k) *reinterpret_cast<uint4*>(dst + k * ROW_STEP * 128 + o) = v[k];
   }
 }
 
 // kMode (development timing probes, never used for results): bit 0 = epilogue skips its
 // arithmetic; bit 1 = unpack skips its data movement; bit 2 = producer skips the TMA loads;
-// bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint.
+// bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint;
+// bit 5 = no output stores.
 template <int BT, bool kDebug, int kMode = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                  const __grid_constant__ CUtensorMap tm_aq4,
                  const __grid_constant__ CUtensorMap tm_wq8,
                  const __grid_constant__ CUtensorMap tm_aq8, const GemmParams p) {
-  static_assert(BT % 32 == 0 && BT >= 32 && BT * kTBuf <= 512, "token tile");
+  static_assert(BT % 32 == 0 && BT >= 32 && BT <= 256, "token tile");
+  constexpr int R = Cfg<BT>::kRing;
+  constexpr uint32_t kTmemCols = Cfg<BT>::kTmemCols;
   auto wait = [](uint64_t* bar, uint32_t parity) {
     if constexpr ((kMode & 16) != 0) mbar_wait_spin(bar, parity);
     else mbar_wait(bar, parity);
@@ -148,19 +158,16 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  constexpr uint32_t kTmemCols = tmem_cols<BT>();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kNumUnpackWarps);
     }
-    for (int u = 0; u < kUbuf; ++u) {
+    for (int u = 0; u < R; ++u) {
       mbar_init(&sm.ufull[u], kNumUnpackWarps);
       mbar_init(&sm.mdone[u], 1);
-    }
-    for (int b = 0; b < kTBuf; ++b) {
-      mbar_init(&sm.tempty[b], kNumEpiWarps);
+      mbar_init(&sm.tempty[u], kNumEpiWarps);
     }
     for (int r = 0; r < kSRing; ++r) {
       mbar_init(&sm.sready[r], 32);  // one cp.async-arrive per producer-warp thread
@@ -183,11 +190,12 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   const int G = p.G, G4 = p.G4;
   const int loads_per_tile = G4 + (p.k_o ? 2 : 0);
 
+  if (warp < kEpiWarp0) setmaxnreg_dec<kRegsLow>();
   if (warp == 0) {
     // ===================== producer warp: group scales (cp.async) + TMA =====================
-    // The scales of a group are staged into the scale ring when its first stage is loaded, i.e.
-    // kStages + kUbuf + kTBuf groups ahead of the epilogue, which hides the L2 latency of the
-    // 4-byte copies (cp.async works for any M; TMA would need 16-byte aligned rows).
+    // The scales of a group are staged into the scale ring when its first stage is loaded,
+    // several groups ahead of the epilogue, which hides the L2 latency of the 4-byte copies
+    // (cp.async works for any M; TMA would need 16-byte aligned rows).
     uint32_t it = 0, g_it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int n0 = (tile / p.m_tiles) * kTileN;
@@ -236,40 +244,49 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       uint32_t g_it = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         for (int t = 0; t < G; ++t, ++g_it) {
-          const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
-          const uint32_t b = g_it % kTBuf, bph = (g_it / kTBuf) & 1;
-          wait(&sm.tempty[b], bph ^ 1);
-          tc_fence_after();
-          const uint32_t d = tmem + b * BT;
-          wait(&sm.ufull[u], uph);
+          const uint32_t u = g_it % R, uph = (g_it / R) & 1;
+          wait(&sm.tempty[u], uph);            // epilogue drained (and re-armed) this accumulator
+          wait(&sm.ufull[u], uph);             // operands unpacked
           tc_fence_after();
           if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256) p.trace[g_it] = clock64();
+          const uint32_t d = tmem + u * BT;
           const uint32_t a_base = smem_u32(sm.ubuf_w[u]);
           const uint32_t b_base = smem_u32(sm.ubuf_a[u]);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
+            // even buffers hold the magic 1.5*2^23 (re-armed by the epilogue): always accumulate;
+            // odd buffers start from zero and the epilogue converts with one LOP3
             umma_i8(d, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
-                    k > 0 ? 1u : 0u);
+                    (k > 0 || (u & 1u) == 0) ? 1u : 0u);
           umma_commit(&sm.mdone[u]);
         }
       }
     }
   } else if (warp < kEpiWarp0) {
     // ===================== unpack warps: packed INT4 -> int8 (16*q), SW128 =====================
-    const int ut = threadIdx.x - kUnpackWarp0 * 32;  // 0..127
+    // threads 0-127: the 128 weight rows + activation rows [0, min(BT,128));
+    // threads 128-191: activation rows [128, BT) (BT = 256 only).
+    const int ut = threadIdx.x - kUnpackWarp0 * 32;  // 0..191
+    const uint32_t r0 = static_cast<uint32_t>(ut & 127) >> 2, c = static_cast<uint32_t>(ut) & 3u;
     uint32_t it = 0, g_it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       for (int t = 0; t < G; ++t, ++g_it) {
-        const uint32_t u = g_it % kUbuf, uph = (g_it / kUbuf) & 1;
-        wait(&sm.mdone[u], uph ^ 1);   // MMAs of group g - kUbuf finished with this buffer
+        const uint32_t u = g_it % R, uph = (g_it / R) & 1;
+        wait(&sm.mdone[u], uph ^ 1);   // MMAs of group g - R finished with this buffer
         const bool int4 = t < G4;
         const int nh = int4 ? 1 : 2;
         for (int h = 0; h < nh; ++h, ++it) {
           const uint32_t s = it % kStages, ph = (it / kStages) & 1;
           wait(&sm.full[s], ph);
           if constexpr ((kMode & 2) == 0) {
-            unpack_tile<kTileN>(sm.stage_w[s], sm.ubuf_w[u], ut, int4, h);
-            unpack_tile<BT>(sm.stage_a[s], sm.ubuf_a[u], ut, int4, h);
+            if (ut < 128) {
+              unpack_rows<4, 32>(sm.stage_w[s], sm.ubuf_w[u], r0, c, int4, h);
+              unpack_rows<(BT < 128 ? BT : 128) / 32, 32>(sm.stage_a[s], sm.ubuf_a[u], r0, c,
+                                                          int4, h);
+            } else if constexpr (BT > 128) {
+              unpack_rows<(BT - 128) / 16, 16>(sm.stage_a[s] + 128 * 64, sm.ubuf_a[u] + 128 * 128,
+                                               r0 & 15u, c, int4, h);
+            }
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -283,13 +300,27 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     }
   } else {
     // ===================== epilogue warps =====================
+    setmaxnreg_inc<kRegsHigh>();
     constexpr int COLS = BT / 2;  // tokens per thread
-    constexpr int CH = COLS >= 32 ? 32 : 16;
+    constexpr int CH = (COLS >= 32 && COLS < 128) ? 32 : 16;   // x16 at COLS = 128: register budget
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;       // TMEM lane quarter this warp may access
     const int half = e >> 2;
     const int n_local = q * 32 + lane;
     const uint32_t tlane = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * COLS;
+    const uint32_t magic = kMagicBits;
+    // Even accumulator buffers carry the magic bias (tcgen05.st, TMEM write port); odd ones are
+    // converted with a LOP3 (ALU).  Splitting the conversion between the two keeps both the TMEM
+    // bandwidth and the ALU pipe below the MMA time.
+#pragma unroll
+    for (int b = 0; b < R; b += 2)
+#pragma unroll
+      for (int ch = 0; ch < COLS / CH; ++ch) tmem_st_const<CH>(tlane + b * BT + ch * CH, magic);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0)
+      for (int b = 0; b < R; ++b) mbar_arrive(&sm.tempty[b]);
     uint32_t g_it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int n0 = (tile / p.m_tiles) * kTileN;
@@ -300,7 +331,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 #pragma unroll
       for (int j = 0; j < COLS / 2; ++j) acc[j] = make_float2(0.0f, 0.0f);
       for (int t = 0; t < G; ++t, ++g_it) {
-        const uint32_t b = g_it % kTBuf, bph = (g_it / kTBuf) & 1;
+        const uint32_t b = g_it % R, bph = (g_it / R) & 1;
         const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
         const bool int4 = t < G4;
         wait(&sm.sready[sr], sph);
@@ -318,26 +349,33 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256 && e == 0 && lane == 0)
           p.trace[512 + g_it] = clock64();
         const uint32_t taddr = tlane + b * BT;
+        const bool prefilled = (b & 1u) == 0;
 #pragma unroll
         for (int ch = 0; ch < COLS / CH; ++ch) {
           uint32_t r[CH];
           if constexpr ((kMode & 8) == 0) {
             tmem_ld<CH>(taddr + ch * CH, r);
             tmem_ld_wait();
+            if (prefilled) tmem_st_const<CH>(taddr + ch * CH, magic);   // re-arm
           } else {
 #pragma unroll
             for (int k = 0; k < CH; ++k) r[k] = 0;
           }
           if (ch == COLS / CH - 1) {
+            if (prefilled) tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.tempty[b]);
+          }
+          if (!prefilled) {
+#pragma unroll
+            for (int k = 0; k < CH; ++k) r[k] = __float_as_uint(biased(r[k], magic));
           }
           if constexpr (kDebug) {
 #pragma unroll
             for (int k = 0; k < CH; ++k) {
               const int m = mc0 + ch * CH + k;
-              const int v = static_cast<int>(r[k]);
+              const int v = static_cast<int>(r[k] - kMagicBits);
               if (m < p.M)
                 p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
             }
@@ -346,10 +384,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           for (int k4 = 0; k4 < ((kMode & 1) ? 0 : CH / 4); ++k4) {
             const float4 s = sa4[ch * (CH / 4) + k4];
             const int j = ch * (CH / 2) + 2 * k4;
-            const float2 g0 = __ffma2_rn(make_float2(biased(r[4 * k4 + 0]), biased(r[4 * k4 + 1])),
-                                         sw2, nc2);
-            const float2 g1 = __ffma2_rn(make_float2(biased(r[4 * k4 + 2]), biased(r[4 * k4 + 3])),
-                                         sw2, nc2);
+            const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
+                                                     __uint_as_float(r[4 * k4 + 1])), sw2, nc2);
+            const float2 g1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 2]),
+                                                     __uint_as_float(r[4 * k4 + 3])), sw2, nc2);
             acc[j] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[j]);
             acc[j + 1] = __ffma2_rn(make_float2(s.z, s.w), g1, acc[j + 1]);
           }
@@ -358,15 +396,58 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (lane == 0) mbar_arrive(&sm.sfree[sr]);
       }
       // ---- tile output ----
+      // Thread = output channel n, registers = tokens m; C is [M][N] with n contiguous.  Each
+      // 8x8 (m, n) block is transposed through a per-warp shared scratch so that every lane
+      // stores 8 consecutive n of one token as one 16-byte vector (4 lanes per 64-byte row
+      // segment), instead of 2-byte scattered stores.
+      if constexpr ((kMode & 32) != 0) continue;
+      const int ga = lane >> 3, gb = lane & 7;
+      float* scr = &sm.oscr[e][ga][0];
+      const int nn = n0 + q * 32 + 8 * ga;   // first of the 8 channels this lane stores
+      if (p.c_f32) {
 #pragma unroll
-      for (int j = 0; j < COLS; ++j) {
-        const int m = mc0 + j;
-        const float v = (j & 1) ? acc[j >> 1].y : acc[j >> 1].x;
-        if (m < p.M) {
-          if (p.c_f32)
-            static_cast<float*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = v;
-          else
-            static_cast<__half*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = __float2half_rn(v);
+        for (int c8 = 0; c8 < COLS / 8; ++c8) {
+          float4* w = reinterpret_cast<float4*>(scr + gb * 8);
+          w[0] = make_float4(acc[4 * c8].x, acc[4 * c8].y, acc[4 * c8 + 1].x, acc[4 * c8 + 1].y);
+          w[1] = make_float4(acc[4 * c8 + 2].x, acc[4 * c8 + 2].y, acc[4 * c8 + 3].x,
+                             acc[4 * c8 + 3].y);
+          __syncwarp();
+          float v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = scr[k * 8 + gb];
+          __syncwarp();
+          const int m = mc0 + 8 * c8 + gb;
+          if (m < p.M) {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.c) +
+                                                    static_cast<int64_t>(m) * p.ldc + nn);
+            dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+            dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+          }
+        }
+      } else {
+        // fp16 first: halves the live registers before the transpose
+        uint32_t hp[COLS / 2];
+#pragma unroll
+        for (int j = 0; j < COLS / 2; ++j) {
+          const __half2 h = __floats2half2_rn(acc[j].x, acc[j].y);
+          hp[j] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        uint16_t* hs = reinterpret_cast<uint16_t*>(scr);
+        __half* crow = static_cast<__half*>(p.c) + static_cast<int64_t>(mc0 + gb) * p.ldc + nn;
+        const int64_t step = 8 * p.ldc;
+#pragma unroll
+        for (int c8 = 0; c8 < COLS / 8; ++c8) {
+          *reinterpret_cast<uint4*>(hs + gb * 8) =
+              make_uint4(hp[4 * c8], hp[4 * c8 + 1], hp[4 * c8 + 2], hp[4 * c8 + 3]);
+          __syncwarp();
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            w[k] = static_cast<uint32_t>(hs[(2 * k) * 8 + gb]) |
+                   (static_cast<uint32_t>(hs[(2 * k + 1) * 8 + gb]) << 16);
+          __syncwarp();
+          if (mc0 + 8 * c8 + gb < p.M)
+            *reinterpret_cast<uint4*>(crow + c8 * step) = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
     }
@@ -452,7 +533,7 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
 
   const size_t smem = sizeof(GemmSmem<BT>) + 1024;
   auto kern = p.debug ? w4a4_gemm_kernel<BT, true> : w4a4_gemm_kernel<BT, false>;
-  if constexpr (BT == 128) {
+  if constexpr (BT == 256) {
     static const char* mode_env = getenv("ATOM_GEMM_PROBE_MODE");   // development probe only
     const int mode = mode_env ? atoi(mode_env) : 0;
     if (mode == 1) kern = w4a4_gemm_kernel<BT, false, 1>;
@@ -463,6 +544,8 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
     if (mode == 15) kern = w4a4_gemm_kernel<BT, false, 15>;
     if (mode == 16) kern = w4a4_gemm_kernel<BT, false, 16>;
     if (mode == 23) kern = w4a4_gemm_kernel<BT, false, 23>;
+    if (mode == 32) kern = w4a4_gemm_kernel<BT, false, 32>;
+
 
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -491,7 +574,8 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, cudaStream_t stream, int num_sms
   const int64_t n_tiles = a.N / kTileN;
   auto tiles = [&](int bt) { return n_tiles * ((a.M + bt - 1) / bt); };
   cudaError_t e;
-  if (tiles(128) >= num_sms) e = launch_bt<128>(a, stream, num_sms);
+  if (tiles(256) >= num_sms) e = launch_bt<256>(a, stream, num_sms);
+  else if (tiles(128) >= num_sms) e = launch_bt<128>(a, stream, num_sms);
   else if (tiles(64) >= num_sms) e = launch_bt<64>(a, stream, num_sms);
   else e = launch_bt<32>(a, stream, num_sms);
   if (e == cudaSuccess) *launches = 1;

@@ -85,6 +85,18 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // ---------------------------------------------------------------------------------------------
+// register reallocation between warpgroups (whole warpgroup executes it)
+// ---------------------------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+// ---------------------------------------------------------------------------------------------
 // cp.async (Ampere-style LDGSTS) with mbarrier completion
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async_4(void* dst_smem, const void* src_gmem) {
@@ -191,6 +203,30 @@ __device__ __forceinline__ void tmem_st16_const(uint32_t taddr, uint32_t v) {
       "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
       "r"(v)
       : "memory");
+}
+
+// Warp-collective: store the same 32-bit value to 32 consecutive columns of this thread's lane.
+__device__ __forceinline__ void tmem_st32_const(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_st_const(uint32_t taddr, uint32_t v) {
+  if constexpr (N == 16) tmem_st16_const(taddr, v);
+  else tmem_st32_const(taddr, v);
+}
+
+// (a & b) ^ c in one LOP3 (the compiler splits it when b and c are both immediates).
+__device__ __forceinline__ uint32_t and_xor(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x6A;" : "=r"(d) : "r"(a), "n"(0x007FFFFF), "r"(c));
+  (void)b;
+  return d;
 }
 
 __device__ __forceinline__ void tmem_st_wait() {

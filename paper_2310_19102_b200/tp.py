@@ -56,7 +56,8 @@ class TensorParallelLinear:
 
         import paper_2310_19102_b200 as atom
         self.atom, self.dist = atom, dist
-        self.P, self.r = dist.get_world_size(), dist.get_rank()
+        init = dist.is_available() and dist.is_initialized()
+        self.P, self.r = (dist.get_world_size(), dist.get_rank()) if init else (1, 0)
         self.shard = shard
         self.clip_a, self.clip_int8 = clip_a, clip_int8
         if shard == "n":
@@ -80,15 +81,27 @@ class TensorParallelLinear:
         return self.atom.w4a4_gemm(a, self.w, out=out, out_dtype=dt)
 
     def combine(self, local, gathered=None):
-        """The collective step (a6)."""
+        """The collective step (a6).  NCCL in production; the gloo branch (CPU staging) exists
+        only so the sharded path can be exercised with several ranks on one GPU in tests."""
         if self.P == 1:
             return local if local.dtype == self.torch.float16 else local.half()
+        gloo = self.dist.get_backend() == "gloo"
         if self.shard == "n":
             if gathered is None:
                 gathered = local.new_empty((self.P,) + tuple(local.shape))
-            self.dist.all_gather_into_tensor(gathered, local)
+            if gloo:
+                parts = [self.torch.empty_like(local, device="cpu") for _ in range(self.P)]
+                self.dist.all_gather(parts, local.cpu())
+                gathered.copy_(self.torch.stack(parts))
+            else:
+                self.dist.all_gather_into_tensor(gathered, local)
             return gathered
-        self.dist.all_reduce(local)
+        if gloo:
+            h = local.cpu()
+            self.dist.all_reduce(h)
+            local.copy_(h)
+        else:
+            self.dist.all_reduce(local)
         return local.half() if gathered is None else gathered.copy_(local)
 
     def __call__(self, x):
