@@ -25,6 +25,7 @@
 //   * persistent CTAs (one per SM) walk output tiles; consecutive CTAs share the weight tile.
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -83,6 +84,7 @@ struct __align__(1024) GemmSmem {
   float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
   float ssa[kSRing][BT];                // activation scales of a group
   float oscr[kNumEpiWarps][4][72];      // per-warp 8x8 transpose scratch for the tile output
+  uint32_t magic4[4];                   // 4 copies of the magic bit pattern
   uint64_t full[kStages], empty[kStages];
   uint64_t ufull[R];
   uint64_t mdone[R];                    // MMAs of a group done: operands free + partial ready
@@ -139,7 +141,7 @@ __device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf,
 // kMode (development timing probes, never used for results): bit 0 = epilogue skips its
 // arithmetic; bit 1 = unpack skips its data movement; bit 2 = producer skips the TMA loads;
 // bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint;
-// bit 5 = no output stores.
+// bit 5 = no output stores; bit 6 = no magic prefill (every buffer converted with LOP3).
 template <int BT, bool kDebug, int kMode = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
@@ -149,6 +151,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   static_assert(BT % 32 == 0 && BT >= 32 && BT <= 256, "token tile");
   constexpr int R = Cfg<BT>::kRing;
   constexpr uint32_t kTmemCols = Cfg<BT>::kTmemCols;
+  constexpr bool kPrefillEven = (kMode & 64) == 0;   // even buffers carry the magic bias
   auto wait = [](uint64_t* bar, uint32_t parity) {
     if constexpr ((kMode & 16) != 0) mbar_wait_spin(bar, parity);
     else mbar_wait(bar, parity);
@@ -181,6 +184,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     tma_prefetch_desc(&tm_wq8);
     tma_prefetch_desc(&tm_aq8);
   }
+  if (threadIdx.x < 4) sm.magic4[threadIdx.x] = kMagicBits;
   if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
   tc_fence_before();
   __syncthreads();
@@ -257,7 +261,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             // even buffers hold the magic 1.5*2^23 (re-armed by the epilogue): always accumulate;
             // odd buffers start from zero and the epilogue converts with one LOP3
             umma_i8(d, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
-                    (k > 0 || (u & 1u) == 0) ? 1u : 0u);
+                    (k > 0 || (kPrefillEven && (u & 1u) == 0)) ? 1u : 0u);
           umma_commit(&sm.mdone[u]);
         }
       }
@@ -309,14 +313,22 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     const int n_local = q * 32 + lane;
     const uint32_t tlane = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * COLS;
     const uint32_t magic = kMagicBits;
+    // Resident copies of the magic as tcgen05.st sources: loaded once from shared memory so the
+    // compiler cannot re-materialise them with 4 IMAD.MOV (FMA pipe) before every store.
+    uint32_t mg[4];
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(mg[0]), "=r"(mg[1]), "=r"(mg[2]), "=r"(mg[3])
+                 : "r"(smem_u32(sm.magic4)));
     // Even accumulator buffers carry the magic bias (tcgen05.st, TMEM write port); odd ones are
     // converted with a LOP3 (ALU).  Splitting the conversion between the two keeps both the TMEM
     // bandwidth and the ALU pipe below the MMA time.
+    if constexpr (kPrefillEven) {
 #pragma unroll
-    for (int b = 0; b < R; b += 2)
+      for (int b = 0; b < R; b += 2)
 #pragma unroll
-      for (int ch = 0; ch < COLS / CH; ++ch) tmem_st_const<CH>(tlane + b * BT + ch * CH, magic);
-    tmem_st_wait();
+        for (int ch = 0; ch < COLS / CH; ++ch) tmem_st_const<CH>(tlane + b * BT + ch * CH, magic);
+      tmem_st_wait();
+    }
     tc_fence_before();
     __syncwarp();
     if (lane == 0)
@@ -349,49 +361,58 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256 && e == 0 && lane == 0)
           p.trace[512 + g_it] = clock64();
         const uint32_t taddr = tlane + b * BT;
-        const bool prefilled = (b & 1u) == 0;
+        // Two specialised copies of the drain: even buffers are magic-prefilled (re-armed with
+        // tcgen05.st), odd ones are converted with a LOP3; no per-element select.
+        auto drain = [&](auto pre_tag) {
+          constexpr bool kPre = decltype(pre_tag)::value;
 #pragma unroll
-        for (int ch = 0; ch < COLS / CH; ++ch) {
-          uint32_t r[CH];
-          if constexpr ((kMode & 8) == 0) {
-            tmem_ld<CH>(taddr + ch * CH, r);
-            tmem_ld_wait();
-            if (prefilled) tmem_st_const<CH>(taddr + ch * CH, magic);   // re-arm
-          } else {
+          for (int ch = 0; ch < COLS / CH; ++ch) {
+            uint32_t r[CH];
+            if constexpr ((kMode & 8) == 0) {
+              tmem_ld<CH>(taddr + ch * CH, r);
+              tmem_ld_wait();
+              if constexpr (kPre) {   // re-arm with the magic
 #pragma unroll
-            for (int k = 0; k < CH; ++k) r[k] = 0;
-          }
-          if (ch == COLS / CH - 1) {
-            if (prefilled) tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.tempty[b]);
-          }
-          if (!prefilled) {
+                for (int k = 0; k < CH; k += 4) tmem_st4(taddr + ch * CH + k, mg);
+              }
+            } else {
 #pragma unroll
-            for (int k = 0; k < CH; ++k) r[k] = __float_as_uint(biased(r[k], magic));
-          }
-          if constexpr (kDebug) {
+              for (int k = 0; k < CH; ++k) r[k] = 0;
+            }
+            if (ch == COLS / CH - 1) {
+              if constexpr (kPre) tmem_st_wait();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&sm.tempty[b]);
+            }
+            if constexpr (!kPre) {
 #pragma unroll
-            for (int k = 0; k < CH; ++k) {
-              const int m = mc0 + ch * CH + k;
-              const int v = static_cast<int>(r[k] - kMagicBits);
-              if (m < p.M)
-                p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
+              for (int k = 0; k < CH; ++k) r[k] = __float_as_uint(biased(r[k], magic));
+            }
+            if constexpr (kDebug) {
+#pragma unroll
+              for (int k = 0; k < CH; ++k) {
+                const int m = mc0 + ch * CH + k;
+                const int v = static_cast<int>(r[k] - kMagicBits);
+                if (m < p.M)
+                  p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
+              }
+            }
+#pragma unroll
+            for (int k4 = 0; k4 < ((kMode & 1) ? 0 : CH / 4); ++k4) {
+              const float4 s = sa4[ch * (CH / 4) + k4];
+              const int j = ch * (CH / 2) + 2 * k4;
+              const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
+                                                       __uint_as_float(r[4 * k4 + 1])), sw2, nc2);
+              const float2 g1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 2]),
+                                                       __uint_as_float(r[4 * k4 + 3])), sw2, nc2);
+              acc[j] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[j]);
+              acc[j + 1] = __ffma2_rn(make_float2(s.z, s.w), g1, acc[j + 1]);
             }
           }
-#pragma unroll
-          for (int k4 = 0; k4 < ((kMode & 1) ? 0 : CH / 4); ++k4) {
-            const float4 s = sa4[ch * (CH / 4) + k4];
-            const int j = ch * (CH / 2) + 2 * k4;
-            const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
-                                                     __uint_as_float(r[4 * k4 + 1])), sw2, nc2);
-            const float2 g1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 2]),
-                                                     __uint_as_float(r[4 * k4 + 3])), sw2, nc2);
-            acc[j] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[j]);
-            acc[j + 1] = __ffma2_rn(make_float2(s.z, s.w), g1, acc[j + 1]);
-          }
-        }
+        };
+        if (kPrefillEven && (b & 1u) == 0) drain(std::true_type{});
+        else drain(std::false_type{});
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.sfree[sr]);
       }
@@ -545,6 +566,7 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
     if (mode == 16) kern = w4a4_gemm_kernel<BT, false, 16>;
     if (mode == 23) kern = w4a4_gemm_kernel<BT, false, 23>;
     if (mode == 32) kern = w4a4_gemm_kernel<BT, false, 32>;
+    if (mode == 64) kern = w4a4_gemm_kernel<BT, false, 64>;
 
 
   }

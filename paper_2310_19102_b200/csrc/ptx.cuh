@@ -215,6 +215,14 @@ __device__ __forceinline__ void tmem_st32_const(uint32_t taddr, uint32_t v) {
       : "memory");
 }
 
+// 4 columns from 4 caller-held registers (keeps the constant source registers resident instead
+// of re-materialising 16 copies per store).
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+
 template <int N>
 __device__ __forceinline__ void tmem_st_const(uint32_t taddr, uint32_t v) {
   if constexpr (N == 16) tmem_st16_const(taddr, v);
