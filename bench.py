@@ -298,10 +298,11 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    step_ms = [E[i][0].elapsed_time(E[i][3]) for i in range(args.steps)]
+    last = 3 if P > 1 else 2          # no collective at P = 1
+    step_ms = [E[i][0].elapsed_time(E[i][last]) for i in range(args.steps)]
     q_ms = [E[i][0].elapsed_time(E[i][1]) for i in range(args.steps)]
     g_ms = [E[i][1].elapsed_time(E[i][2]) for i in range(args.steps)]
-    c_ms = [E[i][2].elapsed_time(E[i][3]) for i in range(args.steps)]
+    c_ms = [E[i][2].elapsed_time(E[i][3]) if P > 1 else 0.0 for i in range(args.steps)]
     stats = torch.tensor([sum(step_ms) / args.steps, sum(q_ms) / args.steps,
                           sum(g_ms) / args.steps, sum(c_ms) / args.steps], device=dev,
                          dtype=torch.float64)

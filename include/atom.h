@@ -106,7 +106,13 @@ atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
  *   M >= 0 (M == 0 is a no-op), N % 128 == 0, K % 128 == 0, k_outlier in {0,128},
  *   ldc >= N, ldc % 8 == 0 (an N-shard can write its column block into a wider buffer).
  *   debug_partials  NULL, or int32 [K/128][M][N]: every exact group partial P_t (test-only).
- *   workspace       may be NULL when atom_w4a4_gemm_workspace_size() returns 0.
+ *   workspace       device buffer of at least atom_w4a4_gemm_workspace_size(M, N, K, k_outlier)
+ *                   bytes, 16-byte aligned (may be NULL when that size is 0).  Used when the
+ *                   output tiles alone cannot fill the GPU (small M): the K groups are split
+ *                   across CTAs, each split publishes fp32 partials there and the last one to
+ *                   finish reduces them.  Contents need not be initialised (the call clears its
+ *                   counters with one cudaMemsetAsync on `stream`).  Must not be shared by calls
+ *                   that may run concurrently.
  */
 atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
                              const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
@@ -115,7 +121,8 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
                              int32_t* debug_partials, void* workspace, size_t workspace_bytes,
                              void* stream);
 
-/* Bytes of device workspace atom_w4a4_gemm needs for this shape (0 today: no split-K). */
+/* Bytes of device workspace atom_w4a4_gemm needs for this shape on the CURRENT device (0 when
+ * no split-K is planned, or when the current device is not an sm_100 GPU). */
 size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier);
 
 /* Test helper: on `stream`, sets *ok_flag (device int32) to 1 iff perm[0..K) is a bijection of

@@ -107,11 +107,11 @@ atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
 }
 
 size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
-  (void)M;
-  (void)N;
-  (void)K;
   (void)k_outlier;
-  return 0;
+  if (M <= 0 || N <= 0 || N % 128 != 0 || K <= 0 || K % ATOM_GROUP != 0) return 0;
+  DeviceInfo dev;
+  if (current_device(&dev) != ATOM_OK) return 0;   // no sm_100 device: the GEMM cannot run
+  return atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
 }
 
 atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
@@ -126,8 +126,6 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
   if (M > 0x7fffffffLL || N > 0x7fffffffLL || K > (1LL << 30)) return ATOM_ERR_SHAPE;
   if (ldc < N || ldc % 8 != 0) return ATOM_ERR_SHAPE;
   if (!(c_dtype == ATOM_F16 || c_dtype == ATOM_F32)) return ATOM_ERR_ARG;
-  const size_t ws = atom_w4a4_gemm_workspace_size(M, N, K, k_outlier);
-  if (ws > 0 && (workspace == nullptr || workspace_bytes < ws)) return ATOM_ERR_WORKSPACE;
   if (M == 0) return ATOM_OK;
   if (!a_scales || !w_scales || !c) return ATOM_ERR_NULL;
   const bool has4 = K > k_outlier, has8 = k_outlier > 0;
@@ -140,6 +138,9 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
   DeviceInfo dev;
   atom_status_t st = current_device(&dev);
   if (st != ATOM_OK) return st;
+  const size_t ws = atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
+  if (ws > 0 && (workspace == nullptr || workspace_bytes < ws || !aligned16(workspace)))
+    return ATOM_ERR_WORKSPACE;
   atom::GemmArgs a;
   a.a_q4 = a_q4;
   a.a_q8 = a_q8;
@@ -156,8 +157,9 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
   a.c_f32 = c_dtype == ATOM_F32;
   a.debug_partials = debug_partials;
   int launches = 0;
-  cudaError_t e =
-      atom::launch_w4a4_gemm(a, static_cast<cudaStream_t>(stream), dev.num_sms, &launches);
+  cudaError_t e = atom::launch_w4a4_gemm(a, workspace, workspace_bytes,
+                                         static_cast<cudaStream_t>(stream), dev.num_sms,
+                                         &launches);
   if (e != cudaSuccess) return ATOM_ERR_CUDA;
   g_last_launches = launches;
   return ATOM_OK;

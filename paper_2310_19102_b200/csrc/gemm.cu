@@ -71,6 +71,9 @@ struct GemmParams {
   int32_t* debug;
   int M, N, G, G4, k_o, c_f32;
   int m_tiles, num_tiles;
+  int ksplit, num_items;     // split-K: item = tile * ksplit + split
+  float* partials;           // [num_tiles][ksplit][128][BT] fp32 (ksplit > 1)
+  int* counters;             // [num_tiles] arrival counters, zeroed by the launcher (ksplit > 1)
   long long* trace;   // development timeline probe (CTA 0): [3][256] clock64 stamps, or null
 };
 
@@ -138,6 +141,23 @@ __device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf,
   }
 }
 
+// One work item = (output tile, K split).  Splits cover contiguous group ranges; the INT8 outlier
+// group (the last one) therefore always lands in the last split.
+struct Item {
+  int n0, m0, t0, t1, tile, split;
+};
+template <int BT>
+__device__ __forceinline__ Item make_item(const GemmParams& p, int item) {
+  Item it;
+  it.tile = item / p.ksplit;
+  it.split = item - it.tile * p.ksplit;
+  it.n0 = (it.tile / p.m_tiles) * kTileN;
+  it.m0 = (it.tile % p.m_tiles) * BT;
+  it.t0 = it.split * p.G / p.ksplit;
+  it.t1 = (it.split + 1) * p.G / p.ksplit;
+  return it;
+}
+
 // kMode (development timing probes, never used for results): bit 0 = epilogue skips its
 // arithmetic; bit 1 = unpack skips its data movement; bit 2 = producer skips the TMA loads;
 // bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint;
@@ -191,8 +211,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  const int G = p.G, G4 = p.G4;
-  const int loads_per_tile = G4 + (p.k_o ? 2 : 0);
+  const int G4 = p.G4;
 
   if (warp < kEpiWarp0) setmaxnreg_dec<kRegsLow>();
   if (warp == 0) {
@@ -201,15 +220,13 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     // several groups ahead of the epilogue, which hides the L2 latency of the 4-byte copies
     // (cp.async works for any M; TMA would need 16-byte aligned rows).
     uint32_t it = 0, g_it = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int n0 = (tile / p.m_tiles) * kTileN;
-      const int m0 = (tile % p.m_tiles) * BT;
-      for (int l = 0; l < loads_per_tile; ++l, ++it) {
-        if (l <= G4) {   // first load of group t = l (the outlier group's 2nd half is l = G4+1)
-          const int t = l;
+    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+      const Item w = make_item<BT>(p, item);
+      for (int t = w.t0; t < w.t1; ++t, ++g_it) {
+        {
           const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
           wait(&sm.sfree[sr], sph ^ 1);
-          const float* ws = p.w_scales + static_cast<int64_t>(t) * p.N + n0;
+          const float* ws = p.w_scales + static_cast<int64_t>(t) * p.N + w.n0;
           const float* as = p.a_scales + static_cast<int64_t>(t) * p.M;
 #pragma unroll
           for (int j = lane; j < kTileN; j += 32) cp_async_4(&sm.ssw[sr][j], ws + j);
@@ -217,28 +234,29 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           for (int j = lane; j < BT; j += 32)
             // rows past M: any finite scale works, their partials are exactly zero (TMA
             // zero-fills out-of-range activation rows) and they are never stored
-            cp_async_4(&sm.ssa[sr][j], as + min(m0 + j, p.M - 1));
+            cp_async_4(&sm.ssa[sr][j], as + min(w.m0 + j, p.M - 1));
           cp_async_mbar_arrive(&sm.sready[sr]);
-          ++g_it;
         }
-        const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-        wait(&sm.empty[s], ph ^ 1);
-        if (lane == 0) {
-          if constexpr ((kMode & 4) != 0) {   // probe: no TMA traffic
-            mbar_arrive(&sm.full[s]);
-          } else {
-            mbar_arrive_expect_tx(&sm.full[s], kTileN * 64 + BT * 64);
-            if (l < G4) {
-              tma_load_2d(sm.stage_w[s], &tm_wq4, &sm.full[s], l * 64, n0);
-              tma_load_2d(sm.stage_a[s], &tm_aq4, &sm.full[s], l * 64, m0);
+        const int nh = t < G4 ? 1 : 2;      // the INT8 outlier group arrives in two halves
+        for (int h = 0; h < nh; ++h, ++it) {
+          const uint32_t s = it % kStages, ph = (it / kStages) & 1;
+          wait(&sm.empty[s], ph ^ 1);
+          if (lane == 0) {
+            if constexpr ((kMode & 4) != 0) {   // probe: no TMA traffic
+              mbar_arrive(&sm.full[s]);
             } else {
-              const int h = l - G4;
-              tma_load_2d(sm.stage_w[s], &tm_wq8, &sm.full[s], h * 64, n0);
-              tma_load_2d(sm.stage_a[s], &tm_aq8, &sm.full[s], h * 64, m0);
+              mbar_arrive_expect_tx(&sm.full[s], kTileN * 64 + BT * 64);
+              if (t < G4) {
+                tma_load_2d(sm.stage_w[s], &tm_wq4, &sm.full[s], t * 64, w.n0);
+                tma_load_2d(sm.stage_a[s], &tm_aq4, &sm.full[s], t * 64, w.m0);
+              } else {
+                tma_load_2d(sm.stage_w[s], &tm_wq8, &sm.full[s], h * 64, w.n0);
+                tma_load_2d(sm.stage_a[s], &tm_aq8, &sm.full[s], h * 64, w.m0);
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else if (warp == 1) {
@@ -246,8 +264,9 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_i8(kTileN, BT);
       uint32_t g_it = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        for (int t = 0; t < G; ++t, ++g_it) {
+      for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+        const Item w = make_item<BT>(p, item);
+        for (int t = w.t0; t < w.t1; ++t, ++g_it) {
           const uint32_t u = g_it % R, uph = (g_it / R) & 1;
           wait(&sm.tempty[u], uph);            // epilogue drained (and re-armed) this accumulator
           wait(&sm.ufull[u], uph);             // operands unpacked
@@ -273,8 +292,9 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     const int ut = threadIdx.x - kUnpackWarp0 * 32;  // 0..191
     const uint32_t r0 = static_cast<uint32_t>(ut & 127) >> 2, c = static_cast<uint32_t>(ut) & 3u;
     uint32_t it = 0, g_it = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      for (int t = 0; t < G; ++t, ++g_it) {
+    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+      const Item w = make_item<BT>(p, item);
+      for (int t = w.t0; t < w.t1; ++t, ++g_it) {
         const uint32_t u = g_it % R, uph = (g_it / R) & 1;
         wait(&sm.mdone[u], uph ^ 1);   // MMAs of group g - R finished with this buffer
         const bool int4 = t < G4;
@@ -334,15 +354,15 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     if (lane == 0)
       for (int b = 0; b < R; ++b) mbar_arrive(&sm.tempty[b]);
     uint32_t g_it = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      const int n0 = (tile / p.m_tiles) * kTileN;
-      const int m0 = (tile % p.m_tiles) * BT;
+    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+      const Item w = make_item<BT>(p, item);
+      const int n0 = w.n0, m0 = w.m0;
       const int n = n0 + n_local;
       const int mc0 = m0 + half * COLS;
       float2 acc[COLS / 2];
 #pragma unroll
       for (int j = 0; j < COLS / 2; ++j) acc[j] = make_float2(0.0f, 0.0f);
-      for (int t = 0; t < G; ++t, ++g_it) {
+      for (int t = w.t0; t < w.t1; ++t, ++g_it) {
         const uint32_t b = g_it % R, bph = (g_it / R) & 1;
         const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
         const bool int4 = t < G4;
@@ -415,6 +435,38 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         else drain(std::false_type{});
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.sfree[sr]);
+      }
+      // ---- split-K: publish this split's fp32 partial; the last split to arrive adds the
+      //      others' partials (same thread <-> element mapping) and stores the tile ----
+      if (p.ksplit > 1) {
+        float4* mine = reinterpret_cast<float4*>(
+            p.partials + ((static_cast<int64_t>(w.tile) * p.ksplit + w.split) * kTileN + n_local) * BT +
+            half * COLS);
+#pragma unroll
+        for (int j = 0; j < COLS / 4; ++j)
+          mine[j] = make_float4(acc[2 * j].x, acc[2 * j].y, acc[2 * j + 1].x, acc[2 * j + 1].y);
+        __threadfence();
+        named_bar_sync(1, kNumEpiWarps * 32);   // all epilogue threads of this CTA have written
+        __shared__ int arrived;
+        if (threadIdx.x == kEpiWarp0 * 32) arrived = atomicAdd(p.counters + w.tile, 1);
+        named_bar_sync(1, kNumEpiWarps * 32);
+        const bool last = arrived == p.ksplit - 1;
+        named_bar_sync(1, kNumEpiWarps * 32);   // everyone has read `arrived`
+        if (!last) continue;
+        __threadfence();
+        if (threadIdx.x == kEpiWarp0 * 32) p.counters[w.tile] = 0;   // self-cleaning
+        for (int sp = 0; sp < p.ksplit; ++sp) {
+          if (sp == w.split) continue;
+          const float4* other = reinterpret_cast<const float4*>(
+              p.partials + ((static_cast<int64_t>(w.tile) * p.ksplit + sp) * kTileN + n_local) * BT +
+              half * COLS);
+#pragma unroll
+          for (int j = 0; j < COLS / 4; ++j) {
+            const float4 o = __ldcg(other + j);
+            acc[2 * j].x += o.x; acc[2 * j].y += o.y;
+            acc[2 * j + 1].x += o.z; acc[2 * j + 1].y += o.w;
+          }
+        }
       }
       // ---- tile output ----
       // Thread = output channel n, registers = tokens m; C is [M][N] with n contiguous.  Each
@@ -521,7 +573,8 @@ static bool make_map_u8(CUtensorMap* map, const void* base, uint64_t cols, uint6
 }
 
 template <int BT>
-static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms) {
+static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* workspace,
+                             cudaStream_t stream, int num_sms, int* launches) {
   const int M = static_cast<int>(a.M), N = static_cast<int>(a.N), K = static_cast<int>(a.K);
   const int k_o = a.k_outlier;
   const uint64_t kp = static_cast<uint64_t>(K - k_o) / 2;
@@ -551,6 +604,17 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
   p.c_f32 = a.c_f32;
   p.m_tiles = (M + BT - 1) / BT;
   p.num_tiles = p.m_tiles * (N / kTileN);
+  p.ksplit = plan.ksplit;
+  p.num_items = p.num_tiles * p.ksplit;
+  p.counters = nullptr;
+  p.partials = nullptr;
+  if (plan.ksplit > 1) {
+    p.counters = static_cast<int*>(workspace);
+    p.partials = reinterpret_cast<float*>(static_cast<char*>(workspace) + plan.counter_bytes);
+    cudaError_t e = cudaMemsetAsync(p.counters, 0, plan.counter_bytes, stream);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+  }
 
   const size_t smem = sizeof(GemmSmem<BT>) + 1024;
   auto kern = p.debug ? w4a4_gemm_kernel<BT, true> : w4a4_gemm_kernel<BT, false>;
@@ -573,12 +637,13 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+  const int grid = p.num_items < num_sms ? p.num_items : num_sms;
   static long long* trace = nullptr;
   static const bool want_trace = getenv("ATOM_GEMM_TRACE") != nullptr;   // development probe only
   if (want_trace && trace == nullptr) cudaMalloc(&trace, 3 * 256 * sizeof(long long));
   p.trace = want_trace ? trace : nullptr;
   kern<<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
+  ++*launches;
   if (want_trace) {
     long long h[768];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
@@ -589,19 +654,53 @@ static cudaError_t launch_bt(const GemmArgs& a, cudaStream_t stream, int num_sms
   return cudaGetLastError();
 }
 
-cudaError_t launch_w4a4_gemm(const GemmArgs& a, cudaStream_t stream, int num_sms,
-                             int* launches) {
+// Tile / split-K plan.  BT = 256 tokens when the 128 x 256 tiles fill the SMs; otherwise the
+// smallest power of two >= M (no wasted token columns) and the K groups are split S ways so that
+// the (tile, split) items fill one wave as evenly as possible (each split >= 4 groups).  Splits
+// publish fp32 partials in the workspace; the last split to arrive reduces (no spinning).
+GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms) {
+  GemmPlan pl;
+  const int64_t n_tiles = N / kTileN;
+  const int G = static_cast<int>(K / 128);
+  auto tiles = [&](int bt) { return n_tiles * ((M + bt - 1) / bt); };
+  if (tiles(256) >= num_sms) {
+    pl.bt = 256;
+  } else {
+    pl.bt = 32;
+    while (pl.bt < 256 && pl.bt < M) pl.bt *= 2;
+  }
+  const int64_t t = tiles(pl.bt);
+  pl.ksplit = 1;
+  if (t < 2 * num_sms) {
+    double best = 1e30;
+    for (int sp = 1; sp <= G / 4 && sp <= 16; ++sp) {
+      const double cost = static_cast<double>((t * sp + num_sms - 1) / num_sms) / sp;
+      if (cost < best - 1e-9) {
+        best = cost;
+        pl.ksplit = sp;
+      }
+    }
+  }
+  pl.num_tiles = t;
+  if (pl.ksplit > 1) {
+    pl.counter_bytes = ((t * sizeof(int) + 255) / 256) * 256;
+    pl.workspace_bytes = pl.counter_bytes + t * pl.ksplit * kTileN * pl.bt * sizeof(float);
+  }
+  return pl;
+}
+
+cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,
+                             cudaStream_t stream, int num_sms, int* launches) {
   *launches = 0;
   if (a.M == 0) return cudaSuccess;
-  const int64_t n_tiles = a.N / kTileN;
-  auto tiles = [&](int bt) { return n_tiles * ((a.M + bt - 1) / bt); };
-  cudaError_t e;
-  if (tiles(256) >= num_sms) e = launch_bt<256>(a, stream, num_sms);
-  else if (tiles(128) >= num_sms) e = launch_bt<128>(a, stream, num_sms);
-  else if (tiles(64) >= num_sms) e = launch_bt<64>(a, stream, num_sms);
-  else e = launch_bt<32>(a, stream, num_sms);
-  if (e == cudaSuccess) *launches = 1;
-  return e;
+  const GemmPlan pl = plan_w4a4_gemm(a.M, a.N, a.K, num_sms);
+  if (workspace_bytes < pl.workspace_bytes) return cudaErrorInvalidValue;
+  switch (pl.bt) {
+    case 256: return launch_bt<256>(a, pl, workspace, stream, num_sms, launches);
+    case 128: return launch_bt<128>(a, pl, workspace, stream, num_sms, launches);
+    case 64: return launch_bt<64>(a, pl, workspace, stream, num_sms, launches);
+    default: return launch_bt<32>(a, pl, workspace, stream, num_sms, launches);
+  }
 }
 
 }  // namespace atom

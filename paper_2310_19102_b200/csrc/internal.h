@@ -30,8 +30,18 @@ struct GemmArgs {
   int32_t* debug_partials;
 };
 
-// Returns the number of kernel launches issued through *launches.
-cudaError_t launch_w4a4_gemm(const GemmArgs& a, cudaStream_t stream, int num_sms,
-                             int* launches);
+struct GemmPlan {
+  int bt = 256;                 // token tile
+  int ksplit = 1;               // K splits per tile
+  int64_t num_tiles = 0;
+  size_t counter_bytes = 0;
+  size_t workspace_bytes = 0;   // 0 when ksplit == 1
+};
+
+GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms);
+
+// Returns the number of kernel launches (incl. memsets) issued through *launches.
+cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,
+                             cudaStream_t stream, int num_sms, int* launches);
 
 }  // namespace atom

@@ -8,9 +8,9 @@
 //
 // B200 design: HBM-bound gather.  One CTA per (row, group-chunk); the fp16 row is staged once in
 // shared memory with 128-bit streaming loads (coalesced), the gather x'[j] = x[perm[j]] then
-// reads shared memory.  One warp per 128-channel group: each lane owns 4 reordered channels
-// (one 128-bit perm load), the group |max| is a 5-step warp-shuffle reduction, codes are packed
-// in registers and written as 64 contiguous bytes per warp (INT4) or 128 bytes (INT8).
+// reads shared memory.  One half-warp per 128-channel group: each lane owns 8 reordered
+// channels (two 128-bit perm loads), the group |max| is a 4-step shuffle reduction, codes are
+// packed in registers and written as 64 contiguous bytes (INT4) or 128 bytes (INT8).
 // Numerics are pinned to the oracle's binary32 steps: __fdiv_rn / __fmul_rn / __frcp_rn are
 // IEEE round-to-nearest and never contracted; cvt.rni gives round-half-to-even.
 #include <cfloat>
@@ -61,33 +61,47 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
   const float alpha8 = __fdiv_rn(__fmul_rn(2.0f, clip8), 255.0f);
   const int64_t row4 = static_cast<int64_t>(G4) * 64;
 
-  for (int t = g_begin + warp; t < g_end; t += kQuantWarps) {
-    const int4 p = __ldg(reinterpret_cast<const int4*>(perm + t * 128 + 4 * lane));
-    const float v0 = __half2float(srow[p.x]);
-    const float v1 = __half2float(srow[p.y]);
-    const float v2 = __half2float(srow[p.z]);
-    const float v3 = __half2float(srow[p.w]);
-    float amax = fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3)));
+  // Each warp quantizes two groups at a time, one per half-warp; a lane owns 8 consecutive
+  // reordered channels (two 128-bit perm loads), the group |max| is a 4-step shuffle.
+  const int hw = lane >> 4, hl = lane & 15;
+  for (int t0 = g_begin + 2 * warp; t0 < g_end; t0 += 2 * kQuantWarps) {
+    const int t = t0 + hw;
+    const bool valid = t < g_end;
+    const int tt = valid ? t : t0;
+    const int4 pa = __ldg(reinterpret_cast<const int4*>(perm + tt * 128 + 8 * hl));
+    const int4 pb = __ldg(reinterpret_cast<const int4*>(perm + tt * 128 + 8 * hl + 4));
+    float v[8];
+    v[0] = __half2float(srow[pa.x]); v[1] = __half2float(srow[pa.y]);
+    v[2] = __half2float(srow[pa.z]); v[3] = __half2float(srow[pa.w]);
+    v[4] = __half2float(srow[pb.x]); v[5] = __half2float(srow[pb.y]);
+    v[6] = __half2float(srow[pb.z]); v[7] = __half2float(srow[pb.w]);
+    float amax = fabsf(v[0]);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
+    for (int k = 1; k < 8; ++k) amax = fmaxf(amax, fabsf(v[k]));
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1)
       amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-    const bool is_int4 = t < G4;
+    const bool is_int4 = tt < G4;
     const float s = (amax == 0.0f) ? FLT_MIN : __fmul_rn(amax, is_int4 ? alpha4 : alpha8);
     const float inv = __frcp_rn(s);
-    if (is_int4) {
-      const int c0 = quant_code(v0, inv, -8, 7), c1 = quant_code(v1, inv, -8, 7);
-      const int c2 = quant_code(v2, inv, -8, 7), c3 = quant_code(v3, inv, -8, 7);
-      const uint16_t packed = static_cast<uint16_t>((c0 & 0xF) | ((c1 & 0xF) << 4) |
-                                                    ((c2 & 0xF) << 8) | ((c3 & 0xF) << 12));
-      reinterpret_cast<uint16_t*>(q4 + row * row4 + t * 64)[lane] = packed;
-    } else {
-      const int c0 = quant_code(v0, inv, -128, 127), c1 = quant_code(v1, inv, -128, 127);
-      const int c2 = quant_code(v2, inv, -128, 127), c3 = quant_code(v3, inv, -128, 127);
-      const uint32_t packed = (c0 & 0xFF) | ((c1 & 0xFF) << 8) | ((c2 & 0xFF) << 16) |
-                              (static_cast<uint32_t>(c3 & 0xFF) << 24);
-      reinterpret_cast<uint32_t*>(q8 + row * 128)[lane] = packed;
+    if (valid) {
+      if (is_int4) {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          packed |= static_cast<uint32_t>(quant_code(v[k], inv, -8, 7) & 0xF) << (4 * k);
+        reinterpret_cast<uint32_t*>(q4 + row * row4 + t * 64)[hl] = packed;
+      } else {
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          lo |= static_cast<uint32_t>(quant_code(v[k], inv, -128, 127) & 0xFF) << (8 * k);
+          hi |= static_cast<uint32_t>(quant_code(v[k + 4], inv, -128, 127) & 0xFF) << (8 * k);
+        }
+        reinterpret_cast<uint2*>(q8 + row * 128)[hl] = make_uint2(lo, hi);
+      }
+      if (hl == 0) scales[static_cast<int64_t>(t) * rows + row] = s;
     }
-    if (lane == 0) scales[static_cast<int64_t>(t) * rows + row] = s;
   }
 }
 
@@ -97,9 +111,9 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     float* scales, cudaStream_t stream, int num_sms) {
   const int G = static_cast<int>(K / 128);
   const int G4 = static_cast<int>((K - k_outlier) / 128);
-  // Enough CTAs to cover the SMs a few times over; each CTA re-stages the row from L2.
-  int splits = static_cast<int>((4LL * 2 * num_sms + rows - 1) / rows);
-  const int max_splits = (G + kQuantWarps - 1) / kQuantWarps;
+  // Enough CTAs to cover the SMs ~4 times; each extra split re-stages the row (from L2).
+  int splits = static_cast<int>((4LL * num_sms + rows - 1) / rows);
+  const int max_splits = (G + 2 * kQuantWarps - 1) / (2 * kQuantWarps);
   splits = max(1, min(splits, max_splits));
   const int gpc = (G + splits - 1) / splits;
   splits = (G + gpc - 1) / gpc;
