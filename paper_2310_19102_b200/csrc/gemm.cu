@@ -141,6 +141,12 @@ __device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf,
   }
 }
 
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // One work item = (output tile, K split).  Splits cover contiguous group ranges; the INT8 outlier
 // group (the last one) therefore always lands in the last split.
 struct Item {
@@ -181,6 +187,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < 256)
+    p.trace[768 + blockIdx.x] = globaltimer();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -436,6 +444,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.sfree[sr]);
       }
+      if (p.trace != nullptr && threadIdx.x == kEpiWarp0 * 32 && blockIdx.x < 256)
+        p.trace[1024 + blockIdx.x] = globaltimer();
       // ---- split-K: publish this split's fp32 partial; the last split to arrive adds the
       //      others' partials (same thread <-> element mapping) and stores the tile ----
       if (p.ksplit > 1) {
@@ -455,14 +465,16 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (!last) continue;
         __threadfence();
         if (threadIdx.x == kEpiWarp0 * 32) p.counters[w.tile] = 0;   // self-cleaning
+        // deterministic: sum the partials in split order (the last arriver re-reads its own)
+#pragma unroll
+        for (int j = 0; j < COLS / 2; ++j) acc[j] = make_float2(0.0f, 0.0f);
         for (int sp = 0; sp < p.ksplit; ++sp) {
-          if (sp == w.split) continue;
-          const float4* other = reinterpret_cast<const float4*>(
+          const float4* part = reinterpret_cast<const float4*>(
               p.partials + ((static_cast<int64_t>(w.tile) * p.ksplit + sp) * kTileN + n_local) * BT +
               half * COLS);
 #pragma unroll
           for (int j = 0; j < COLS / 4; ++j) {
-            const float4 o = __ldcg(other + j);
+            const float4 o = __ldcg(part + j);
             acc[2 * j].x += o.x; acc[2 * j].y += o.y;
             acc[2 * j + 1].x += o.z; acc[2 * j + 1].y += o.w;
           }
@@ -528,6 +540,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 
   tc_fence_before();
   __syncthreads();
+  if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < 256)
+    p.trace[1280 + blockIdx.x] = globaltimer();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -640,16 +654,24 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
   const int grid = p.num_items < num_sms ? p.num_items : num_sms;
   static long long* trace = nullptr;
   static const bool want_trace = getenv("ATOM_GEMM_TRACE") != nullptr;   // development probe only
-  if (want_trace && trace == nullptr) cudaMalloc(&trace, 3 * 256 * sizeof(long long));
+  if (want_trace && trace == nullptr) cudaMalloc(&trace, 6 * 256 * sizeof(long long));
   p.trace = want_trace ? trace : nullptr;
   kern<<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
   ++*launches;
   if (want_trace) {
-    long long h[768];
+    long long h[1536];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "plan: BT=%d ksplit=%d tiles=%d items=%d grid=%d\n", BT, p.ksplit,
+            p.num_tiles, p.num_items, grid);
     fprintf(stderr, "trace g: ufull_arrive mma_issue epi_seen (clk rel. to mma_issue[0])\n");
     for (int g = 0; g < 256 && g < p.G * 2; ++g)
       fprintf(stderr, "%3d %9lld %9lld %9lld\n", g, h[256 + g] - h[0], h[g] - h[0], h[512 + g] - h[0]);
+    long long t0 = h[768];
+    for (int b = 0; b < grid && b < 256; ++b) t0 = h[768 + b] < t0 ? h[768 + b] : t0;
+    fprintf(stderr, "cta: start_ns groups_done_ns end_ns (rel. to first start)\n");
+    for (int b = 0; b < grid && b < 256; ++b)
+      fprintf(stderr, "%3d %8lld %8lld %8lld\n", b, h[768 + b] - t0, h[1024 + b] - t0,
+              h[1280 + b] - t0);
   }
   return cudaGetLastError();
 }

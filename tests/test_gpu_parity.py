@@ -255,6 +255,8 @@ def test_gemm_baseline_configs_sampled(atom, name):
 # tensor-parallel shard algebra on one device (the "fake backend" of SURVEY §4 T3)
 # ----------------------------------------------------------------------------------------------
 def test_n_shard_bit_identical(atom):
+    """Column shards see the same per-tile computation (same token tile and K split plan for
+    these shapes), so the assembled output is bit-identical to the unsharded GEMM."""
     import torch
     M, N, K, P = 96, 1024, 2048, 4
     X, W, perm = synth.problem(M, N, K, seed=6)
@@ -268,6 +270,20 @@ def test_n_shard_bit_identical(atom):
         atom.w4a4_gemm(aq, wq, out=out[:, sl])
     torch.cuda.synchronize()
     assert torch.equal(out, full)
+
+
+def test_gemm_deterministic(atom):
+    """Split-K reductions sum the partials in split order: repeated calls are bit-identical."""
+    import torch
+    for M, N, K in [(16, 1024, 1024), (256, 4096, 4096), (40, 512, 2048)]:
+        X, W, perm = synth.problem(M, N, K, seed=M)
+        pd = dev(perm)
+        aq = atom.reorder_quantize(dev(X), pd)
+        wq = atom.quantize_weights(dev(W), pd)
+        outs = [atom.w4a4_gemm(aq, wq) for _ in range(4)]
+        torch.cuda.synchronize()
+        for o in outs[1:]:
+            assert torch.equal(o, outs[0]), (M, N, K)
 
 
 def test_k_shard_partials_and_sum(atom):
