@@ -290,6 +290,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             umma_i8(d, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
                     (k > 0 || (kPrefillEven && (u & 1u) == 0)) ? 1u : 0u);
           umma_commit(&sm.mdone[u]);
+          if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256) p.trace[1536 + g_it] = clock64();
         }
       }
     }
@@ -393,21 +394,30 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         // tcgen05.st), odd ones are converted with a LOP3; no per-element select.
         auto drain = [&](auto pre_tag) {
           constexpr bool kPre = decltype(pre_tag)::value;
+          constexpr int NCH = COLS / CH;
+          // software-pipelined: chunk ch+1 is loaded from TMEM while chunk ch is computed
+          uint32_t rb[2][CH];
+          if constexpr ((kMode & 8) == 0) {
+            tmem_ld<CH>(taddr, rb[0]);
+            tmem_ld_wait();
+          } else {
 #pragma unroll
-          for (int ch = 0; ch < COLS / CH; ++ch) {
-            uint32_t r[CH];
-            if constexpr ((kMode & 8) == 0) {
-              tmem_ld<CH>(taddr + ch * CH, r);
-              tmem_ld_wait();
-              if constexpr (kPre) {   // re-arm with the magic
+            for (int k = 0; k < CH; ++k) rb[0][k] = 0;
+          }
 #pragma unroll
-                for (int k = 0; k < CH; k += 4) tmem_st4(taddr + ch * CH + k, mg);
+          for (int ch = 0; ch < NCH; ++ch) {
+            uint32_t (&r)[CH] = rb[ch & 1];
+            if constexpr (kPre && (kMode & 8) == 0) {   // re-arm this chunk with the magic
+#pragma unroll
+              for (int k = 0; k < CH; k += 4) tmem_st4(taddr + ch * CH + k, mg);
+            }
+            if (ch + 1 < NCH) {
+              if constexpr ((kMode & 8) == 0) tmem_ld<CH>(taddr + (ch + 1) * CH, rb[(ch + 1) & 1]);
+              else {
+#pragma unroll
+                for (int k = 0; k < CH; ++k) rb[(ch + 1) & 1][k] = 0;
               }
             } else {
-#pragma unroll
-              for (int k = 0; k < CH; ++k) r[k] = 0;
-            }
-            if (ch == COLS / CH - 1) {
               if constexpr (kPre) tmem_st_wait();
               tc_fence_before();
               __syncwarp();
@@ -437,6 +447,9 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
               acc[j] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[j]);
               acc[j + 1] = __ffma2_rn(make_float2(s.z, s.w), g1, acc[j + 1]);
             }
+            if (ch + 1 < NCH) {
+              if constexpr ((kMode & 8) == 0) tmem_ld_wait();
+            }
           }
         };
         if (kPrefillEven && (b & 1u) == 0) drain(std::true_type{});
@@ -446,65 +459,48 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       }
       if (p.trace != nullptr && threadIdx.x == kEpiWarp0 * 32 && blockIdx.x < 256)
         p.trace[1024 + blockIdx.x] = globaltimer();
-      // ---- split-K: publish this split's fp32 partial; the last split to arrive adds the
-      //      others' partials (same thread <-> element mapping) and stores the tile ----
-      if (p.ksplit > 1) {
-        float4* mine = reinterpret_cast<float4*>(
-            p.partials + ((static_cast<int64_t>(w.tile) * p.ksplit + w.split) * kTileN + n_local) * BT +
-            half * COLS);
-#pragma unroll
-        for (int j = 0; j < COLS / 4; ++j)
-          mine[j] = make_float4(acc[2 * j].x, acc[2 * j].y, acc[2 * j + 1].x, acc[2 * j + 1].y);
-        __threadfence();
-        named_bar_sync(1, kNumEpiWarps * 32);   // all epilogue threads of this CTA have written
-        __shared__ int arrived;
-        if (threadIdx.x == kEpiWarp0 * 32) arrived = atomicAdd(p.counters + w.tile, 1);
-        named_bar_sync(1, kNumEpiWarps * 32);
-        const bool last = arrived == p.ksplit - 1;
-        named_bar_sync(1, kNumEpiWarps * 32);   // everyone has read `arrived`
-        if (!last) continue;
-        __threadfence();
-        if (threadIdx.x == kEpiWarp0 * 32) p.counters[w.tile] = 0;   // self-cleaning
-        // deterministic: sum the partials in split order (the last arriver re-reads its own)
-#pragma unroll
-        for (int j = 0; j < COLS / 2; ++j) acc[j] = make_float2(0.0f, 0.0f);
-        for (int sp = 0; sp < p.ksplit; ++sp) {
-          const float4* part = reinterpret_cast<const float4*>(
-              p.partials + ((static_cast<int64_t>(w.tile) * p.ksplit + sp) * kTileN + n_local) * BT +
-              half * COLS);
-#pragma unroll
-          for (int j = 0; j < COLS / 4; ++j) {
-            const float4 o = __ldcg(part + j);
-            acc[2 * j].x += o.x; acc[2 * j].y += o.y;
-            acc[2 * j + 1].x += o.z; acc[2 * j + 1].y += o.w;
-          }
-        }
-      }
       // ---- tile output ----
       // Thread = output channel n, registers = tokens m; C is [M][N] with n contiguous.  Each
       // 8x8 (m, n) block is transposed through a per-warp shared scratch so that every lane
       // stores 8 consecutive n of one token as one 16-byte vector (4 lanes per 64-byte row
-      // segment), instead of 2-byte scattered stores.
+      // segment), instead of 2-byte scattered stores.  With split-K the same fp32 path writes the
+      // split's partial tile [BT][128] to the workspace; the last split to arrive then sums the
+      // partials in split order (deterministic) with coalesced 16-byte loads and stores C.
       if constexpr ((kMode & 32) != 0) continue;
       const int ga = lane >> 3, gb = lane & 7;
       float* scr = &sm.oscr[e][ga][0];
-      const int nn = n0 + q * 32 + 8 * ga;   // first of the 8 channels this lane stores
-      if (p.c_f32) {
+      const bool split = p.ksplit > 1;
+      float* f32_base;
+      int64_t f32_ld;
+      int row0, col0, row_limit;
+      if (split) {
+        f32_base = p.partials + (static_cast<int64_t>(w.tile) * p.ksplit + w.split) * BT * kTileN;
+        f32_ld = kTileN;
+        row0 = half * COLS;
+        col0 = q * 32 + 8 * ga;
+        row_limit = BT;
+      } else {
+        f32_base = static_cast<float*>(p.c);
+        f32_ld = p.ldc;
+        row0 = mc0;
+        col0 = n0 + q * 32 + 8 * ga;
+        row_limit = p.M;
+      }
+      if (split || p.c_f32) {
 #pragma unroll
         for (int c8 = 0; c8 < COLS / 8; ++c8) {
-          float4* w = reinterpret_cast<float4*>(scr + gb * 8);
-          w[0] = make_float4(acc[4 * c8].x, acc[4 * c8].y, acc[4 * c8 + 1].x, acc[4 * c8 + 1].y);
-          w[1] = make_float4(acc[4 * c8 + 2].x, acc[4 * c8 + 2].y, acc[4 * c8 + 3].x,
-                             acc[4 * c8 + 3].y);
+          float4* wv = reinterpret_cast<float4*>(scr + gb * 8);
+          wv[0] = make_float4(acc[4 * c8].x, acc[4 * c8].y, acc[4 * c8 + 1].x, acc[4 * c8 + 1].y);
+          wv[1] = make_float4(acc[4 * c8 + 2].x, acc[4 * c8 + 2].y, acc[4 * c8 + 3].x,
+                              acc[4 * c8 + 3].y);
           __syncwarp();
           float v[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) v[k] = scr[k * 8 + gb];
           __syncwarp();
-          const int m = mc0 + 8 * c8 + gb;
-          if (m < p.M) {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.c) +
-                                                    static_cast<int64_t>(m) * p.ldc + nn);
+          const int m = row0 + 8 * c8 + gb;
+          if (m < row_limit) {
+            float4* dst = reinterpret_cast<float4*>(f32_base + static_cast<int64_t>(m) * f32_ld + col0);
             dst[0] = make_float4(v[0], v[1], v[2], v[3]);
             dst[1] = make_float4(v[4], v[5], v[6], v[7]);
           }
@@ -518,21 +514,74 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           hp[j] = *reinterpret_cast<const uint32_t*>(&h);
         }
         uint16_t* hs = reinterpret_cast<uint16_t*>(scr);
-        __half* crow = static_cast<__half*>(p.c) + static_cast<int64_t>(mc0 + gb) * p.ldc + nn;
+        __half* crow = static_cast<__half*>(p.c) + static_cast<int64_t>(mc0 + gb) * p.ldc + col0;
         const int64_t step = 8 * p.ldc;
 #pragma unroll
         for (int c8 = 0; c8 < COLS / 8; ++c8) {
           *reinterpret_cast<uint4*>(hs + gb * 8) =
               make_uint4(hp[4 * c8], hp[4 * c8 + 1], hp[4 * c8 + 2], hp[4 * c8 + 3]);
           __syncwarp();
-          uint32_t w[4];
+          uint32_t wv[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            w[k] = static_cast<uint32_t>(hs[(2 * k) * 8 + gb]) |
-                   (static_cast<uint32_t>(hs[(2 * k + 1) * 8 + gb]) << 16);
+            wv[k] = static_cast<uint32_t>(hs[(2 * k) * 8 + gb]) |
+                    (static_cast<uint32_t>(hs[(2 * k + 1) * 8 + gb]) << 16);
           __syncwarp();
           if (mc0 + 8 * c8 + gb < p.M)
-            *reinterpret_cast<uint4*>(crow + c8 * step) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(crow + c8 * step) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+      }
+      if (split) {
+        __threadfence();
+        named_bar_sync(1, kNumEpiWarps * 32);   // all epilogue threads of this CTA have written
+        __shared__ int arrived;
+        if (threadIdx.x == kEpiWarp0 * 32) arrived = atomicAdd(p.counters + w.tile, 1);
+        named_bar_sync(1, kNumEpiWarps * 32);
+        const bool last = arrived == p.ksplit - 1;
+        named_bar_sync(1, kNumEpiWarps * 32);   // everyone has read `arrived`
+        if (!last) continue;
+        __threadfence();
+        if (threadIdx.x == kEpiWarp0 * 32) p.counters[w.tile] = 0;   // self-cleaning
+        const float* slot0 = p.partials + static_cast<int64_t>(w.tile) * p.ksplit * BT * kTileN;
+        const int et = threadIdx.x - kEpiWarp0 * 32;   // 0..255
+        constexpr int kChunks = BT * (kTileN / 4);       // float4 chunks of the tile
+        constexpr int kPerThread = kChunks / (kNumEpiWarps * 32);
+        constexpr int kBatch = kPerThread < 4 ? kPerThread : 4;
+        // batches of kBatch chunks: all loads of a batch are issued before any use (L2 latency)
+        for (int b0 = 0; b0 < kPerThread; b0 += kBatch) {
+          float4 sum[kBatch];
+#pragma unroll
+          for (int k = 0; k < kBatch; ++k) sum[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          for (int sp = 0; sp < p.ksplit; ++sp) {
+            float4 o[kBatch];
+#pragma unroll
+            for (int k = 0; k < kBatch; ++k)
+              o[k] = __ldcg(reinterpret_cast<const float4*>(
+                         slot0 + static_cast<int64_t>(sp) * BT * kTileN) +
+                     et + (b0 + k) * (kNumEpiWarps * 32));
+#pragma unroll
+            for (int k = 0; k < kBatch; ++k) {
+              sum[k].x += o[k].x; sum[k].y += o[k].y; sum[k].z += o[k].z; sum[k].w += o[k].w;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kBatch; ++k) {
+            const int idx = et + (b0 + k) * (kNumEpiWarps * 32);
+            const int ml = idx / (kTileN / 4), nl = (idx % (kTileN / 4)) * 4;
+            const int m = m0 + ml;
+            if (m >= p.M) continue;
+            if (p.c_f32) {
+              *reinterpret_cast<float4*>(static_cast<float*>(p.c) + static_cast<int64_t>(m) * p.ldc +
+                                         n0 + nl) = sum[k];
+            } else {
+              const __half2 h0 = __floats2half2_rn(sum[k].x, sum[k].y);
+              const __half2 h1 = __floats2half2_rn(sum[k].z, sum[k].w);
+              *reinterpret_cast<uint2*>(static_cast<__half*>(p.c) + static_cast<int64_t>(m) * p.ldc +
+                                        n0 + nl) =
+                  make_uint2(*reinterpret_cast<const uint32_t*>(&h0),
+                             *reinterpret_cast<const uint32_t*>(&h1));
+            }
+          }
         }
       }
     }
@@ -654,18 +703,19 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
   const int grid = p.num_items < num_sms ? p.num_items : num_sms;
   static long long* trace = nullptr;
   static const bool want_trace = getenv("ATOM_GEMM_TRACE") != nullptr;   // development probe only
-  if (want_trace && trace == nullptr) cudaMalloc(&trace, 6 * 256 * sizeof(long long));
+  if (want_trace && trace == nullptr) cudaMalloc(&trace, 7 * 256 * sizeof(long long));
   p.trace = want_trace ? trace : nullptr;
   kern<<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
   ++*launches;
   if (want_trace) {
-    long long h[1536];
+    long long h[1792];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "plan: BT=%d ksplit=%d tiles=%d items=%d grid=%d\n", BT, p.ksplit,
             p.num_tiles, p.num_items, grid);
-    fprintf(stderr, "trace g: ufull_arrive mma_issue epi_seen (clk rel. to mma_issue[0])\n");
+    fprintf(stderr, "trace g: ufull_arrive mma_issue mma_committed epi_seen (clk rel. to mma_issue[0])\n");
     for (int g = 0; g < 256 && g < p.G * 2; ++g)
-      fprintf(stderr, "%3d %9lld %9lld %9lld\n", g, h[256 + g] - h[0], h[g] - h[0], h[512 + g] - h[0]);
+      fprintf(stderr, "%3d %9lld %9lld %9lld %9lld\n", g, h[256 + g] - h[0], h[g] - h[0],
+              h[1536 + g] - h[0], h[512 + g] - h[0]);
     long long t0 = h[768];
     for (int b = 0; b < grid && b < 256; ++b) t0 = h[768 + b] < t0 ? h[768 + b] : t0;
     fprintf(stderr, "cta: start_ns groups_done_ns end_ns (rel. to first start)\n");
