@@ -694,6 +694,9 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
     if (mode == 23) kern = w4a4_gemm_kernel<BT, false, 23>;
     if (mode == 32) kern = w4a4_gemm_kernel<BT, false, 32>;
     if (mode == 64) kern = w4a4_gemm_kernel<BT, false, 64>;
+    if (mode == 33) kern = w4a4_gemm_kernel<BT, false, 33>;
+    if (mode == 34) kern = w4a4_gemm_kernel<BT, false, 34>;
+    if (mode == 39) kern = w4a4_gemm_kernel<BT, false, 39>;
 
 
   }
