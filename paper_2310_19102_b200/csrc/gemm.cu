@@ -86,7 +86,7 @@ struct __align__(1024) GemmSmem {
   uint8_t stage_a[kStages][BT * 64];    // packed activation group
   float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
   float ssa[kSRing][BT];                // activation scales of a group
-  float oscr[kNumEpiWarps][4][72];      // per-warp 8x8 transpose scratch for the tile output
+  uint8_t ostg[kNumEpiWarps][1280];     // per-warp output staging (2 x 8 rows x 80 B)
   uint32_t magic4[4];                   // 4 copies of the magic bit pattern
   uint64_t full[kStages], empty[kStages];
   uint64_t ufull[R];
@@ -333,122 +333,137 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     }
   } else {
     // ===================== epilogue warps =====================
+    // TMEM is read with the 16x256b shape: thread (tr = lane/4, tc = lane%4) holds, for each
+    // 16-lane block blk of its warp's lane quarter and each 8-column chunk j, the MMA-fragment
+    // values (row tr, cols 2tc, 2tc+1) and (row tr+8, same cols).  Column pairs share one s_a
+    // pair (one 8-byte shared load per chunk for the whole warp), and at the tile end the fp16
+    // fragments go through stmatrix.trans into [token][channel] rows for 16-byte global stores.
     setmaxnreg_inc<kRegsHigh>();
-    constexpr int COLS = BT / 2;  // tokens per thread
-    constexpr int CH = (COLS >= 32 && COLS < 128) ? 32 : 16;   // x16 at COLS = 128: register budget
+    constexpr int COLS = BT / 2;         // token columns per warp (column half of the tile)
+    constexpr int NJ = COLS / 8;         // 8-column chunks
+    constexpr int JL = NJ >= 4 ? 4 : NJ; // chunks per TMEM load (16x256b.xJL)
     const int e = warp - kEpiWarp0;
-    const int q = warp & 3;       // TMEM lane quarter this warp may access
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int half = e >> 2;
-    const int n_local = q * 32 + lane;
-    const uint32_t tlane = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * COLS;
+    const int tr = lane >> 2, tc = lane & 3;
+    const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * COLS;
     const uint32_t magic = kMagicBits;
-    // Resident copies of the magic as tcgen05.st sources: loaded once from shared memory so the
-    // compiler cannot re-materialise them with 4 IMAD.MOV (FMA pipe) before every store.
+    // Resident copies of the magic as tcgen05.st sources (see the STTM re-arm below).
     uint32_t mg[4];
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(mg[0]), "=r"(mg[1]), "=r"(mg[2]), "=r"(mg[3])
                  : "r"(smem_u32(sm.magic4)));
     // Even accumulator buffers carry the magic bias (tcgen05.st, TMEM write port); odd ones are
-    // converted with a LOP3 (ALU).  Splitting the conversion between the two keeps both the TMEM
-    // bandwidth and the ALU pipe below the MMA time.
+    // converted with a LOP3 (ALU) -- see DESIGN.md "Epilogue arithmetic".
     if constexpr (kPrefillEven) {
 #pragma unroll
       for (int b = 0; b < R; b += 2)
 #pragma unroll
-        for (int ch = 0; ch < COLS / CH; ++ch) tmem_st_const<CH>(tlane + b * BT + ch * CH, magic);
+        for (int c = 0; c < COLS; c += 4) tmem_st4(tq + b * BT + c, mg);
       tmem_st_wait();
     }
     tc_fence_before();
     __syncwarp();
     if (lane == 0)
       for (int b = 0; b < R; ++b) mbar_arrive(&sm.tempty[b]);
+    uint8_t* stg = sm.ostg[e];           // per-warp staging for the transposed output
     uint32_t g_it = 0;
     for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
       const Item w = make_item<BT>(p, item);
       const int n0 = w.n0, m0 = w.m0;
-      const int n = n0 + n_local;
       const int mc0 = m0 + half * COLS;
-      float2 acc[COLS / 2];
+      // acc[blk][j][h]: rows 32q + 16 blk + tr + 8 h, columns (token) 8j + 2tc + {0, 1}
+      float2 acc[2][NJ][2];
 #pragma unroll
-      for (int j = 0; j < COLS / 2; ++j) acc[j] = make_float2(0.0f, 0.0f);
+      for (int bk = 0; bk < 2; ++bk)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          acc[bk][j][0] = make_float2(0.0f, 0.0f);
+          acc[bk][j][1] = make_float2(0.0f, 0.0f);
+        }
       for (int t = w.t0; t < w.t1; ++t, ++g_it) {
         const uint32_t b = g_it % R, bph = (g_it / R) & 1;
         const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
         const bool int4 = t < G4;
         wait(&sm.sready[sr], sph);
-        float sw = sm.ssw[sr][n_local];
-        if (int4) sw *= (1.0f / 256.0f);  // undo the 16*16 operand pre-scaling (exact)
         // Dequantize T = float(1.5*2^23 + R) with ONE fma: g = T*sw' - 1.5*2^23*sw' = sw'*R,
-        // rounded once.  sw' = sw with its 2 lowest mantissa bits cleared (relative change
-        // < 2^-22) so that 1.5*2^23*sw' is exact; see DESIGN.md "Epilogue arithmetic".
-        const float swh = __uint_as_float(__float_as_uint(sw) & 0xFFFFFFFCu);
-        const float2 sw2 = make_float2(swh, swh);
-        const float2 nc2 = make_float2(-kMagic * swh, -kMagic * swh);
-        const float4* sa4 = reinterpret_cast<const float4*>(&sm.ssa[sr][half * COLS]);
+        // rounded once.  sw' = sw (x1/256 for INT4 groups, exact) with its 2 lowest mantissa
+        // bits cleared so that 1.5*2^23*sw' is exact; see DESIGN.md "Epilogue arithmetic".
+        float2 sw2[2][2], nc2[2][2];
+#pragma unroll
+        for (int bk = 0; bk < 2; ++bk)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float sw = sm.ssw[sr][q * 32 + 16 * bk + 8 * h + tr];
+            if (int4) sw *= (1.0f / 256.0f);
+            const float swh = __uint_as_float(__float_as_uint(sw) & 0xFFFFFFFCu);
+            sw2[bk][h] = make_float2(swh, swh);
+            nc2[bk][h] = make_float2(-kMagic * swh, -kMagic * swh);
+          }
+        const float2* sa2 = reinterpret_cast<const float2*>(&sm.ssa[sr][half * COLS + 2 * tc]);
         wait(&sm.mdone[b], bph);
         tc_fence_after();
         if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256 && e == 0 && lane == 0)
           p.trace[512 + g_it] = clock64();
-        const uint32_t taddr = tlane + b * BT;
-        // Two specialised copies of the drain: even buffers are magic-prefilled (re-armed with
-        // tcgen05.st), odd ones are converted with a LOP3; no per-element select.
+        const uint32_t taddr = tq + b * BT;
         auto drain = [&](auto pre_tag) {
           constexpr bool kPre = decltype(pre_tag)::value;
-          constexpr int NCH = COLS / CH;
-          // software-pipelined: chunk ch+1 is loaded from TMEM while chunk ch is computed
-          uint32_t rb[2][CH];
-          if constexpr ((kMode & 8) == 0) {
-            tmem_ld<CH>(taddr, rb[0]);
-            tmem_ld_wait();
-          } else {
 #pragma unroll
-            for (int k = 0; k < CH; ++k) rb[0][k] = 0;
-          }
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-            uint32_t (&r)[CH] = rb[ch & 1];
-            if constexpr (kPre && (kMode & 8) == 0) {   // re-arm this chunk with the magic
-#pragma unroll
-              for (int k = 0; k < CH; k += 4) tmem_st4(taddr + ch * CH + k, mg);
-            }
-            if (ch + 1 < NCH) {
-              if constexpr ((kMode & 8) == 0) tmem_ld<CH>(taddr + (ch + 1) * CH, rb[(ch + 1) & 1]);
-              else {
-#pragma unroll
-                for (int k = 0; k < CH; ++k) rb[(ch + 1) & 1][k] = 0;
-              }
+          for (int jl = 0; jl < NJ / JL; ++jl) {
+            uint32_t r[2][4 * JL];
+            if constexpr ((kMode & 8) == 0) {
+              tmem_ld_16x256b<JL>(taddr + jl * 8 * JL, r[0]);
+              tmem_ld_16x256b<JL>(taddr + (16u << 16) + jl * 8 * JL, r[1]);
+              tmem_ld_wait();
             } else {
-              if constexpr (kPre) tmem_st_wait();
+#pragma unroll
+              for (int k = 0; k < 4 * JL; ++k) r[0][k] = r[1][k] = 0;
+            }
+            if (jl == NJ / JL - 1) {
+              if constexpr (kPre && (kMode & 8) == 0) {   // re-arm the whole region
+#pragma unroll
+                for (int c = 0; c < COLS; c += 4) tmem_st4(taddr + c, mg);
+                tmem_st_wait();
+              }
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&sm.tempty[b]);
             }
             if constexpr (!kPre) {
 #pragma unroll
-              for (int k = 0; k < CH; ++k) r[k] = __float_as_uint(biased(r[k], magic));
-            }
-            if constexpr (kDebug) {
-#pragma unroll
-              for (int k = 0; k < CH; ++k) {
-                const int m = mc0 + ch * CH + k;
-                const int v = static_cast<int>(r[k] - kMagicBits);
-                if (m < p.M)
-                  p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (v >> 8) : v;
+              for (int k = 0; k < 4 * JL; ++k) {
+                r[0][k] = __float_as_uint(biased(r[0][k], magic));
+                r[1][k] = __float_as_uint(biased(r[1][k], magic));
               }
             }
 #pragma unroll
-            for (int k4 = 0; k4 < ((kMode & 1) ? 0 : CH / 4); ++k4) {
-              const float4 s = sa4[ch * (CH / 4) + k4];
-              const int j = ch * (CH / 2) + 2 * k4;
-              const float2 g0 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 0]),
-                                                       __uint_as_float(r[4 * k4 + 1])), sw2, nc2);
-              const float2 g1 = __ffma2_rn(make_float2(__uint_as_float(r[4 * k4 + 2]),
-                                                       __uint_as_float(r[4 * k4 + 3])), sw2, nc2);
-              acc[j] = __ffma2_rn(make_float2(s.x, s.y), g0, acc[j]);
-              acc[j + 1] = __ffma2_rn(make_float2(s.z, s.w), g1, acc[j + 1]);
-            }
-            if (ch + 1 < NCH) {
-              if constexpr ((kMode & 8) == 0) tmem_ld_wait();
+            for (int jj = 0; jj < JL; ++jj) {
+              const int j = jl * JL + jj;
+              if constexpr (kDebug) {
+#pragma unroll
+                for (int bk = 0; bk < 2; ++bk)
+#pragma unroll
+                  for (int v = 0; v < 4; ++v) {
+                    const int m = mc0 + 8 * j + 2 * tc + (v & 1);
+                    const int n = n0 + q * 32 + 16 * bk + tr + 8 * (v >> 1);
+                    const int raw = static_cast<int>(r[bk][4 * jj + v] - kMagicBits);
+                    if (m < p.M)
+                      p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (raw >> 8) : raw;
+                  }
+              }
+              if constexpr ((kMode & 1) == 0) {
+                const float2 sa = sa2[4 * j];   // s_a of columns 8j + 2tc, +1
+#pragma unroll
+                for (int bk = 0; bk < 2; ++bk)
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    const float2 g = __ffma2_rn(
+                        make_float2(__uint_as_float(r[bk][4 * jj + 2 * h]),
+                                    __uint_as_float(r[bk][4 * jj + 2 * h + 1])),
+                        sw2[bk][h], nc2[bk][h]);
+                    acc[bk][j][h] = __ffma2_rn(sa, g, acc[bk][j][h]);
+                  }
+              }
             }
           }
         };
@@ -459,79 +474,23 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       }
       if (p.trace != nullptr && threadIdx.x == kEpiWarp0 * 32 && blockIdx.x < 256)
         p.trace[1024 + blockIdx.x] = globaltimer();
-      // ---- tile output ----
-      // Thread = output channel n, registers = tokens m; C is [M][N] with n contiguous.  Each
-      // 8x8 (m, n) block is transposed through a per-warp shared scratch so that every lane
-      // stores 8 consecutive n of one token as one 16-byte vector (4 lanes per 64-byte row
-      // segment), instead of 2-byte scattered stores.  With split-K the same fp32 path writes the
-      // split's partial tile [BT][128] to the workspace; the last split to arrive then sums the
-      // partials in split order (deterministic) with coalesced 16-byte loads and stores C.
       if constexpr ((kMode & 32) != 0) continue;
-      const int ga = lane >> 3, gb = lane & 7;
-      float* scr = &sm.oscr[e][ga][0];
-      const bool split = p.ksplit > 1;
-      float* f32_base;
-      int64_t f32_ld;
-      int row0, col0, row_limit;
-      if (split) {
-        f32_base = p.partials + (static_cast<int64_t>(w.tile) * p.ksplit + w.split) * BT * kTileN;
-        f32_ld = kTileN;
-        row0 = half * COLS;
-        col0 = q * 32 + 8 * ga;
-        row_limit = BT;
-      } else {
-        f32_base = static_cast<float*>(p.c);
-        f32_ld = p.ldc;
-        row0 = mc0;
-        col0 = n0 + q * 32 + 8 * ga;
-        row_limit = p.M;
-      }
-      if (split || p.c_f32) {
+
+      // ---- split-K: publish this split's fp32 partial in the fragment layout; the last
+      //      split to arrive sums all partials in split order (deterministic) into acc ----
+      if (p.ksplit > 1) {
+        float* slot = p.partials + (static_cast<int64_t>(w.tile) * p.ksplit + w.split) * kTileN * BT;
+        auto frag_ptr = [&](float* base, int bk, int j, int h) {
+          return reinterpret_cast<float2*>(
+              base + static_cast<int64_t>(q * 32 + 16 * bk + 8 * h + tr) * BT + half * COLS +
+              8 * j + 2 * tc);
+        };
 #pragma unroll
-        for (int c8 = 0; c8 < COLS / 8; ++c8) {
-          float4* wv = reinterpret_cast<float4*>(scr + gb * 8);
-          wv[0] = make_float4(acc[4 * c8].x, acc[4 * c8].y, acc[4 * c8 + 1].x, acc[4 * c8 + 1].y);
-          wv[1] = make_float4(acc[4 * c8 + 2].x, acc[4 * c8 + 2].y, acc[4 * c8 + 3].x,
-                              acc[4 * c8 + 3].y);
-          __syncwarp();
-          float v[8];
+        for (int bk = 0; bk < 2; ++bk)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = scr[k * 8 + gb];
-          __syncwarp();
-          const int m = row0 + 8 * c8 + gb;
-          if (m < row_limit) {
-            float4* dst = reinterpret_cast<float4*>(f32_base + static_cast<int64_t>(m) * f32_ld + col0);
-            dst[0] = make_float4(v[0], v[1], v[2], v[3]);
-            dst[1] = make_float4(v[4], v[5], v[6], v[7]);
-          }
-        }
-      } else {
-        // fp16 first: halves the live registers before the transpose
-        uint32_t hp[COLS / 2];
+          for (int j = 0; j < NJ; ++j)
 #pragma unroll
-        for (int j = 0; j < COLS / 2; ++j) {
-          const __half2 h = __floats2half2_rn(acc[j].x, acc[j].y);
-          hp[j] = *reinterpret_cast<const uint32_t*>(&h);
-        }
-        uint16_t* hs = reinterpret_cast<uint16_t*>(scr);
-        __half* crow = static_cast<__half*>(p.c) + static_cast<int64_t>(mc0 + gb) * p.ldc + col0;
-        const int64_t step = 8 * p.ldc;
-#pragma unroll
-        for (int c8 = 0; c8 < COLS / 8; ++c8) {
-          *reinterpret_cast<uint4*>(hs + gb * 8) =
-              make_uint4(hp[4 * c8], hp[4 * c8 + 1], hp[4 * c8 + 2], hp[4 * c8 + 3]);
-          __syncwarp();
-          uint32_t wv[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            wv[k] = static_cast<uint32_t>(hs[(2 * k) * 8 + gb]) |
-                    (static_cast<uint32_t>(hs[(2 * k + 1) * 8 + gb]) << 16);
-          __syncwarp();
-          if (mc0 + 8 * c8 + gb < p.M)
-            *reinterpret_cast<uint4*>(crow + c8 * step) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        }
-      }
-      if (split) {
+            for (int h = 0; h < 2; ++h) *frag_ptr(slot, bk, j, h) = acc[bk][j][h];
         __threadfence();
         named_bar_sync(1, kNumEpiWarps * 32);   // all epilogue threads of this CTA have written
         __shared__ int arrived;
@@ -542,45 +501,78 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (!last) continue;
         __threadfence();
         if (threadIdx.x == kEpiWarp0 * 32) p.counters[w.tile] = 0;   // self-cleaning
-        const float* slot0 = p.partials + static_cast<int64_t>(w.tile) * p.ksplit * BT * kTileN;
-        const int et = threadIdx.x - kEpiWarp0 * 32;   // 0..255
-        constexpr int kChunks = BT * (kTileN / 4);       // float4 chunks of the tile
-        constexpr int kPerThread = kChunks / (kNumEpiWarps * 32);
-        constexpr int kBatch = kPerThread < 4 ? kPerThread : 4;
-        // batches of kBatch chunks: all loads of a batch are issued before any use (L2 latency)
-        for (int b0 = 0; b0 < kPerThread; b0 += kBatch) {
-          float4 sum[kBatch];
+        float* slot0 = p.partials + static_cast<int64_t>(w.tile) * p.ksplit * kTileN * BT;
 #pragma unroll
-          for (int k = 0; k < kBatch; ++k) sum[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-          for (int sp = 0; sp < p.ksplit; ++sp) {
-            float4 o[kBatch];
+        for (int bk = 0; bk < 2; ++bk)
 #pragma unroll
-            for (int k = 0; k < kBatch; ++k)
-              o[k] = __ldcg(reinterpret_cast<const float4*>(
-                         slot0 + static_cast<int64_t>(sp) * BT * kTileN) +
-                     et + (b0 + k) * (kNumEpiWarps * 32));
+          for (int j = 0; j < NJ; ++j)
 #pragma unroll
-            for (int k = 0; k < kBatch; ++k) {
-              sum[k].x += o[k].x; sum[k].y += o[k].y; sum[k].z += o[k].z; sum[k].w += o[k].w;
-            }
+            for (int h = 0; h < 2; ++h) acc[bk][j][h] = make_float2(0.0f, 0.0f);
+        for (int sp = 0; sp < p.ksplit; ++sp) {
+          float* sl = slot0 + static_cast<int64_t>(sp) * kTileN * BT;
+#pragma unroll
+          for (int bk = 0; bk < 2; ++bk)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const float2 o = __ldcg(frag_ptr(sl, bk, j, h));
+                acc[bk][j][h].x += o.x;
+                acc[bk][j][h].y += o.y;
+              }
+        }
+      }
+
+      // ---- tile output: stmatrix.trans turns the 8x8 (channel, token) fragments into
+      //      [token][channel] rows of the per-warp staging; each lane then moves 16 bytes
+      //      (8 channels of one token) to C.  fp32 output transposes the high and low 16-bit
+      //      halves separately and re-interleaves them. ----
+      // staging rows: 8 tokens x (32 channels) with an 80-byte pitch (bank-conflict free)
+      const uint32_t st_addr = smem_u32(stg) + (lane & 7) * 80 + (lane >> 3) * 16;
+      const int om = lane >> 2, op = lane & 3;                 // readback: token row, 8-ch piece
+      const int ncol = n0 + q * 32 + 8 * op;
+      for (int j = 0; j < NJ; ++j) {
+        const int m = mc0 + 8 * j + om;
+        if (!p.c_f32) {
+          uint32_t h4[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const __half2 hh = __floats2half2_rn(acc[i >> 1][j][i & 1].x, acc[i >> 1][j][i & 1].y);
+            h4[i] = *reinterpret_cast<const uint32_t*>(&hh);
           }
+          stmatrix_x4_trans(st_addr, h4);
+          __syncwarp();
+          const uint4 v = *reinterpret_cast<const uint4*>(stg + om * 80 + op * 16);
+          __syncwarp();
+          if (m < p.M)
+            *reinterpret_cast<uint4*>(static_cast<__half*>(p.c) + static_cast<int64_t>(m) * p.ldc +
+                                      ncol) = v;
+        } else {
+          uint32_t hi4[4], lo4[4];
 #pragma unroll
-          for (int k = 0; k < kBatch; ++k) {
-            const int idx = et + (b0 + k) * (kNumEpiWarps * 32);
-            const int ml = idx / (kTileN / 4), nl = (idx % (kTileN / 4)) * 4;
-            const int m = m0 + ml;
-            if (m >= p.M) continue;
-            if (p.c_f32) {
-              *reinterpret_cast<float4*>(static_cast<float*>(p.c) + static_cast<int64_t>(m) * p.ldc +
-                                         n0 + nl) = sum[k];
-            } else {
-              const __half2 h0 = __floats2half2_rn(sum[k].x, sum[k].y);
-              const __half2 h1 = __floats2half2_rn(sum[k].z, sum[k].w);
-              *reinterpret_cast<uint2*>(static_cast<__half*>(p.c) + static_cast<int64_t>(m) * p.ldc +
-                                        n0 + nl) =
-                  make_uint2(*reinterpret_cast<const uint32_t*>(&h0),
-                             *reinterpret_cast<const uint32_t*>(&h1));
-            }
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t a = __float_as_uint(acc[i >> 1][j][i & 1].x);
+            const uint32_t c = __float_as_uint(acc[i >> 1][j][i & 1].y);
+            hi4[i] = __byte_perm(a, c, 0x7632);   // (hi(a), hi(c))
+            lo4[i] = __byte_perm(a, c, 0x5410);   // (lo(a), lo(c))
+          }
+          stmatrix_x4_trans(st_addr, hi4);
+          stmatrix_x4_trans(st_addr + 640, lo4);
+          __syncwarp();
+          const uint4 hv = *reinterpret_cast<const uint4*>(stg + om * 80 + op * 16);
+          const uint4 lv = *reinterpret_cast<const uint4*>(stg + 640 + om * 80 + op * 16);
+          __syncwarp();
+          if (m < p.M) {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.c) +
+                                                    static_cast<int64_t>(m) * p.ldc + ncol);
+            dst[0] = make_float4(__uint_as_float(__byte_perm(lv.x, hv.x, 0x5410)),
+                                 __uint_as_float(__byte_perm(lv.x, hv.x, 0x7632)),
+                                 __uint_as_float(__byte_perm(lv.y, hv.y, 0x5410)),
+                                 __uint_as_float(__byte_perm(lv.y, hv.y, 0x7632)));
+            dst[1] = make_float4(__uint_as_float(__byte_perm(lv.z, hv.z, 0x5410)),
+                                 __uint_as_float(__byte_perm(lv.z, hv.z, 0x7632)),
+                                 __uint_as_float(__byte_perm(lv.w, hv.w, 0x5410)),
+                                 __uint_as_float(__byte_perm(lv.w, hv.w, 0x7632)));
           }
         }
       }

@@ -201,6 +201,43 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "memory");
 }
 
+// Warp-collective 16x256b load: 16 TMEM lanes x (8*N) 32-bit columns.  Thread t receives, for
+// each 8-column chunk c < N, the values (lane t/4, col 8c + 2(t%4)), (lane t/4, +1),
+// (lane t/4 + 8, col 8c + 2(t%4)), (lane t/4 + 8, +1) in r[4c .. 4c+3].
+template <int N>
+__device__ __forceinline__ void tmem_ld_16x256b(uint32_t taddr, uint32_t* r);
+
+template <>
+__device__ __forceinline__ void tmem_ld_16x256b<4>(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+template <>
+__device__ __forceinline__ void tmem_ld_16x256b<2>(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+}
+
+// Four 8x8 b16 matrices, transposed on the way to shared memory.  Thread t holds, in h[i], the
+// fragment (row t/4, cols 2(t%4), 2(t%4)+1) of matrix i and provides the address of stored row
+// (t%8) of matrix t/8; stored row c of matrix i receives the 8 values of fragment column c.
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, const uint32_t (&h)[4]) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1,%2,%3,%4};" ::"r"(saddr),
+               "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3])
+               : "memory");
+}
+
 // Warp-collective: store the same 32-bit value to 16 consecutive columns of this thread's lane.
 __device__ __forceinline__ void tmem_st16_const(uint32_t taddr, uint32_t v) {
   asm volatile(
