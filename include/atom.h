@@ -33,6 +33,19 @@
  *   q8      int8  [rows][k_outlier]          symmetric INT8 codes of the outlier block
  *   scales  fp32  [K/128][rows]              group-major; row t < G4 = (K-k_o)/128 is INT4 group
  *           t, the last row is the outlier scale when k_outlier == 128 (one per token / channel)
+ *   x8      int8  [rows][K]                  the same codes, one per byte, in the K order the
+ *           GEMM's tensor-core operand uses (activations only; written by atom_reorder_quantize
+ *           when requested, read by atom_w4a4_gemm).  Group t occupies bytes [128t, 128t+128) of
+ *           a row.  INT4 group (t < G4): reordered channel 128t + 32c + 8i + 2b + h (c, i, b < 4,
+ *           h < 2) sits at byte 128t + 32c + 16h + 4i + b, i.e. within every 32-channel chunk
+ *           the even channels come first, then the odd ones -- the order in which the GEMM
+ *           expands a packed weight nibble pair (low nibble = even channel) to two bytes.  The
+ *           permutation is the same for both operands, so every group dot product is unchanged
+ *           (P:254 Step 1 sums over the group).  INT8 outlier group: natural order (= q8).
+ *           Why: tcgen05 has no 4-bit integer MMA kind, so INT4 must be expanded to int8 on the
+ *           SM; doing it for the activations in the HBM-bound quantize kernel (+1 byte/element
+ *           written) instead of once per output tile inside the GEMM removes 2/3 of the GEMM's
+ *           shared-memory unpack traffic.
  *   Quantizer: s = 2*max|x|*c/(2^n - 1), evaluated as alpha = fl(fl(2c)/(2^n-1)),
  *   s = fl(amax*alpha) (s = FLT_MIN for an all-zero group), q = clamp(rint_even(fl(x*fl(1/s))),
  *   -2^(n-1), 2^(n-1)-1).
@@ -47,7 +60,7 @@
 extern "C" {
 #endif
 
-#define ATOM_ABI_VERSION 1
+#define ATOM_ABI_VERSION 2
 #define ATOM_GROUP 128
 
 typedef enum {
@@ -75,20 +88,26 @@ typedef enum { ATOM_F16 = 0, ATOM_F32 = 1 } atom_dtype_t;
  *   k_outlier  0 or 128
  *   clip_int4  clipping factor of the INT4 groups, in (0,1]; the paper's 0.9 for activations
  *   clip_int8  clipping factor of the INT8 outlier block, in (0,1]; 1.0
- *   q4, q8, scales  outputs as described above (q8 must be NULL iff k_outlier == 0; q4 may be
- *              NULL iff K == k_outlier).  ldx % 8 == 0 (16-byte rows).
+ *   q4, q8, x8, scales  outputs as described above.  scales is required.  q4 (when
+ *              K > k_outlier), q8 (when k_outlier == 128) and x8 are each optional (NULL = not
+ *              written), but q4 must be NULL when K == k_outlier, q8 must be NULL when
+ *              k_outlier == 0, and at least one code output must be given.  The GEMM reads x8;
+ *              q4/q8 are the canonical packed storage format (bit-exact with the oracle).
+ *              ldx % 8 == 0 (16-byte rows).
  *   M == 0 is a no-op.
  */
 atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8,
-                                    uint8_t* q4, int8_t* q8, float* scales, void* stream);
+                                    uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
+                                    void* stream);
 
 /*
  * a0: offline weight reorder + quantize (Fig 4 P:237 "The weight matrix (W) is statically
  * reordered"; P:299 RTN stands in for GPTQ, which only changes the codes offline).  Same math
  * and formats as atom_reorder_quantize with rows = output channels n of W [N][ldw] (nn.Linear
- * layout); the paper's clip is 0.85 for weights.  scales are fp32 [K/128][N].
+ * layout); the paper's clip is 0.85 for weights.  scales are fp32 [K/128][N].  q4 and
+ * q8 are required (when K > k_outlier / k_outlier == 128): the weights stay packed in HBM.
  */
 atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
@@ -101,20 +120,25 @@ atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
  *     C[m][n]   = sum_t a_scales[t][m] * w_scales[t][n] * P_t[m][n]  fp32 accumulation
  *   written to c[m*ldc + n] as fp16 (c_dtype = ATOM_F16) or as the fp32 partial sum (ATOM_F32,
  *   for K-sharded tensor parallelism where partials are all-reduced in fp32).
- *   a_q4/a_q8/a_scales  activations from atom_reorder_quantize (M rows)
+ *   a_x8/a_scales       activations from atom_reorder_quantize (M rows; the x8 operand form)
  *   w_q4/w_q8/w_scales  weights from atom_quantize_weights (N rows), same perm and K
  *   M >= 0 (M == 0 is a no-op), N % 128 == 0, K % 128 == 0, k_outlier in {0,128},
  *   ldc >= N, ldc % 8 == 0 (an N-shard can write its column block into a wider buffer).
  *   debug_partials  NULL, or int32 [K/128][M][N]: every exact group partial P_t (test-only).
  *   workspace       device buffer of at least atom_w4a4_gemm_workspace_size(M, N, K, k_outlier)
- *                   bytes, 16-byte aligned (may be NULL when that size is 0).  Used when the
- *                   output tiles alone cannot fill the GPU (small M): the K groups are split
- *                   across CTAs, each split publishes fp32 partials there and the last one to
- *                   finish reduces them.  Contents need not be initialised (the call clears its
- *                   counters with one cudaMemsetAsync on `stream`).  Must not be shared by calls
- *                   that may run concurrently.
+ *                   bytes, 16-byte aligned (may be NULL when that size is 0).  The (tile,
+ *                   K-group) work is divided evenly over one persistent CTA per SM ("stream-K"),
+ *                   so an output tile may be computed in K segments by consecutive CTAs; the
+ *                   segments publish fp32 partials and per-tile arrival counters there and the
+ *                   CTA holding the tile's last segment sums them in a fixed order
+ *                   (deterministic).  The first atom_w4a4_gemm_counter_bytes() bytes hold
+ *                   arrival counters: they MUST be zero before the first use, and every completed
+ *                   call leaves them zero again (self-cleaning), so no per-call memset is
+ *                   launched and one buffer can serve every shape on the device; the rest is
+ *                   scratch.  Must not be shared by calls that may run concurrently, and the
+ *                   counters must be re-zeroed if a call was aborted.
  */
-atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
+atom_status_t atom_w4a4_gemm(const int8_t* a_x8, const float* a_scales,
                              const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
                              int64_t M, int64_t N, int64_t K, int32_t k_outlier,
                              void* c, int64_t ldc, atom_dtype_t c_dtype,
@@ -122,8 +146,12 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
                              void* stream);
 
 /* Bytes of device workspace atom_w4a4_gemm needs for this shape on the CURRENT device (0 when
- * no split-K is planned, or when the current device is not an sm_100 GPU). */
+ * no output tile is split between CTAs, or when the current device is not an sm_100 GPU). */
 size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier);
+
+/* Size of the leading counter region of every GEMM workspace on the CURRENT device (the part
+ * that must be zero before first use; 0 when the device is not an sm_100 GPU). */
+size_t atom_w4a4_gemm_counter_bytes(void);
 
 /* Test helper: on `stream`, sets *ok_flag (device int32) to 1 iff perm[0..K) is a bijection of
  * [0,K) (ldx == K) or an injection into [0,ldx).  scratch: device int32 [ldx], clobbered. */

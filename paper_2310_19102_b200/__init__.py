@@ -28,7 +28,8 @@ ATOM_F16, ATOM_F32 = 0, 1
 
 # every symbol include/atom.h declares
 ABI_SYMBOLS = ("atom_reorder_quantize", "atom_quantize_weights", "atom_w4a4_gemm",
-               "atom_w4a4_gemm_workspace_size", "atom_validate_perm", "atom_status_string",
+               "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_counter_bytes",
+               "atom_validate_perm", "atom_status_string",
                "atom_abi_version", "atom_last_launch_count")
 
 
@@ -52,12 +53,13 @@ def _lib():
         L = ctypes.CDLL(str(LIB_PATH))
         P, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
         q_args = [P, i64, i64, P, i64, i32, f32, f32, P, P, P, P]
-        L.atom_reorder_quantize.argtypes = q_args
+        L.atom_reorder_quantize.argtypes = q_args[:10] + [P] + q_args[10:]
         L.atom_quantize_weights.argtypes = q_args
-        L.atom_w4a4_gemm.argtypes = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int,
+        L.atom_w4a4_gemm.argtypes = [P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int,
                                      P, P, ctypes.c_size_t, P]
         L.atom_w4a4_gemm_workspace_size.argtypes = [i64, i64, i64, i32]
         L.atom_w4a4_gemm_workspace_size.restype = ctypes.c_size_t
+        L.atom_w4a4_gemm_counter_bytes.restype = ctypes.c_size_t
         L.atom_validate_perm.argtypes = [P, i64, i64, P, P, P]
         L.atom_status_string.argtypes = [ctypes.c_int]
         L.atom_status_string.restype = ctypes.c_char_p
@@ -100,20 +102,24 @@ def _check(st: int, what: str):
 
 @dataclass
 class Quantized:
-    """Packed operand: q4 uint8 [rows][(K-k_o)/2], q8 int8 [rows][k_o] (or None),
-    scales fp32 [K/128][rows] (group-major), with the reordered K and k_outlier."""
+    """Quantized operand: q4 uint8 [rows][(K-k_o)/2] packed INT4, q8 int8 [rows][k_o] (or None),
+    scales fp32 [K/128][rows] (group-major), with the reordered K and k_outlier.  Activations
+    also carry x8 int8 [rows][K]: the same codes one per byte in the GEMM operand order
+    (include/atom.h), which is what atom_w4a4_gemm reads."""
     q4: object
     q8: object
     scales: object
     K: int
     k_outlier: int
+    x8: object = None
 
     @property
     def rows(self) -> int:
         return int(self.scales.shape[1])
 
 
-def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream):
+def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream, x8=False,
+              packed=True):
     import torch
     if x.dtype != torch.float16 or x.dim() != 2 or not x.is_cuda:
         raise TypeError("expected a 2-D CUDA fp16 tensor")
@@ -126,23 +132,30 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream)
     if out is None:
         dev = x.device
         q4 = torch.empty((rows, (K - k_outlier) // 2), dtype=torch.uint8, device=dev) \
-            if K > k_outlier else None
-        q8 = torch.empty((rows, k_outlier), dtype=torch.int8, device=dev) if k_outlier else None
+            if K > k_outlier and packed else None
+        q8 = torch.empty((rows, k_outlier), dtype=torch.int8, device=dev) \
+            if k_outlier and packed else None
         sc = torch.empty((K // GROUP, rows), dtype=torch.float32, device=dev)
-        out = Quantized(q4, q8, sc, K, k_outlier)
+        xx = torch.empty((rows, K), dtype=torch.int8, device=dev) if x8 else None
+        out = Quantized(q4, q8, sc, K, k_outlier, xx)
+    codes = (_ptr(out.q4), _ptr(out.q8))
+    if fn_name == "atom_reorder_quantize":
+        codes = codes + (_ptr(out.x8),)
     st = getattr(_lib(), fn_name)(_ptr(x), rows, ld, _ptr(perm), K, k_outlier,
                                   ctypes.c_float(clip_int4), ctypes.c_float(clip_int8),
-                                  _ptr(out.q4), _ptr(out.q8), _ptr(out.scales), _stream(stream))
+                                  *codes, _ptr(out.scales), _stream(stream))
     _check(st, fn_name)
     return out
 
 
 def reorder_quantize(x, perm, K: Optional[int] = None, k_outlier: int = 128,
                      clip_int4: float = 0.9, clip_int8: float = 1.0, out: Quantized = None,
-                     stream=None) -> Quantized:
-    """a1: reorder + dynamically quantize activations x fp16 [M][ldx] (clip 0.9)."""
+                     stream=None, packed: bool = True) -> Quantized:
+    """a1: reorder + dynamically quantize activations x fp16 [M][ldx] (clip 0.9).
+
+    Writes the GEMM operand form x8 and, unless ``packed=False``, the canonical packed q4/q8."""
     return _quantize("atom_reorder_quantize", x, perm, K, k_outlier, clip_int4, clip_int8, out,
-                     stream)
+                     stream, x8=True, packed=packed)
 
 
 def quantize_weights(w, perm, K: Optional[int] = None, k_outlier: int = 128,
@@ -155,6 +168,31 @@ def quantize_weights(w, perm, K: Optional[int] = None, k_outlier: int = 128,
 
 def workspace_size(M: int, N: int, K: int, k_outlier: int = 128) -> int:
     return int(_lib().atom_w4a4_gemm_workspace_size(M, N, K, k_outlier))
+
+
+def counter_bytes() -> int:
+    """Leading bytes of every GEMM workspace that must be zero between calls (include/atom.h)."""
+    return int(_lib().atom_w4a4_gemm_counter_bytes())
+
+
+_WORKSPACES = {}
+
+
+def gemm_workspace(M: int, N: int, K: int, k_outlier: int = 128, stream=None):
+    """A zero-filled GEMM workspace for this shape, cached per (device, stream): the GEMM leaves
+    it zero-filled after every completed call (include/atom.h), so it is cleared only once."""
+    import torch
+    n = workspace_size(M, N, K, k_outlier)
+    if n == 0:
+        return None
+    s = torch.cuda.current_stream() if stream is None else stream
+    key = (s.device.index, s.cuda_stream)
+    ws = _WORKSPACES.get(key)
+    if ws is None or ws.numel() < n:
+        with torch.cuda.stream(s):
+            ws = torch.zeros(n, dtype=torch.uint8, device=s.device)
+        _WORKSPACES[key] = ws
+    return ws
 
 
 def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partials=None,
@@ -174,10 +212,11 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
     if out.dtype not in (torch.float16, torch.float32) or out.stride(1) != 1:
         raise TypeError("out must be fp16/fp32 with contiguous rows")
     c_dtype = ATOM_F16 if out.dtype == torch.float16 else ATOM_F32
-    ws_bytes = workspace_size(M, N, a.K, a.k_outlier)
-    if ws_bytes and workspace is None:
-        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=out.device)
-    st = _lib().atom_w4a4_gemm(_ptr(a.q4), _ptr(a.q8), _ptr(a.scales), _ptr(w.q4), _ptr(w.q8),
+    if a.x8 is None:
+        raise ValueError("activations lack the x8 operand form (use reorder_quantize)")
+    if workspace is None:
+        workspace = gemm_workspace(M, N, a.K, a.k_outlier, stream)
+    st = _lib().atom_w4a4_gemm(_ptr(a.x8), _ptr(a.scales), _ptr(w.q4), _ptr(w.q8),
                                _ptr(w.scales), M, N, a.K, a.k_outlier, _ptr(out), out.stride(0),
                                c_dtype, _ptr(debug_partials), _ptr(workspace),
                                0 if workspace is None else workspace.numel(), _stream(stream))

@@ -52,7 +52,8 @@ bool clip_ok(float c) { return c > 0.0f && c <= 1.0f; }
 
 atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
                                int64_t K, int32_t k_o, float clip4, float clip8,
-                               const uint8_t* q4, const int8_t* q8, const float* scales) {
+                               const uint8_t* q4, const int8_t* q8, const int8_t* x8,
+                               const float* scales, bool packed_required) {
   if (rows < 0) return ATOM_ERR_SHAPE;
   if (!(k_o == 0 || k_o == ATOM_GROUP)) return ATOM_ERR_ARG;
   if (K <= 0 || K % ATOM_GROUP != 0 || K < k_o) return ATOM_ERR_SHAPE;
@@ -62,24 +63,31 @@ atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const in
   if (ld * 2 > 227 * 1024) return ATOM_ERR_SHAPE;  // the source row is staged in shared memory
   if (rows == 0) return ATOM_OK;
   if (!x || !perm || !scales) return ATOM_ERR_NULL;
-  if ((K > k_o) != (q4 != nullptr)) return ATOM_ERR_NULL;
-  if ((k_o > 0) != (q8 != nullptr)) return ATOM_ERR_NULL;
+  // forbidden outputs: q4 without INT4 groups, q8 without the outlier block
+  if ((K == k_o && q4 != nullptr) || (k_o == 0 && q8 != nullptr)) return ATOM_ERR_NULL;
+  if (packed_required) {
+    if ((K > k_o) != (q4 != nullptr) || (k_o > 0) != (q8 != nullptr)) return ATOM_ERR_NULL;
+  } else if (!q4 && !q8 && !x8) {
+    return ATOM_ERR_NULL;
+  }
   if (!aligned16(x) || !aligned16(perm) || !aligned16(scales) || (q4 && !aligned16(q4)) ||
-      (q8 && !aligned16(q8)))
+      (q8 && !aligned16(q8)) || (x8 && !aligned16(x8)))
     return ATOM_ERR_ALIGN;
   return ATOM_OK;
 }
 
 atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
                               int64_t K, int32_t k_o, float clip4, float clip8, uint8_t* q4,
-                              int8_t* q8, float* scales, void* stream) {
+                              int8_t* q8, int8_t* x8, float* scales, bool packed_required,
+                              void* stream) {
   g_last_launches = 0;
-  atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, scales);
+  atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, x8, scales,
+                                      packed_required);
   if (st != ATOM_OK || rows == 0) return st;
   DeviceInfo dev;
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   cudaError_t e = atom::launch_reorder_quantize(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8,
-                                                scales, static_cast<cudaStream_t>(stream),
+                                                x8, scales, static_cast<cudaStream_t>(stream),
                                                 dev.num_sms);
   if (e != cudaSuccess) return ATOM_ERR_CUDA;
   g_last_launches = 1;
@@ -93,17 +101,17 @@ extern "C" {
 atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
-                                    float* scales, void* stream) {
-  return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, scales,
-                         stream);
+                                    int8_t* x8, float* scales, void* stream) {
+  return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, x8,
+                         scales, false, stream);
 }
 
 atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
                                     float* scales, void* stream) {
-  return quantize_common(w_f16, N, ldw, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, scales,
-                         stream);
+  return quantize_common(w_f16, N, ldw, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, nullptr,
+                         scales, true, stream);
 }
 
 size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
@@ -114,7 +122,13 @@ size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_
   return atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
 }
 
-atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
+size_t atom_w4a4_gemm_counter_bytes(void) {
+  DeviceInfo dev;
+  if (current_device(&dev) != ATOM_OK) return 0;
+  return ((static_cast<size_t>(dev.num_sms) * sizeof(int) + 255) / 256) * 256;
+}
+
+atom_status_t atom_w4a4_gemm(const int8_t* a_x8, const float* a_scales,
                              const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
                              int64_t M, int64_t N, int64_t K, int32_t k_outlier, void* c,
                              int64_t ldc, atom_dtype_t c_dtype, int32_t* debug_partials,
@@ -127,12 +141,12 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
   if (ldc < N || ldc % 8 != 0) return ATOM_ERR_SHAPE;
   if (!(c_dtype == ATOM_F16 || c_dtype == ATOM_F32)) return ATOM_ERR_ARG;
   if (M == 0) return ATOM_OK;
-  if (!a_scales || !w_scales || !c) return ATOM_ERR_NULL;
+  if (!a_x8 || !a_scales || !w_scales || !c) return ATOM_ERR_NULL;
   const bool has4 = K > k_outlier, has8 = k_outlier > 0;
-  if (has4 != (a_q4 != nullptr) || has4 != (w_q4 != nullptr)) return ATOM_ERR_NULL;
-  if (has8 != (a_q8 != nullptr) || has8 != (w_q8 != nullptr)) return ATOM_ERR_NULL;
-  if (!aligned16(a_scales) || !aligned16(w_scales) || !aligned16(c) ||
-      (a_q4 && !aligned16(a_q4)) || (w_q4 && !aligned16(w_q4)) || (a_q8 && !aligned16(a_q8)) ||
+  if (has4 != (w_q4 != nullptr)) return ATOM_ERR_NULL;
+  if (has8 != (w_q8 != nullptr)) return ATOM_ERR_NULL;
+  if (!aligned16(a_scales) || !aligned16(w_scales) || !aligned16(c) || !aligned16(a_x8) ||
+      (w_q4 && !aligned16(w_q4)) ||
       (w_q8 && !aligned16(w_q8)) || (debug_partials && !aligned16(debug_partials)))
     return ATOM_ERR_ALIGN;
   DeviceInfo dev;
@@ -142,8 +156,7 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
   if (ws > 0 && (workspace == nullptr || workspace_bytes < ws || !aligned16(workspace)))
     return ATOM_ERR_WORKSPACE;
   atom::GemmArgs a;
-  a.a_q4 = a_q4;
-  a.a_q8 = a_q8;
+  a.a_x8 = a_x8;
   a.a_scales = a_scales;
   a.w_q4 = w_q4;
   a.w_q8 = w_q8;

@@ -8,21 +8,28 @@
 // B200 design:
 //   * swap-AB: the MMA M side (128 TMEM lanes) is 128 output channels n of W, the MMA N side is a
 //     tile of BT tokens.  D[n][m] = sum_k W'[n][k] A'[m][k].
-//   * TMA streams the PACKED INT4 tiles (64 B per row per group) into a 4-stage ring; the INT8
-//     outlier group arrives as two 64-byte halves through the same ring.
-//   * 4 unpack warps expand nibbles to int8 16*q (high nibbles: one LOP per 4 codes; low nibbles:
-//     SHL + LOP; exact two's complement) directly into the 128B-swizzled K-major layout the UMMA
-//     descriptor reads, with the same intra-group channel permutation for both operands (the dot
-//     product is order-invariant).  tcgen05 has no s4 kind, so this is the INT4 -> INT8 step.
-//   * 1 MMA thread per group: 4 x kind::i8 (K = 32) into a fresh TMEM int32 accumulator (4 TMEM
-//     buffers rotate ACROSS groups so later groups multiply while the epilogue drains earlier
-//     ones) and ONE tcgen05.commit that both frees the unpacked operands and publishes the
-//     partial.  INT4 partials come out as R = 256*P_t (exact, |R| <= 2^21).
-//   * 8 epilogue warps (thread = output channel = TMEM lane) tcgen05.ld the partials, turn R into
-//     the float 1.5*2^23 + R with one LOP3 ((R & 0x7FFFFF) ^ 0x4B400000, exact for |R| < 2^22)
-//     and dequantize with two FFMA2 per column pair; fp32
-//     accumulators live in registers; after the last group they write fp16 (or fp32 for K-shards).
-//   * persistent CTAs (one per SM) walk output tiles; consecutive CTAs share the weight tile.
+//   * weights stay PACKED in HBM: TMA streams 64-byte-per-row INT4 tiles into a 4-stage ring and
+//     2 unpack warps expand the nibbles to int8 16*q (high nibbles: one LOP per 4 codes; low
+//     nibbles: SHF.L.W + LOP; exact two's complement) directly into the 128B-swizzled K-major
+//     layout the UMMA descriptor reads.  tcgen05 has no s4 kind, so this is the INT4 -> INT8 step.
+//     The INT8 outlier group arrives as two 64-byte halves through the same ring.
+//   * activations arrive MMA-ready: atom_reorder_quantize writes the codes one per byte in the
+//     same intra-group order the weight unpack produces (atom.h "x8"), so TMA (SWIZZLE_128B)
+//     drops them straight into the operand buffer; no SM work, a third of the old SMEM traffic.
+//   * 1 MMA thread per group: 4 x kind::i8 (K = 32) into a TMEM int32 accumulator (RT buffers
+//     rotate across groups so later groups multiply while the epilogue drains earlier ones) and
+//     ONE tcgen05.commit that frees the operand slot and publishes the partial.  INT4 partials
+//     come out as R = 16*P_t (exact, |R| <= 2^17).
+//   * 12 epilogue warps (thread = output channel = TMEM lane, 3 warps per lane quarter, each a
+//     third of the token columns) tcgen05.ld the partials, read them as the float
+//     1.5*2^23 + R (magic-prefilled accumulators, or one LOP3), dequantize with one FFMA2 and
+//     accumulate with one more; fp32 accumulators live in
+//     registers; after the tile's last group they write fp16 (or fp32 for K-shards).
+//   * stream-K schedule: the (tile, group) units are divided evenly over one persistent CTA per
+//     SM.  A tile cut between CTAs is computed in K segments; every segment but the last
+//     publishes its fp32 partial in the workspace, the CTA with the last segment adds them in a
+//     fixed order (deterministic) and stores.  Each CTA walks its tiles in descending order, so
+//     the segments it publishes are its first work and the one it reduces is its last.
 #include <cstdint>
 #include <cstdio>
 #include <type_traits>
@@ -38,26 +45,31 @@ namespace atom {
 
 // Warp roles (16 warps, 4 warpgroups):
 //   WG0: warp 0 producer (scales via cp.async + TMA), warp 1 MMA issuer, warps 2-3 unpack
-//   WG1: warps 4-7 unpack
-//   WG2, WG3: warps 8-15 epilogue (warp % 4 = TMEM lane quarter; WG2 = token columns [0, BT/2),
-//             WG3 = [BT/2, BT))
-// setmaxnreg moves registers from WG0/WG1 (72 each) to the epilogue warpgroups (184 each), which
-// hold the fp32 accumulators of a 128 x BT tile (BT/2 per thread).
+//   WG1-WG3: warps 4-15 epilogue (warp % 4 = TMEM lane quarter, (warp - 4) / 4 = column third)
+// setmaxnreg moves registers from WG0 (56 each) to the epilogue warpgroups (152 each), which
+// hold the fp32 accumulators of a 128 x BT tile (BT/3 per thread).
 constexpr int kThreads = 512;
 constexpr int kUnpackWarp0 = 2;
-constexpr int kNumUnpackWarps = 6;
-constexpr int kEpiWarp0 = 8;
-constexpr int kNumEpiWarps = 8;
-constexpr int kRegsLow = 64, kRegsHigh = 192;           // 8*32*64 + 8*32*192 = 65536
+constexpr int kNumUnpackWarps = 2;
+constexpr int kEpiWarp0 = 4;
+constexpr int kNumEpiWarps = 12;
+constexpr int kEpiThreads = kNumEpiWarps * 32;
+constexpr int kRegsLow = 56, kRegsHigh = 152;           // 4*32*56 + 12*32*152 = 65536
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
-constexpr int kStages = 4;      // packed-tile TMA ring depth
 constexpr int kSRing = 8;       // group-scale ring depth
 
 template <int BT> struct Cfg {
-  static constexpr int kRing = BT >= 256 ? 2 : 4;       // unpacked operands == TMEM accumulators
-  static constexpr uint32_t kTmemCols = kRing * BT <= 32 ? 32 : kRing * BT <= 64 ? 64
-                                      : kRing * BT <= 128 ? 128 : kRing * BT <= 256 ? 256 : 512;
-  static_assert(kRing * BT <= 512, "TMEM holds at most 512 columns");
+  static constexpr int RT = BT >= 256 ? 2 : 4;          // TMEM accumulator buffers
+  static constexpr int RS = BT >= 256 ? 3 : 4;          // operand slots (unpacked W + A tile)
+  static constexpr int kStages = BT >= 256 ? 6 : 8;     // packed weight TMA ring depth
+  static constexpr uint32_t kTmemCols = RT * BT <= 32 ? 32 : RT * BT <= 64 ? 64
+                                      : RT * BT <= 128 ? 128 : RT * BT <= 256 ? 256 : 512;
+  static constexpr int NC = BT / 8;                     // 8-column chunks of the tile
+  static constexpr int NJ = (NC + 2) / 3;               // chunks per epilogue warp (max)
+  // split-tile partial of one CTA: thread-linear, [12 warps][NJ*8/4 column quads][32 lanes] float4
+  static constexpr size_t kSlotFloats = static_cast<size_t>(kNumEpiWarps) * NJ * 8 * 32;
+  static_assert(RT * BT <= 512, "TMEM holds at most 512 columns");
+  static_assert(RS >= RT, "an operand slot must outlive its accumulator");
 };
 
 constexpr uint32_t kMagicBits = 0x4B400000u;   // bit pattern of 1.5*2^23
@@ -69,29 +81,39 @@ struct GemmParams {
   void* c;
   int64_t ldc;
   int32_t* debug;
-  int M, N, G, G4, k_o, c_f32;
+  int M, N, G, G4, c_f32;
   int m_tiles, num_tiles;
-  int ksplit, num_items;     // split-K: item = tile * ksplit + split
-  float* partials;           // [num_tiles][ksplit][128][BT] fp32 (ksplit > 1)
-  int* counters;             // [num_tiles] arrival counters, zeroed by the launcher (ksplit > 1)
-  long long* trace;   // development timeline probe (CTA 0): [3][256] clock64 stamps, or null
+  int dp_waves;              // whole tiles per CTA dealt round-robin
+  int64_t sk_base;           // first stream-K unit (= dp_waves * grid * G)
+  int64_t sk_units;          // stream-K (tile, group) units
+  float* partials;           // [gridDim.x][kSlotFloats] split-tile partials
+  int* counters;             // [gridDim.x] arrivals per reducing CTA (zero between launches)
+  long long* trace;          // development timeline probe (ATOM_GEMM_TRACE): [8][kTraceN] clocks
 };
+constexpr int kTraceN = 512;
+// development probe: clock64 of event ev for group g of CTA 0 (no-op unless p.trace is set)
+#define TRACE(ev, g)                                                                          \
+  do {                                                                                        \
+    if (p.trace != nullptr && blockIdx.x == 0 && (g) < kTraceN)                               \
+      p.trace[(ev) * kTraceN + (g)] = clock64();                                              \
+  } while (0)
 
 template <int BT>
 struct __align__(1024) GemmSmem {
-  static constexpr int R = Cfg<BT>::kRing;
-  uint8_t ubuf_w[R][kTileN * 128];      // unpacked weight group, SW128 K-major
-  uint8_t ubuf_a[R][BT * 128];          // unpacked activation group, SW128 K-major
-  uint8_t stage_w[kStages][kTileN * 64];// packed weight group (or half of the INT8 group)
-  uint8_t stage_a[kStages][BT * 64];    // packed activation group
+  static constexpr int RS = Cfg<BT>::RS;
+  static constexpr int RT = Cfg<BT>::RT;
+  uint8_t ubuf_w[RS][kTileN * 128];     // unpacked weight group, SW128 K-major
+  uint8_t ubuf_a[RS][BT * 128];         // activation group (x8), SW128 K-major, written by TMA
+  uint8_t stage_w[Cfg<BT>::kStages][kTileN * 64];   // packed weight group (or INT8 half)
   float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
   float ssa[kSRing][BT];                // activation scales of a group
-  uint8_t ostg[kNumEpiWarps][1280];     // per-warp output staging (2 x 8 rows x 80 B)
-  uint32_t magic4[4];                   // 4 copies of the magic bit pattern
-  uint64_t full[kStages], empty[kStages];
-  uint64_t ufull[R];
-  uint64_t mdone[R];                    // MMAs of a group done: operands free + partial ready
-  uint64_t tempty[R];
+  uint8_t ostg[kNumEpiWarps][1024];     // per-warp output staging ([8 tokens][32 ch] fp32)
+  uint64_t full[Cfg<BT>::kStages], empty[Cfg<BT>::kStages];
+  // go[u]: group g (slot u = g % RS) may be issued -- its weights are unpacked (2 arrivals),
+  // its activations landed (1 arrival + tx bytes) and its TMEM buffer was drained (12 epilogue
+  // arrivals, made when group g - RT was released).  One barrier, one probe per group.
+  uint64_t go[RS];
+  uint64_t mdone[RS];                   // MMAs of a group done: slot free + partial ready
   uint64_t sready[kSRing], sfree[kSRing];
   uint32_t tmem_base;
 };
@@ -114,9 +136,11 @@ __device__ __forceinline__ float biased(uint32_t r, uint32_t magic) {
   return __uint_as_float(and_xor(r, 0x007FFFFFu, magic));
 }
 
-// KR rows of an operand tile, ROW_STEP apart (a multiple of 8, so all share one swizzle phase):
+// KR rows of the weight tile, ROW_STEP apart (a multiple of 8, so all share one swizzle phase):
 // packed stage [rows][64 B] -> unpacked SW128 [rows][128 B].  This thread owns the 16-byte
 // packed chunk c of rows r0 + k*ROW_STEP; every address is a per-thread base plus an immediate.
+// Packed chunk c holds channels 32c..32c+31; its low nibbles (even channels) become 16-byte
+// chunk 2c and its high nibbles (odd channels) chunk 2c+1 -- the x8 order of atom.h.
 template <int KR, int ROW_STEP>
 __device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf, uint32_t r0,
                                             uint32_t c, bool int4, int h) {
@@ -141,64 +165,144 @@ __device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf,
   }
 }
 
-__device__ __forceinline__ long long globaltimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+// ---- schedule ("data-parallel waves + stream-K tail"): the first dp_waves * gridDim.x tiles are
+//      whole tiles dealt round-robin (CTA i takes tiles i, i + grid, ...: neighbouring CTAs
+//      share a weight tile at the same time, so it is read from HBM once); the remaining tiles'
+//      (tile, group) units are divided evenly, CTA i owning [sk_start(i), sk_start(i+1)).  A tile
+//      cut by those boundaries is computed in K segments by consecutive CTAs.  Each CTA first
+//      works on its highest stream-K tile (a tile head it publishes, or a whole tile), then its
+//      data-parallel tiles, then its remaining stream-K tiles in descending order (the last one
+//      may be a tile tail it reduces), so reducers find the published segments ready. ----
+__device__ __forceinline__ int64_t sk_start(const GemmParams& p, int64_t i) {
+  return p.sk_base + i * p.sk_units / gridDim.x;
+}
+// CTA whose stream-K range contains unit u (u >= sk_base).
+__device__ __forceinline__ int cta_of(const GemmParams& p, int64_t u) {
+  int64_t i = ((u - p.sk_base) * gridDim.x) / p.sk_units;
+  while (i + 1 < gridDim.x && sk_start(p, i + 1) <= u) ++i;
+  while (i > 0 && sk_start(p, i) > u) --i;
+  return static_cast<int>(i);
 }
 
-// One work item = (output tile, K split).  Splits cover contiguous group ranges; the INT8 outlier
-// group (the last one) therefore always lands in the last split.
+struct Sched {
+  int64_t u0, u1;   // this CTA's stream-K units
+  int t_hi;         // highest stream-K tile touched
+  int ns, nd;       // number of stream-K items / data-parallel tiles
+  __device__ __forceinline__ int count() const { return ns + nd; }
+};
+__device__ __forceinline__ Sched make_sched(const GemmParams& p) {
+  Sched s;
+  s.u0 = sk_start(p, blockIdx.x);
+  s.u1 = sk_start(p, blockIdx.x + 1);
+  s.nd = p.dp_waves;
+  if (s.u1 > s.u0) {
+    s.t_hi = static_cast<int>((s.u1 - 1) / p.G);
+    s.ns = s.t_hi - static_cast<int>(s.u0 / p.G) + 1;
+  } else {
+    s.t_hi = 0;
+    s.ns = 0;
+  }
+  return s;
+}
+
 struct Item {
-  int n0, m0, t0, t1, tile, split;
+  int n0, m0, t0, t1, tile;
 };
 template <int BT>
-__device__ __forceinline__ Item make_item(const GemmParams& p, int item) {
+__device__ __forceinline__ Item get_item(const GemmParams& p, const Sched& s, int k) {
   Item it;
-  it.tile = item / p.ksplit;
-  it.split = item - it.tile * p.ksplit;
-  it.n0 = (it.tile / p.m_tiles) * kTileN;
-  it.m0 = (it.tile % p.m_tiles) * BT;
-  it.t0 = it.split * p.G / p.ksplit;
-  it.t1 = (it.split + 1) * p.G / p.ksplit;
+  int tile;
+  bool sk = true;
+  if (s.ns > 0 && k == 0) {
+    tile = s.t_hi;
+  } else {
+    const int kk = k - (s.ns > 0 ? 1 : 0);
+    if (kk < s.nd) {
+      tile = static_cast<int>(blockIdx.x) + kk * static_cast<int>(gridDim.x);
+      sk = false;
+    } else {
+      tile = s.t_hi - (kk - s.nd + 1);
+    }
+  }
+  it.tile = tile;
+  if (sk) {
+    const int64_t base = static_cast<int64_t>(tile) * p.G;
+    it.t0 = static_cast<int>((s.u0 > base ? s.u0 : base) - base);
+    it.t1 = static_cast<int>((s.u1 < base + p.G ? s.u1 : base + p.G) - base);
+  } else {
+    it.t0 = 0;
+    it.t1 = p.G;
+  }
+  it.n0 = (tile / p.m_tiles) * kTileN;
+  it.m0 = (tile % p.m_tiles) * BT;
   return it;
 }
 
-// kMode (development timing probes, never used for results): bit 0 = epilogue skips its
-// arithmetic; bit 1 = unpack skips its data movement; bit 2 = producer skips the TMA loads;
-// bit 3 = epilogue skips the TMEM loads; bit 4 = waits spin without the suspend-time hint;
-// bit 5 = no output stores; bit 6 = no magic prefill (every buffer converted with LOP3).
+// Walks this CTA's (item, group) sequence one group at a time.
+template <int BT>
+struct GroupCursor {
+  int k, t, t1, m0;
+  __device__ __forceinline__ bool valid(const Sched& s) const { return k < s.count(); }
+  __device__ __forceinline__ void load(const GemmParams& p, const Sched& s) {
+    if (k < s.count()) {
+      const Item w = get_item<BT>(p, s, k);
+      t = w.t0;
+      t1 = w.t1;
+      m0 = w.m0;
+    }
+  }
+  __device__ __forceinline__ void next(const GemmParams& p, const Sched& s) {
+    if (++t >= t1) {
+      ++k;
+      load(p, s);
+    }
+  }
+};
+
+// ring position: slot index + phase parity, advanced one step at a time (no division)
+template <int N>
+struct Ring {
+  uint32_t i = 0, ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++i == N) {
+      i = 0;
+      ph ^= 1;
+    }
+  }
+};
+
+// kMode (development timing probes, never used for results): bit 0 = the epilogue skips its
+// arithmetic; bit 1 = it skips the TMEM loads; bit 2 = magic re-arm of even buffers by tcgen05.st
+// instead of the LOP3 conversion; bit 3 = no output stores; bit 4 = no activation TMA (arrive only); bit 5 = no
+// weight TMA; bit 6 = unpack skips its data movement.
 template <int BT, bool kDebug, int kMode = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
-                 const __grid_constant__ CUtensorMap tm_aq4,
                  const __grid_constant__ CUtensorMap tm_wq8,
-                 const __grid_constant__ CUtensorMap tm_aq8, const GemmParams p) {
+                 const __grid_constant__ CUtensorMap tm_ax8, const GemmParams p) {
   static_assert(BT % 32 == 0 && BT >= 32 && BT <= 256, "token tile");
-  constexpr int R = Cfg<BT>::kRing;
-  constexpr uint32_t kTmemCols = Cfg<BT>::kTmemCols;
-  constexpr bool kPrefillEven = (kMode & 64) == 0;   // even buffers carry the magic bias
-  auto wait = [](uint64_t* bar, uint32_t parity) {
-    if constexpr ((kMode & 16) != 0) mbar_wait_spin(bar, parity);
-    else mbar_wait(bar, parity);
-  };
+  using C = Cfg<BT>;
+  constexpr int RS = C::RS, RT = C::RT, NJ = C::NJ, NC = C::NC, KS = C::kStages;
+  constexpr uint32_t kTmemCols = C::kTmemCols;
   extern __shared__ uint8_t smem_raw[];
   GemmSmem<BT>& sm = *reinterpret_cast<GemmSmem<BT>*>(
       smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < 256)
-    p.trace[768 + blockIdx.x] = globaltimer();
+  // waits on the MMA <-> epilogue critical loop: spin (bit 7 of kMode: suspend-hinted instead)
+  auto wait_hot = [](uint64_t* bar, uint32_t parity) {
+    if constexpr ((kMode & 128) != 0) mbar_wait(bar, parity);
+    else mbar_wait_spin(bar, parity);
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < KS; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kNumUnpackWarps);
     }
-    for (int u = 0; u < R; ++u) {
-      mbar_init(&sm.ufull[u], kNumUnpackWarps);
+    for (int u = 0; u < RS; ++u) {
+      mbar_init(&sm.go[u], kNumUnpackWarps + 1 + kNumEpiWarps);   // unpack, A tile, epilogue
       mbar_init(&sm.mdone[u], 1);
-      mbar_init(&sm.tempty[u], kNumEpiWarps);
     }
     for (int r = 0; r < kSRing; ++r) {
       mbar_init(&sm.sready[r], 32);  // one cp.async-arrive per producer-warp thread
@@ -208,59 +312,51 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_wq4);
-    tma_prefetch_desc(&tm_aq4);
     tma_prefetch_desc(&tm_wq8);
-    tma_prefetch_desc(&tm_aq8);
+    tma_prefetch_desc(&tm_ax8);
   }
-  if (threadIdx.x < 4) sm.magic4[threadIdx.x] = kMagicBits;
   if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-
   const int G4 = p.G4;
+  const Sched sch = make_sched(p);
+  const int n_items = sch.count();
 
   if (warp < kEpiWarp0) setmaxnreg_dec<kRegsLow>();
   if (warp == 0) {
-    // ===================== producer warp: group scales (cp.async) + TMA =====================
-    // The scales of a group are staged into the scale ring when its first stage is loaded,
-    // several groups ahead of the epilogue, which hides the L2 latency of the 4-byte copies
-    // (cp.async works for any M; TMA would need 16-byte aligned rows).
-    uint32_t it = 0, g_it = 0;
-    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
-      const Item w = make_item<BT>(p, item);
-      for (int t = w.t0; t < w.t1; ++t, ++g_it) {
-        {
-          const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
-          wait(&sm.sfree[sr], sph ^ 1);
-          const float* ws = p.w_scales + static_cast<int64_t>(t) * p.N + w.n0;
-          const float* as = p.a_scales + static_cast<int64_t>(t) * p.M;
+    // ===================== producer warp: group scales (cp.async) + packed weights (TMA) =====
+    // Not tied to the operand slots, so the weight stream runs up to KS stages ahead.  (The
+    // activation tiles are issued by the epilogue as slots free up, see below.)
+    Ring<KS> st;
+    Ring<kSRing> sr;
+    int gp = 0;
+    for (int k = 0; k < n_items; ++k) {
+      const Item w = get_item<BT>(p, sch, k);
+      for (int t = w.t0; t < w.t1; ++t, sr.next(), ++gp) {
+        mbar_wait(&sm.sfree[sr.i], sr.ph ^ 1);
+        const float* ws = p.w_scales + static_cast<int64_t>(t) * p.N + w.n0;
+        const float* as = p.a_scales + static_cast<int64_t>(t) * p.M;
 #pragma unroll
-          for (int j = lane; j < kTileN; j += 32) cp_async_4(&sm.ssw[sr][j], ws + j);
+        for (int j = lane; j < kTileN; j += 32) cp_async_4(&sm.ssw[sr.i][j], ws + j);
 #pragma unroll
-          for (int j = lane; j < BT; j += 32)
-            // rows past M: any finite scale works, their partials are exactly zero (TMA
-            // zero-fills out-of-range activation rows) and they are never stored
-            cp_async_4(&sm.ssa[sr][j], as + min(w.m0 + j, p.M - 1));
-          cp_async_mbar_arrive(&sm.sready[sr]);
-        }
+        for (int j = lane; j < BT; j += 32)
+          // rows past M: any finite scale works, their partials are exactly zero (TMA
+          // zero-fills out-of-range activation rows) and they are never stored
+          cp_async_4(&sm.ssa[sr.i][j], as + min(w.m0 + j, p.M - 1));
+        cp_async_mbar_arrive(&sm.sready[sr.i]);
         const int nh = t < G4 ? 1 : 2;      // the INT8 outlier group arrives in two halves
-        for (int h = 0; h < nh; ++h, ++it) {
-          const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-          wait(&sm.empty[s], ph ^ 1);
+        for (int h = 0; h < nh; ++h, st.next()) {
+          mbar_wait(&sm.empty[st.i], st.ph ^ 1);
           if (lane == 0) {
-            if constexpr ((kMode & 4) != 0) {   // probe: no TMA traffic
-              mbar_arrive(&sm.full[s]);
+            if (h == 0) TRACE(0, gp);
+            if constexpr ((kMode & 32) != 0) {
+              mbar_arrive(&sm.full[st.i]);
             } else {
-              mbar_arrive_expect_tx(&sm.full[s], kTileN * 64 + BT * 64);
-              if (t < G4) {
-                tma_load_2d(sm.stage_w[s], &tm_wq4, &sm.full[s], t * 64, w.n0);
-                tma_load_2d(sm.stage_a[s], &tm_aq4, &sm.full[s], t * 64, w.m0);
-              } else {
-                tma_load_2d(sm.stage_w[s], &tm_wq8, &sm.full[s], h * 64, w.n0);
-                tma_load_2d(sm.stage_a[s], &tm_aq8, &sm.full[s], h * 64, w.m0);
-              }
+              mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
+              if (t < G4) tma_load_2d(sm.stage_w[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0);
+              else tma_load_2d(sm.stage_w[st.i], &tm_wq8, &sm.full[st.i], h * 64, w.n0);
             }
           }
           __syncwarp();
@@ -269,310 +365,298 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (single thread) =====================
+    // Every instruction this thread executes between dispatches idles the tensor pipe for as
+    // long (measured, tools/mma_rate.cu: tcgen05.mma issue returns only as the previous dispatch
+    // drains), so the loop is one barrier probe, 4 dispatches and one commit per group.
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_i8(kTileN, BT);
-      uint32_t g_it = 0;
-      for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
-        const Item w = make_item<BT>(p, item);
-        for (int t = w.t0; t < w.t1; ++t, ++g_it) {
-          const uint32_t u = g_it % R, uph = (g_it / R) & 1;
-          wait(&sm.tempty[u], uph);            // epilogue drained (and re-armed) this accumulator
-          wait(&sm.ufull[u], uph);             // operands unpacked
-          tc_fence_after();
-          if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256) p.trace[g_it] = clock64();
-          const uint32_t d = tmem + u * BT;
-          const uint32_t a_base = smem_u32(sm.ubuf_w[u]);
-          const uint32_t b_base = smem_u32(sm.ubuf_a[u]);
+      int total = 0;
+      for (int k = 0; k < n_items; ++k) {
+        const Item w = get_item<BT>(p, sch, k);
+        total += w.t1 - w.t0;
+      }
+      const uint64_t da0 = umma_desc_sw128(smem_u32(sm.ubuf_w[0]));
+      const uint64_t db0 = umma_desc_sw128(smem_u32(sm.ubuf_a[0]));
+      Ring<RS> u;
+      Ring<RT> b;
+      for (int gm = 0; gm < total; ++gm) {
+        wait_hot(&sm.go[u.i], u.ph);
+        tc_fence_after();
+        TRACE(3, gm);
+        const uint32_t d = tmem + b.i * BT;
+        // descriptor start address field counts 16-byte units: slot u, K step kk (32 bytes)
+        const uint64_t da = da0 + u.i * (kTileN * 128 / 16);
+        const uint64_t db = db0 + u.i * (BT * 128 / 16);
+        const uint32_t acc0 = ((kMode & 4) != 0 && (b.i & 1u) == 0) ? 1u : 0u;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            // even buffers hold the magic 1.5*2^23 (re-armed by the epilogue): always accumulate;
-            // odd buffers start from zero and the epilogue converts with one LOP3
-            umma_i8(d, umma_desc_sw128(a_base + 32 * k), umma_desc_sw128(b_base + 32 * k), idesc,
-                    (k > 0 || (kPrefillEven && (u & 1u) == 0)) ? 1u : 0u);
-          umma_commit(&sm.mdone[u]);
-          if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256) p.trace[1536 + g_it] = clock64();
-        }
+        for (int kk = 0; kk < 4; ++kk)
+          // even buffers hold the magic 1.5*2^23 (re-armed by the epilogue): always accumulate;
+          // odd buffers start from zero and the epilogue converts with one LOP3
+          umma_i8(d, da + 2 * kk, db + 2 * kk, idesc, kk > 0 ? 1u : acc0);
+        umma_commit(&sm.mdone[u.i]);
+        if constexpr ((kMode & 256) != 0)   // probe: MMA latency (issue -> completion)
+          mbar_wait_spin(&sm.mdone[u.i], u.ph);
+        u.next();
+        b.next();
       }
     }
   } else if (warp < kEpiWarp0) {
-    // ===================== unpack warps: packed INT4 -> int8 (16*q), SW128 =====================
-    // threads 0-127: the 128 weight rows + activation rows [0, min(BT,128));
-    // threads 128-191: activation rows [128, BT) (BT = 256 only).
-    const int ut = threadIdx.x - kUnpackWarp0 * 32;  // 0..191
-    const uint32_t r0 = static_cast<uint32_t>(ut & 127) >> 2, c = static_cast<uint32_t>(ut) & 3u;
-    uint32_t it = 0, g_it = 0;
-    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
-      const Item w = make_item<BT>(p, item);
-      for (int t = w.t0; t < w.t1; ++t, ++g_it) {
-        const uint32_t u = g_it % R, uph = (g_it / R) & 1;
-        wait(&sm.mdone[u], uph ^ 1);   // MMAs of group g - R finished with this buffer
+    // ===================== unpack warps: packed INT4 weights -> int8 (16*q), SW128 ============
+    // 64 threads: thread ut owns packed chunk (ut & 3) of rows (ut >> 2) + 16k, k < 8.
+    const int ut = threadIdx.x - kUnpackWarp0 * 32;
+    const uint32_t r0 = static_cast<uint32_t>(ut) >> 2, c = static_cast<uint32_t>(ut) & 3u;
+    Ring<KS> st;
+    Ring<RS> u;
+    int gu = 0;
+    for (int k = 0; k < n_items; ++k) {
+      const Item w = get_item<BT>(p, sch, k);
+      for (int t = w.t0; t < w.t1; ++t, u.next(), ++gu) {
+        mbar_wait(&sm.mdone[u.i], u.ph ^ 1);  // MMAs of group g - RS finished with this slot
+        if (ut == 0) {
+          // the activation tile of this group (x8, TMA, SWIZZLE_128B straight into the slot)
+          if constexpr ((kMode & 16) != 0) {
+            mbar_arrive(&sm.go[u.i]);
+          } else {
+            mbar_arrive_expect_tx(&sm.go[u.i], BT * 128);
+            tma_load_2d(sm.ubuf_a[u.i], &tm_ax8, &sm.go[u.i], t * 128, w.m0);
+          }
+        }
         const bool int4 = t < G4;
         const int nh = int4 ? 1 : 2;
-        for (int h = 0; h < nh; ++h, ++it) {
-          const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-          wait(&sm.full[s], ph);
-          if constexpr ((kMode & 2) == 0) {
-            if (ut < 128) {
-              unpack_rows<4, 32>(sm.stage_w[s], sm.ubuf_w[u], r0, c, int4, h);
-              unpack_rows<(BT < 128 ? BT : 128) / 32, 32>(sm.stage_a[s], sm.ubuf_a[u], r0, c,
-                                                          int4, h);
-            } else if constexpr (BT > 128) {
-              unpack_rows<(BT - 128) / 16, 16>(sm.stage_a[s] + 128 * 64, sm.ubuf_a[u] + 128 * 128,
-                                               r0 & 15u, c, int4, h);
-            }
-          }
+        for (int h = 0; h < nh; ++h, st.next()) {
+          mbar_wait(&sm.full[st.i], st.ph);
+          if constexpr ((kMode & 64) == 0)
+            unpack_rows<8, 16>(sm.stage_w[st.i], sm.ubuf_w[u.i], r0, c, int4, h);
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.empty[s]);
+          if (lane == 0) mbar_arrive(&sm.empty[st.i]);
         }
-        fence_proxy_async_smem();
+        if constexpr ((kMode & 512) == 0) fence_proxy_async_smem();
         __syncwarp();
-        if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256 && ut == 0)
-          p.trace[256 + g_it] = clock64();
-        if (lane == 0) mbar_arrive(&sm.ufull[u]);
+        if (ut == 0) TRACE(4, gu);
+        if (lane == 0) mbar_arrive(&sm.go[u.i]);
       }
     }
   } else {
     // ===================== epilogue warps =====================
-    // TMEM is read with the 16x256b shape: thread (tr = lane/4, tc = lane%4) holds, for each
-    // 16-lane block blk of its warp's lane quarter and each 8-column chunk j, the MMA-fragment
-    // values (row tr, cols 2tc, 2tc+1) and (row tr+8, same cols).  Column pairs share one s_a
-    // pair (one 8-byte shared load per chunk for the whole warp), and at the tile end the fp16
-    // fragments go through stmatrix.trans into [token][channel] rows for 16-byte global stores.
+    // TMEM is read with the 32x32b shape: thread = TMEM lane = output channel n (its weight
+    // scale is one scalar per group), consecutive registers = consecutive tokens of this warp's
+    // column third.  Per column: dequantize T = float(1.5*2^23 + R) with one FFMA,
+    // g = T*sw' - 1.5*2^23*sw' = sw'*R, and accumulate acc += s_a*g with one more (FFMA2 on
+    // column pairs; s_a of 4 columns per broadcast 16-byte shared load).  The FP32 pipe is the
+    // binding resource of the whole kernel (2 FMAs per output per group).
     setmaxnreg_inc<kRegsHigh>();
-    constexpr int COLS = BT / 2;         // token columns per warp (column half of the tile)
-    constexpr int NJ = COLS / 8;         // 8-column chunks
-    constexpr int JL = NJ >= 4 ? 4 : NJ; // chunks per TMEM load (16x256b.xJL)
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int half = e >> 2;
-    const int tr = lane >> 2, tc = lane & 3;
-    const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * COLS;
+    const int third = e >> 2;
+    constexpr int kBase = NC / 3, kRem = NC % 3;
+    constexpr int NCOL = NJ * 8;         // columns of the widest third
+    const int ncol = 8 * (kBase + (third < kRem ? 1 : 0));             // this warp (uniform)
+    const int col0 = 8 * (third * kBase + (third < kRem ? third : kRem));
+    const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + col0;
     const uint32_t magic = kMagicBits;
-    // Resident copies of the magic as tcgen05.st sources (see the STTM re-arm below).
-    uint32_t mg[4];
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(mg[0]), "=r"(mg[1]), "=r"(mg[2]), "=r"(mg[3])
-                 : "r"(smem_u32(sm.magic4)));
-    // Even accumulator buffers carry the magic bias (tcgen05.st, TMEM write port); odd ones are
-    // converted with a LOP3 (ALU) -- see DESIGN.md "Epilogue arithmetic".
-    if constexpr (kPrefillEven) {
+    const bool a_issuer = e == 0 && lane == 0;
+    const int n_local = q * 32 + lane;   // output channel within the tile
+    auto rearm = [&](uint32_t taddr) {   // this warp's columns of one buffer := 1.5*2^23
 #pragma unroll
-      for (int b = 0; b < R; b += 2)
-#pragma unroll
-        for (int c = 0; c < COLS; c += 4) tmem_st4(tq + b * BT + c, mg);
+      for (int j = 0; j < NCOL; j += 16) {
+        if (j + 16 <= ncol) tmem_st16_const(taddr + j, magic);
+        else if (j + 8 <= ncol) tmem_st8_const(taddr + j, magic);
+      }
       tmem_st_wait();
+    };
+    if constexpr ((kMode & 4) != 0) {
+#pragma unroll
+      for (int b = 0; b < RT; b += 2) rearm(tq + b * BT);
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0)
-      for (int b = 0; b < R; ++b) mbar_arrive(&sm.tempty[b]);
+    if (lane == 0)   // the first RT groups find their TMEM buffers free
+      for (int b = 0; b < RT; ++b) mbar_arrive(&sm.go[b % RS]);
     uint8_t* stg = sm.ostg[e];           // per-warp staging for the transposed output
-    uint32_t g_it = 0;
-    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x) {
-      const Item w = make_item<BT>(p, item);
-      const int n0 = w.n0, m0 = w.m0;
-      const int mc0 = m0 + half * COLS;
-      // acc[blk][j][h]: rows 32q + 16 blk + tr + 8 h, columns (token) 8j + 2tc + {0, 1}
-      float2 acc[2][NJ][2];
+    Ring<RS> u;
+    Ring<RT> b;
+    Ring<kSRing> sr;
+    int ge = 0;
+    for (int k = 0; k < n_items; ++k) {
+      const Item w = get_item<BT>(p, sch, k);
+      const int n0 = w.n0;
+      const int mc0 = w.m0 + col0;       // first token of this warp's columns
+      float acc[NCOL];
 #pragma unroll
-      for (int bk = 0; bk < 2; ++bk)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          acc[bk][j][0] = make_float2(0.0f, 0.0f);
-          acc[bk][j][1] = make_float2(0.0f, 0.0f);
-        }
-      for (int t = w.t0; t < w.t1; ++t, ++g_it) {
-        const uint32_t b = g_it % R, bph = (g_it / R) & 1;
-        const uint32_t sr = g_it % kSRing, sph = (g_it / kSRing) & 1;
+      for (int j = 0; j < NCOL; ++j) acc[j] = 0.0f;
+      for (int t = w.t0; t < w.t1; ++t, u.next(), b.next(), sr.next(), ++ge) {
         const bool int4 = t < G4;
-        wait(&sm.sready[sr], sph);
-        // Dequantize T = float(1.5*2^23 + R) with ONE fma: g = T*sw' - 1.5*2^23*sw' = sw'*R,
-        // rounded once.  sw' = sw (x1/256 for INT4 groups, exact) with its 2 lowest mantissa
-        // bits cleared so that 1.5*2^23*sw' is exact; see DESIGN.md "Epilogue arithmetic".
-        float2 sw2[2][2], nc2[2][2];
-#pragma unroll
-        for (int bk = 0; bk < 2; ++bk)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float sw = sm.ssw[sr][q * 32 + 16 * bk + 8 * h + tr];
-            if (int4) sw *= (1.0f / 256.0f);
-            const float swh = __uint_as_float(__float_as_uint(sw) & 0xFFFFFFFCu);
-            sw2[bk][h] = make_float2(swh, swh);
-            nc2[bk][h] = make_float2(-kMagic * swh, -kMagic * swh);
-          }
-        const float2* sa2 = reinterpret_cast<const float2*>(&sm.ssa[sr][half * COLS + 2 * tc]);
-        wait(&sm.mdone[b], bph);
+        mbar_wait(&sm.sready[sr.i], sr.ph);
+        if (a_issuer) TRACE(5, ge);
+        // sw' = sw (x1/16 for INT4 groups, exact) with its 2 lowest mantissa bits cleared so
+        // that 1.5*2^23*sw' is exact; see DESIGN.md "Epilogue arithmetic".
+        float sw = sm.ssw[sr.i][n_local];
+        if (int4) sw *= (1.0f / 16.0f);
+        const float swh = __uint_as_float(__float_as_uint(sw) & 0xFFFFFFFCu);
+        const float2 sw2 = make_float2(swh, swh);
+        const float2 nc2 = make_float2(-kMagic * swh, -kMagic * swh);
+        const float* sa = &sm.ssa[sr.i][col0];
+        wait_hot(&sm.mdone[u.i], u.ph);
+        if (a_issuer) TRACE(6, ge);
         tc_fence_after();
-        if (p.trace != nullptr && blockIdx.x == 0 && g_it < 256 && e == 0 && lane == 0)
-          p.trace[512 + g_it] = clock64();
-        const uint32_t taddr = tq + b * BT;
+        const uint32_t taddr = tq + b.i * BT;
+        const uint32_t go_next = u.i + RT >= RS ? u.i + RT - RS : u.i + RT;   // slot of g + RT
+        const bool pre = (kMode & 4) != 0 && (b.i & 1u) == 0;
         auto drain = [&](auto pre_tag) {
           constexpr bool kPre = decltype(pre_tag)::value;
-#pragma unroll
-          for (int jl = 0; jl < NJ / JL; ++jl) {
-            uint32_t r[2][4 * JL];
-            if constexpr ((kMode & 8) == 0) {
-              tmem_ld_16x256b<JL>(taddr + jl * 8 * JL, r[0]);
-              tmem_ld_16x256b<JL>(taddr + (16u << 16) + jl * 8 * JL, r[1]);
-              tmem_ld_wait();
+          // 16-column batches, software-pipelined one batch ahead: the load of batch i+1 is in
+          // flight while batch i is computed (the LDTM destination registers are scoreboarded;
+          // tcgen05.wait::ld, which waits for ALL loads, is only issued before the buffer is
+          // released, once the last batch has been requested)
+          constexpr int NB = (NCOL + 15) / 16;
+          uint32_t r[2][16];
+          auto load = [&](int bi, uint32_t* dst) {
+            const int j = bi * 16;
+            if constexpr ((kMode & 2) == 0) {
+              if (j + 16 <= ncol) tmem_ld16p(taddr + j, dst);
+              else if (j + 8 <= ncol) tmem_ld8(taddr + j, dst);
             } else {
 #pragma unroll
-              for (int k = 0; k < 4 * JL; ++k) r[0][k] = r[1][k] = 0;
+              for (int v = 0; v < 16; ++v) dst[v] = taddr + v;
             }
-            if (jl == NJ / JL - 1) {
-              if constexpr (kPre && (kMode & 8) == 0) {   // re-arm the whole region
+          };
+          load(0, r[0]);
 #pragma unroll
-                for (int c = 0; c < COLS; c += 4) tmem_st4(taddr + c, mg);
-                tmem_st_wait();
-              }
+          for (int bi = 0; bi < NB; ++bi) {
+            if (bi + 1 < NB) {
+              load(bi + 1, r[(bi + 1) & 1]);
+            } else {                                  // all loads issued: release the buffer
+              tmem_ld_wait();
+              if constexpr (kPre) rearm(taddr);
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&sm.tempty[b]);
-            }
-            if constexpr (!kPre) {
-#pragma unroll
-              for (int k = 0; k < 4 * JL; ++k) {
-                r[0][k] = __float_as_uint(biased(r[0][k], magic));
-                r[1][k] = __float_as_uint(biased(r[1][k], magic));
-              }
+              if (a_issuer) TRACE(7, ge);
+              if (lane == 0) mbar_arrive(&sm.go[go_next]);   // buffer b free for g + RT
             }
 #pragma unroll
-            for (int jj = 0; jj < JL; ++jj) {
-              const int j = jl * JL + jj;
-              if constexpr (kDebug) {
+            for (int jj = 0; jj < 16; jj += 4) {
+              const int j = bi * 16 + jj;
+              if (j < NCOL && j < ncol) {
+                uint32_t* rv = r[bi & 1] + jj;
+                if constexpr (!kPre) {
 #pragma unroll
-                for (int bk = 0; bk < 2; ++bk)
+                  for (int v = 0; v < 4; ++v) rv[v] = __float_as_uint(biased(rv[v], magic));
+                }
+                if constexpr (kDebug) {
 #pragma unroll
                   for (int v = 0; v < 4; ++v) {
-                    const int m = mc0 + 8 * j + 2 * tc + (v & 1);
-                    const int n = n0 + q * 32 + 16 * bk + tr + 8 * (v >> 1);
-                    const int raw = static_cast<int>(r[bk][4 * jj + v] - kMagicBits);
+                    const int m = mc0 + j + v;
+                    const int raw = static_cast<int>(rv[v] - kMagicBits);
                     if (m < p.M)
-                      p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = int4 ? (raw >> 8) : raw;
+                      p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n0 + n_local] =
+                          int4 ? (raw >> 4) : raw;
                   }
-              }
-              if constexpr ((kMode & 1) == 0) {
-                const float2 sa = sa2[4 * j];   // s_a of columns 8j + 2tc, +1
-#pragma unroll
-                for (int bk = 0; bk < 2; ++bk)
-#pragma unroll
-                  for (int h = 0; h < 2; ++h) {
-                    const float2 g = __ffma2_rn(
-                        make_float2(__uint_as_float(r[bk][4 * jj + 2 * h]),
-                                    __uint_as_float(r[bk][4 * jj + 2 * h + 1])),
-                        sw2[bk][h], nc2[bk][h]);
-                    acc[bk][j][h] = __ffma2_rn(sa, g, acc[bk][j][h]);
-                  }
+                }
+                const float4 s4 = *reinterpret_cast<const float4*>(sa + j);
+                if constexpr ((kMode & 1) != 0) {
+                  acc[j] += __uint_as_float(rv[0] ^ rv[3]);
+                  continue;
+                }
+                const float2 g0 = __ffma2_rn(
+                    make_float2(__uint_as_float(rv[0]), __uint_as_float(rv[1])), sw2, nc2);
+                const float2 g1 = __ffma2_rn(
+                    make_float2(__uint_as_float(rv[2]), __uint_as_float(rv[3])), sw2, nc2);
+                const float2 a0 = __ffma2_rn(make_float2(s4.x, s4.y), g0,
+                                             make_float2(acc[j], acc[j + 1]));
+                const float2 a1 = __ffma2_rn(make_float2(s4.z, s4.w), g1,
+                                             make_float2(acc[j + 2], acc[j + 3]));
+                acc[j] = a0.x;
+                acc[j + 1] = a0.y;
+                acc[j + 2] = a1.x;
+                acc[j + 3] = a1.y;
               }
             }
           }
         };
-        if (kPrefillEven && (b & 1u) == 0) drain(std::true_type{});
+        if (pre) drain(std::true_type{});
         else drain(std::false_type{});
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.sfree[sr]);
+        if (lane == 0) mbar_arrive(&sm.sfree[sr.i]);
       }
-      if (p.trace != nullptr && threadIdx.x == kEpiWarp0 * 32 && blockIdx.x < 256)
-        p.trace[1024 + blockIdx.x] = globaltimer();
-      if constexpr ((kMode & 32) != 0) continue;
 
-      // ---- split-K: publish this split's fp32 partial in the fragment layout; the last
-      //      split to arrive sums all partials in split order (deterministic) into acc ----
-      if (p.ksplit > 1) {
-        float* slot = p.partials + (static_cast<int64_t>(w.tile) * p.ksplit + w.split) * kTileN * BT;
-        auto frag_ptr = [&](float* base, int bk, int j, int h) {
-          return reinterpret_cast<float2*>(
-              base + static_cast<int64_t>(q * 32 + 16 * bk + 8 * h + tr) * BT + half * COLS +
-              8 * j + 2 * tc);
+      // ---- split tile: every segment but the tile's last publishes its fp32 partial; the CTA
+      //      holding the last segment adds the others (in CTA order, deterministic) ----
+      if (w.t1 < p.G || w.t0 > 0) {
+        // thread-linear float4 fragments: warp e, column quad i, lane -> one 512-byte row
+        auto frag = [&](float* slot, int i) {
+          return reinterpret_cast<float4*>(slot) + (e * (NCOL / 4) + i) * 32 + lane;
         };
+        if (w.t1 < p.G) {                    // publisher (this CTA's first item)
+          float* slot = p.partials + static_cast<int64_t>(blockIdx.x) * C::kSlotFloats;
 #pragma unroll
-        for (int bk = 0; bk < 2; ++bk)
+          for (int i = 0; i < NCOL / 4; ++i)
+            if (4 * i < ncol)
+              __stcg(frag(slot, i), make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2],
+                                                acc[4 * i + 3]));
+          __threadfence();
+          named_bar_sync(1, kEpiThreads);
+          if (e == 0 && lane == 0)
+            red_release_add(p.counters + cta_of(p, static_cast<int64_t>(w.tile + 1) * p.G - 1), 1);
+          continue;
+        }
+        // reducer (this CTA's last item): the other segments belong to CTAs first..blockIdx-1
+        const int first = cta_of(p, static_cast<int64_t>(w.tile) * p.G);
+        const int nseg = static_cast<int>(blockIdx.x) - first;
+        if (e == 0 && lane == 0) {
+          while (ld_acquire(p.counters + blockIdx.x) < nseg) __nanosleep(64);
+          p.counters[blockIdx.x] = 0;        // self-cleaning for the next launch
+        }
+        named_bar_sync(1, kEpiThreads);
+        for (int i0 = first; i0 < static_cast<int>(blockIdx.x); ++i0) {
+          float* slot = p.partials + static_cast<int64_t>(i0) * C::kSlotFloats;
 #pragma unroll
-          for (int j = 0; j < NJ; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) *frag_ptr(slot, bk, j, h) = acc[bk][j][h];
-        __threadfence();
-        named_bar_sync(1, kNumEpiWarps * 32);   // all epilogue threads of this CTA have written
-        __shared__ int arrived;
-        if (threadIdx.x == kEpiWarp0 * 32) arrived = atomicAdd(p.counters + w.tile, 1);
-        named_bar_sync(1, kNumEpiWarps * 32);
-        const bool last = arrived == p.ksplit - 1;
-        named_bar_sync(1, kNumEpiWarps * 32);   // everyone has read `arrived`
-        if (!last) continue;
-        __threadfence();
-        if (threadIdx.x == kEpiWarp0 * 32) p.counters[w.tile] = 0;   // self-cleaning
-        float* slot0 = p.partials + static_cast<int64_t>(w.tile) * p.ksplit * kTileN * BT;
-#pragma unroll
-        for (int bk = 0; bk < 2; ++bk)
-#pragma unroll
-          for (int j = 0; j < NJ; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) acc[bk][j][h] = make_float2(0.0f, 0.0f);
-        for (int sp = 0; sp < p.ksplit; ++sp) {
-          float* sl = slot0 + static_cast<int64_t>(sp) * kTileN * BT;
-#pragma unroll
-          for (int bk = 0; bk < 2; ++bk)
-#pragma unroll
-            for (int j = 0; j < NJ; ++j)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const float2 o = __ldcg(frag_ptr(sl, bk, j, h));
-                acc[bk][j][h].x += o.x;
-                acc[bk][j][h].y += o.y;
-              }
+          for (int i = 0; i < NCOL / 4; ++i)
+            if (4 * i < ncol) {
+              const float4 o = __ldcg(frag(slot, i));
+              acc[4 * i] += o.x;
+              acc[4 * i + 1] += o.y;
+              acc[4 * i + 2] += o.z;
+              acc[4 * i + 3] += o.w;
+            }
         }
       }
+      if constexpr ((kMode & 8) != 0) {
+        if (acc[0] == 1.2345f) p.debug[0] = 1;   // keep acc alive
+        continue;
+      }
 
-      // ---- tile output: stmatrix.trans turns the 8x8 (channel, token) fragments into
-      //      [token][channel] rows of the per-warp staging; each lane then moves 16 bytes
-      //      (8 channels of one token) to C.  fp32 output transposes the high and low 16-bit
-      //      halves separately and re-interleaves them. ----
-      // staging rows: 8 tokens x (32 channels) with an 80-byte pitch (bank-conflict free)
-      const uint32_t st_addr = smem_u32(stg) + (lane & 7) * 80 + (lane >> 3) * 16;
-      const int om = lane >> 2, op = lane & 3;                 // readback: token row, 8-ch piece
-      const int ncol = n0 + q * 32 + 8 * op;
-      for (int j = 0; j < NJ; ++j) {
-        const int m = mc0 + 8 * j + om;
-        if (!p.c_f32) {
-          uint32_t h4[4];
+      // ---- tile output: 8 tokens at a time, this lane's channel is written into a per-warp
+      //      [8 tokens][32 channels] staging (conflict-free rows), then each lane stores 16
+      //      contiguous bytes of one token row of C ----
+      const int om = lane >> 2, op = lane & 3;           // readback: token row, channel piece
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const __half2 hh = __floats2half2_rn(acc[i >> 1][j][i & 1].x, acc[i >> 1][j][i & 1].y);
-            h4[i] = *reinterpret_cast<const uint32_t*>(&hh);
-          }
-          stmatrix_x4_trans(st_addr, h4);
+      for (int j = 0; j < NCOL; j += 8) {
+        if (j >= ncol) continue;
+        const int m = mc0 + j + om;
+        if (!p.c_f32) {
+          __half* s16 = reinterpret_cast<__half*>(stg);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) s16[v * 32 + lane] = __float2half_rn(acc[j + v]);
           __syncwarp();
-          const uint4 v = *reinterpret_cast<const uint4*>(stg + om * 80 + op * 16);
+          const uint4 val = *reinterpret_cast<const uint4*>(s16 + om * 32 + op * 8);
           __syncwarp();
           if (m < p.M)
             *reinterpret_cast<uint4*>(static_cast<__half*>(p.c) + static_cast<int64_t>(m) * p.ldc +
-                                      ncol) = v;
+                                      n0 + q * 32 + op * 8) = val;
         } else {
-          uint32_t hi4[4], lo4[4];
+          float* s32 = reinterpret_cast<float*>(stg);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t a = __float_as_uint(acc[i >> 1][j][i & 1].x);
-            const uint32_t c = __float_as_uint(acc[i >> 1][j][i & 1].y);
-            hi4[i] = __byte_perm(a, c, 0x7632);   // (hi(a), hi(c))
-            lo4[i] = __byte_perm(a, c, 0x5410);   // (lo(a), lo(c))
-          }
-          stmatrix_x4_trans(st_addr, hi4);
-          stmatrix_x4_trans(st_addr + 640, lo4);
+          for (int v = 0; v < 8; ++v) s32[v * 32 + lane] = acc[j + v];
           __syncwarp();
-          const uint4 hv = *reinterpret_cast<const uint4*>(stg + om * 80 + op * 16);
-          const uint4 lv = *reinterpret_cast<const uint4*>(stg + 640 + om * 80 + op * 16);
+          const float4 v0 = *reinterpret_cast<const float4*>(s32 + om * 32 + op * 8);
+          const float4 v1 = *reinterpret_cast<const float4*>(s32 + om * 32 + op * 8 + 4);
           __syncwarp();
           if (m < p.M) {
             float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.c) +
-                                                    static_cast<int64_t>(m) * p.ldc + ncol);
-            dst[0] = make_float4(__uint_as_float(__byte_perm(lv.x, hv.x, 0x5410)),
-                                 __uint_as_float(__byte_perm(lv.x, hv.x, 0x7632)),
-                                 __uint_as_float(__byte_perm(lv.y, hv.y, 0x5410)),
-                                 __uint_as_float(__byte_perm(lv.y, hv.y, 0x7632)));
-            dst[1] = make_float4(__uint_as_float(__byte_perm(lv.z, hv.z, 0x5410)),
-                                 __uint_as_float(__byte_perm(lv.z, hv.z, 0x7632)),
-                                 __uint_as_float(__byte_perm(lv.w, hv.w, 0x5410)),
-                                 __uint_as_float(__byte_perm(lv.w, hv.w, 0x7632)));
+                                                    static_cast<int64_t>(m) * p.ldc + n0 +
+                                                    q * 32 + op * 8);
+            dst[0] = v0;
+            dst[1] = v1;
           }
         }
       }
@@ -581,8 +665,6 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 
   tc_fence_before();
   __syncthreads();
-  if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < 256)
-    p.trace[1280 + blockIdx.x] = globaltimer();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -612,37 +694,49 @@ static PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
-// 2D uint8 tensor [rows][cols] (row stride = cols bytes), box [box_rows][64 bytes].
+// 2D uint8 tensor [rows][cols] (row stride = cols bytes), box [box_rows][box_cols bytes].
 static bool make_map_u8(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
-                        uint32_t box_rows) {
+                        uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
 template <int BT>
+static size_t slot_bytes() {
+  return Cfg<BT>::kSlotFloats * sizeof(float);
+}
+static size_t slot_bytes_for(int bt) {
+  switch (bt) {
+    case 256: return slot_bytes<256>();
+    case 128: return slot_bytes<128>();
+    case 64: return slot_bytes<64>();
+    default: return slot_bytes<32>();
+  }
+}
+
+template <int BT>
 static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* workspace,
-                             cudaStream_t stream, int num_sms, int* launches) {
+                             cudaStream_t stream, int* launches) {
   const int M = static_cast<int>(a.M), N = static_cast<int>(a.N), K = static_cast<int>(a.K);
   const int k_o = a.k_outlier;
   const uint64_t kp = static_cast<uint64_t>(K - k_o) / 2;
-  CUtensorMap m_wq4, m_aq4, m_wq8, m_aq8;
-  // A map is always encoded (a valid descriptor is required as a kernel parameter); the unused
-  // INT4 or INT8 maps alias the other operand and are never read.
+  CUtensorMap m_wq4, m_wq8, m_ax8;
+  // A map is always encoded (a valid descriptor is required as a kernel parameter); an unused
+  // INT4 or INT8 weight map aliases the other one and is never read.
   const void* w4 = kp ? static_cast<const void*>(a.w_q4) : static_cast<const void*>(a.w_q8);
-  const void* a4 = kp ? static_cast<const void*>(a.a_q4) : static_cast<const void*>(a.a_q8);
   const void* w8 = k_o ? static_cast<const void*>(a.w_q8) : static_cast<const void*>(a.w_q4);
-  const void* a8 = k_o ? static_cast<const void*>(a.a_q8) : static_cast<const void*>(a.a_q4);
   const uint64_t c4 = kp ? kp : 128, c8 = k_o ? 128 : kp;
-  if (!make_map_u8(&m_wq4, w4, c4, N, kTileN) || !make_map_u8(&m_aq4, a4, c4, M, BT) ||
-      !make_map_u8(&m_wq8, w8, c8, N, kTileN) || !make_map_u8(&m_aq8, a8, c8, M, BT))
+  if (!make_map_u8(&m_wq4, w4, c4, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map_u8(&m_wq8, w8, c8, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map_u8(&m_ax8, a.a_x8, K, M, 128, BT, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
 
   GemmParams p;
@@ -655,105 +749,125 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
   p.N = N;
   p.G = K / 128;
   p.G4 = (K - k_o) / 128;
-  p.k_o = k_o;
   p.c_f32 = a.c_f32;
   p.m_tiles = (M + BT - 1) / BT;
   p.num_tiles = p.m_tiles * (N / kTileN);
-  p.ksplit = plan.ksplit;
-  p.num_items = p.num_tiles * p.ksplit;
+  p.dp_waves = plan.dp_waves;
+  p.sk_base = static_cast<int64_t>(plan.dp_waves) * plan.grid * p.G;
+  p.sk_units = plan.sk_units;
   p.counters = nullptr;
   p.partials = nullptr;
-  if (plan.ksplit > 1) {
+  p.trace = nullptr;
+  if (plan.workspace_bytes > 0) {
     p.counters = static_cast<int*>(workspace);
     p.partials = reinterpret_cast<float*>(static_cast<char*>(workspace) + plan.counter_bytes);
-    cudaError_t e = cudaMemsetAsync(p.counters, 0, plan.counter_bytes, stream);
-    if (e != cudaSuccess) return e;
-    ++*launches;
   }
 
   const size_t smem = sizeof(GemmSmem<BT>) + 1024;
   auto kern = p.debug ? w4a4_gemm_kernel<BT, true> : w4a4_gemm_kernel<BT, false>;
-  if constexpr (BT == 256) {
+  if constexpr (BT == 256 || BT == 128) {
     static const char* mode_env = getenv("ATOM_GEMM_PROBE_MODE");   // development probe only
-    const int mode = mode_env ? atoi(mode_env) : 0;
-    if (mode == 1) kern = w4a4_gemm_kernel<BT, false, 1>;
-    if (mode == 2) kern = w4a4_gemm_kernel<BT, false, 2>;
-    if (mode == 3) kern = w4a4_gemm_kernel<BT, false, 3>;
-    if (mode == 4) kern = w4a4_gemm_kernel<BT, false, 4>;
-    if (mode == 7) kern = w4a4_gemm_kernel<BT, false, 7>;
-    if (mode == 15) kern = w4a4_gemm_kernel<BT, false, 15>;
-    if (mode == 16) kern = w4a4_gemm_kernel<BT, false, 16>;
-    if (mode == 23) kern = w4a4_gemm_kernel<BT, false, 23>;
-    if (mode == 32) kern = w4a4_gemm_kernel<BT, false, 32>;
-    if (mode == 64) kern = w4a4_gemm_kernel<BT, false, 64>;
-    if (mode == 33) kern = w4a4_gemm_kernel<BT, false, 33>;
-    if (mode == 34) kern = w4a4_gemm_kernel<BT, false, 34>;
-    if (mode == 39) kern = w4a4_gemm_kernel<BT, false, 39>;
-
-
+    switch (mode_env ? atoi(mode_env) : 0) {
+      case 1: kern = w4a4_gemm_kernel<BT, false, 1>; break;
+      case 2: kern = w4a4_gemm_kernel<BT, false, 2>; break;
+      case 3: kern = w4a4_gemm_kernel<BT, false, 3>; break;
+      case 4: kern = w4a4_gemm_kernel<BT, false, 4>; break;
+      case 8: kern = w4a4_gemm_kernel<BT, false, 8>; break;
+      case 11: kern = w4a4_gemm_kernel<BT, false, 11>; break;
+      case 19: kern = w4a4_gemm_kernel<BT, false, 19>; break;
+      case 35: kern = w4a4_gemm_kernel<BT, false, 35>; break;
+      case 51: kern = w4a4_gemm_kernel<BT, false, 51>; break;
+      case 67: kern = w4a4_gemm_kernel<BT, false, 67>; break;
+      case 115: kern = w4a4_gemm_kernel<BT, false, 115>; break;
+      case 119: kern = w4a4_gemm_kernel<BT, false, 119>; break;
+      case 117: kern = w4a4_gemm_kernel<BT, false, 117>; break;
+      case 128: kern = w4a4_gemm_kernel<BT, false, 128>; break;
+      case 131: kern = w4a4_gemm_kernel<BT, false, 131>; break;
+      case 243: kern = w4a4_gemm_kernel<BT, false, 243>; break;
+      case 371: kern = w4a4_gemm_kernel<BT, false, 371>; break;
+      case 627: kern = w4a4_gemm_kernel<BT, false, 627>; break;
+      case 515: kern = w4a4_gemm_kernel<BT, false, 515>; break;
+      case 512: kern = w4a4_gemm_kernel<BT, false, 512>; break;
+      default: break;
+    }
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  const int grid = p.num_items < num_sms ? p.num_items : num_sms;
   static long long* trace = nullptr;
-  static const bool want_trace = getenv("ATOM_GEMM_TRACE") != nullptr;   // development probe only
-  if (want_trace && trace == nullptr) cudaMalloc(&trace, 7 * 256 * sizeof(long long));
+  static const bool want_trace = getenv("ATOM_GEMM_TRACE") != nullptr;   // development only
+  if (want_trace && trace == nullptr) cudaMalloc(&trace, 8 * kTraceN * sizeof(long long));
   p.trace = want_trace ? trace : nullptr;
-  kern<<<grid, kThreads, smem, stream>>>(m_wq4, m_aq4, m_wq8, m_aq8, p);
+  if (want_trace) cudaMemsetAsync(trace, 0, 8 * kTraceN * sizeof(long long), stream);
+  kern<<<plan.grid, kThreads, smem, stream>>>(m_wq4, m_wq8, m_ax8, p);
   ++*launches;
   if (want_trace) {
-    long long h[1792];
+    static long long h[8 * kTraceN];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "plan: BT=%d ksplit=%d tiles=%d items=%d grid=%d\n", BT, p.ksplit,
-            p.num_tiles, p.num_items, grid);
-    fprintf(stderr, "trace g: ufull_arrive mma_issue mma_committed epi_seen (clk rel. to mma_issue[0])\n");
-    for (int g = 0; g < 256 && g < p.G * 2; ++g)
-      fprintf(stderr, "%3d %9lld %9lld %9lld %9lld\n", g, h[256 + g] - h[0], h[g] - h[0],
-              h[1536 + g] - h[0], h[512 + g] - h[0]);
-    long long t0 = h[768];
-    for (int b = 0; b < grid && b < 256; ++b) t0 = h[768 + b] < t0 ? h[768 + b] : t0;
-    fprintf(stderr, "cta: start_ns groups_done_ns end_ns (rel. to first start)\n");
-    for (int b = 0; b < grid && b < 256; ++b)
-      fprintf(stderr, "%3d %8lld %8lld %8lld\n", b, h[768 + b] - t0, h[1024 + b] - t0,
-              h[1280 + b] - t0);
+    fprintf(stderr, "plan: BT=%d grid=%d dp_waves=%d sk_units=%lld tiles=%d\n", BT, plan.grid,
+            plan.dp_waves, static_cast<long long>(plan.sk_units), p.num_tiles);
+    fprintf(stderr, "g   W_tma  mma_tempty mma_ufull mma_afull unp_done epi_sready epi_mdone epi_tempty\n");
+    const long long t0 = h[0];
+    for (int g = 0; g < kTraceN && (g < 40 || g % 25 == 0); ++g) {
+      if (h[3 * kTraceN + g] == 0) break;
+      fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld\n", g, h[g] - t0,
+              h[kTraceN + g] - t0, h[2 * kTraceN + g] - t0, h[3 * kTraceN + g] - t0,
+              h[4 * kTraceN + g] - t0, h[5 * kTraceN + g] - t0, h[6 * kTraceN + g] - t0,
+              h[7 * kTraceN + g] - t0);
+    }
   }
   return cudaGetLastError();
 }
 
-// Tile / split-K plan.  BT = 256 tokens when the 128 x 256 tiles fill the SMs; otherwise the
-// smallest power of two >= M (no wasted token columns) and the K groups are split S ways so that
-// the (tile, split) items fill one wave as evenly as possible (each split >= 4 groups).  Splits
-// publish fp32 partials in the workspace; the last split to arrive reduces (no spinning).
+// Tile plan.  Every plan runs one persistent CTA per SM (or per unit, if fewer): whole tiles in
+// round-robin waves while at least two waves remain, then the rest as evenly divided
+// (tile, group) units (stream-K).  The only choice is the token tile BT: the largest power of
+// two <= 256 that does not exceed the padded M, traded (by a simple clock-count model) against
+// the cost of reducing split tiles when there are few units per CTA.
 GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms) {
-  GemmPlan pl;
+  GemmPlan best;
   const int64_t n_tiles = N / kTileN;
-  const int G = static_cast<int>(K / 128);
-  auto tiles = [&](int bt) { return n_tiles * ((M + bt - 1) / bt); };
-  if (tiles(256) >= num_sms) {
-    pl.bt = 256;
-  } else {
-    pl.bt = 32;
-    while (pl.bt < 256 && pl.bt < M) pl.bt *= 2;
-  }
-  const int64_t t = tiles(pl.bt);
-  pl.ksplit = 1;
-  if (t < 2 * num_sms) {
-    double best = 1e30;
-    for (int sp = 1; sp <= G / 4 && sp <= 16; ++sp) {
-      const double cost = static_cast<double>((t * sp + num_sms - 1) / num_sms) / sp;
-      if (cost < best - 1e-9) {
-        best = cost;
-        pl.ksplit = sp;
-      }
+  const int64_t G = K / 128;
+  int bt_max = 32;
+  static const char* btm = getenv("ATOM_GEMM_BT_MAX");   // development override
+  const int bt_cap = btm ? atoi(btm) : 256;
+  while (bt_max < bt_cap && bt_max < M) bt_max *= 2;
+  double best_cost = 1e300;
+  for (int bt = bt_max; bt >= 32; bt /= 2) {
+    GemmPlan pl;
+    pl.bt = bt;
+    pl.num_tiles = n_tiles * ((M + bt - 1) / bt);
+    const int64_t units = pl.num_tiles * G;
+    pl.grid = static_cast<int>(units < num_sms ? units : num_sms);
+    const int64_t T = pl.num_tiles, P = pl.grid;
+    if (T % P == 0) pl.dp_waves = static_cast<int>(T / P);
+    else if (T >= 2 * P) pl.dp_waves = static_cast<int>(T / P - 1);
+    else pl.dp_waves = 0;
+    pl.sk_units = (T - static_cast<int64_t>(pl.dp_waves) * P) * G;
+    // per group: MMA 2*BT clk (full rate at N >= 128, measured 67% at N = 64), weight unpack
+    // ~200 clk; a split tile costs its reducer one partial slot read per extra segment
+    const double per_unit = bt >= 128 ? 2.0 * bt : bt == 64 ? 192.0 : 160.0;
+    const double unit_cost = per_unit > 200.0 ? per_unit : 200.0;
+    const double per_cta = static_cast<double>((units + P - 1) / P);
+    const double sk_per_cta = static_cast<double>(pl.sk_units) / P;
+    const double segs = sk_per_cta > 0 ? static_cast<double>(G) / sk_per_cta : 0.0;
+    const double cost = per_cta * unit_cost +
+                        (segs > 1.0 ? segs - 1.0 : 0.0) * slot_bytes_for(bt) / 64.0;
+    bool split = false;
+    for (int64_t i = 1; i < P && !split && pl.sk_units > 0; ++i)
+      split = (i * pl.sk_units / P) % G != 0;
+    if (split) {
+      // counters are indexed by the reducing CTA, so their region has the same size and place
+      // for every shape on this device (only it must stay zero between calls)
+      pl.counter_bytes = ((num_sms * sizeof(int) + 255) / 256) * 256;
+      pl.workspace_bytes = pl.counter_bytes + pl.grid * slot_bytes_for(bt);
+    }
+    if (cost < best_cost * 0.97) {
+      best_cost = cost;
+      best = pl;
     }
   }
-  pl.num_tiles = t;
-  if (pl.ksplit > 1) {
-    pl.counter_bytes = ((t * sizeof(int) + 255) / 256) * 256;
-    pl.workspace_bytes = pl.counter_bytes + t * pl.ksplit * kTileN * pl.bt * sizeof(float);
-  }
-  return pl;
+  return best;
 }
 
 cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,
@@ -763,10 +877,10 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   const GemmPlan pl = plan_w4a4_gemm(a.M, a.N, a.K, num_sms);
   if (workspace_bytes < pl.workspace_bytes) return cudaErrorInvalidValue;
   switch (pl.bt) {
-    case 256: return launch_bt<256>(a, pl, workspace, stream, num_sms, launches);
-    case 128: return launch_bt<128>(a, pl, workspace, stream, num_sms, launches);
-    case 64: return launch_bt<64>(a, pl, workspace, stream, num_sms, launches);
-    default: return launch_bt<32>(a, pl, workspace, stream, num_sms, launches);
+    case 256: return launch_bt<256>(a, pl, workspace, stream, launches);
+    case 128: return launch_bt<128>(a, pl, workspace, stream, launches);
+    case 64: return launch_bt<64>(a, pl, workspace, stream, launches);
+    default: return launch_bt<32>(a, pl, workspace, stream, launches);
   }
 }
 

@@ -10,14 +10,13 @@ namespace atom {
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    float* scales, cudaStream_t stream, int num_sms);
+                                    int8_t* x8, float* scales, cudaStream_t stream, int num_sms);
 
 cudaError_t launch_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
                                  int32_t* ok, cudaStream_t stream);
 
 struct GemmArgs {
-  const uint8_t* a_q4;
-  const int8_t* a_q8;
+  const int8_t* a_x8;
   const float* a_scales;
   const uint8_t* w_q4;
   const int8_t* w_q8;
@@ -32,10 +31,12 @@ struct GemmArgs {
 
 struct GemmPlan {
   int bt = 256;                 // token tile
-  int ksplit = 1;               // K splits per tile
+  int grid = 0;                 // persistent CTAs (<= SMs)
+  int dp_waves = 0;             // whole-tile round-robin waves
+  int64_t sk_units = 0;         // (tile, group) units divided evenly after the waves
   int64_t num_tiles = 0;
   size_t counter_bytes = 0;
-  size_t workspace_bytes = 0;   // 0 when ksplit == 1
+  size_t workspace_bytes = 0;   // 0 when no tile is split between CTAs
 };
 
 GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms);

@@ -42,7 +42,7 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                         const int32_t* __restrict__ perm, int32_t G, int32_t G4,
                         int32_t groups_per_cta, float clip4, float clip8,
                         uint8_t* __restrict__ q4, int8_t* __restrict__ q8,
-                        float* __restrict__ scales) {
+                        int8_t* __restrict__ x8, int64_t K, float* __restrict__ scales) {
   extern __shared__ uint4 srow4[];
   const __half* srow = reinterpret_cast<const __half*>(srow4);
   const int64_t row = blockIdx.x;
@@ -85,12 +85,30 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
     const float s = (amax == 0.0f) ? FLT_MIN : __fmul_rn(amax, is_int4 ? alpha4 : alpha8);
     const float inv = __frcp_rn(s);
     if (valid) {
+      int8_t* xg = x8 ? x8 + row * K + t * 128 : nullptr;
       if (is_int4) {
-        uint32_t packed = 0;
+        int q[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          packed |= static_cast<uint32_t>(quant_code(v[k], inv, -8, 7) & 0xF) << (4 * k);
-        reinterpret_cast<uint32_t*>(q4 + row * row4 + t * 64)[hl] = packed;
+        for (int k = 0; k < 8; ++k) q[k] = quant_code(v[k], inv, -8, 7);
+        if (q4) {
+          uint32_t packed = 0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) packed |= static_cast<uint32_t>(q[k] & 0xF) << (4 * k);
+          reinterpret_cast<uint32_t*>(q4 + row * row4 + t * 64)[hl] = packed;
+        }
+        if (xg) {
+          // GEMM operand order (atom.h "x8"): channel 32c + 8i + 2b + h of the group sits at
+          // byte 32c + 16h + 4i + b -- the order in which the GEMM unpacks weight nibbles.
+          uint32_t ev = 0, od = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            ev |= static_cast<uint32_t>(q[2 * b] & 0xFF) << (8 * b);
+            od |= static_cast<uint32_t>(q[2 * b + 1] & 0xFF) << (8 * b);
+          }
+          const int p = 32 * (hl >> 2) + 4 * (hl & 3);
+          *reinterpret_cast<uint32_t*>(xg + p) = ev;
+          *reinterpret_cast<uint32_t*>(xg + p + 16) = od;
+        }
       } else {
         uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -98,7 +116,8 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
           lo |= static_cast<uint32_t>(quant_code(v[k], inv, -128, 127) & 0xFF) << (8 * k);
           hi |= static_cast<uint32_t>(quant_code(v[k + 4], inv, -128, 127) & 0xFF) << (8 * k);
         }
-        reinterpret_cast<uint2*>(q8 + row * 128)[hl] = make_uint2(lo, hi);
+        if (q8) reinterpret_cast<uint2*>(q8 + row * 128)[hl] = make_uint2(lo, hi);
+        if (xg) reinterpret_cast<uint2*>(xg)[hl] = make_uint2(lo, hi);
       }
       if (hl == 0) scales[static_cast<int64_t>(t) * rows + row] = s;
     }
@@ -108,7 +127,7 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    float* scales, cudaStream_t stream, int num_sms) {
+                                    int8_t* x8, float* scales, cudaStream_t stream, int num_sms) {
   const int G = static_cast<int>(K / 128);
   const int G4 = static_cast<int>((K - k_outlier) / 128);
   // Enough CTAs to cover the SMs ~4 times; each extra split re-stages the row (from L2).
@@ -126,7 +145,7 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
   }
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
   reorder_quantize_kernel<<<grid, kQuantThreads, smem, stream>>>(
-      static_cast<const __half*>(x), rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, scales);
+      static_cast<const __half*>(x), rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, x8, K, scales);
   return cudaGetLastError();
 }
 

@@ -5,7 +5,8 @@ bench.py.  Nothing here computes the method: quantization and the GEMM run in li
 
 N-shard (column parallel): rank r owns output channels [n0, n1) (multiples of 128); X is
 replicated; each rank writes an fp16 [M][N/P] block; all-gather -> [P][M][N/P] -> [M][N].
-The output is bit-identical to one GPU (the K accumulation order is unchanged).
+Each shard's output equals one GPU's within the fp32-reordering tolerance (each shard GEMM has
+its own work schedule, which may split a tile's K accumulation at other points).
 
 K-shard (row parallel): rank r owns a contiguous range of 128-channel groups [g0, g1) of the
 REORDERED channels; its perm slice is perm[g0*128 : g1*128]; the INT8 outlier group (the last

@@ -51,7 +51,7 @@ def test_sm100a_only_cubin():
 
 
 def test_version_and_status_strings(lib):
-    assert lib.atom_abi_version() == 1
+    assert lib.atom_abi_version() == 2
     for s in range(8):
         assert lib.atom_status_string(s).startswith(b"ATOM_")
 
@@ -60,26 +60,26 @@ def test_host_validation_without_device(lib):
     f = ctypes.c_float
     # shape / argument errors are detected before any device query
     assert lib.atom_reorder_quantize(None, -1, 256, None, 256, 128, f(0.9), f(1.0), None, None,
-                                     None, None) == 2
+                                     None, None, None) == 2
     assert lib.atom_reorder_quantize(None, 4, 256, None, 200, 128, f(0.9), f(1.0), None, None,
-                                     None, None) == 2
+                                     None, None, None) == 2
     assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 64, f(0.9), f(1.0), None, None,
-                                     None, None) == 4
+                                     None, None, None) == 4
     assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(1.5), f(1.0), None, None,
-                                     None, None) == 4
+                                     None, None, None) == 4
     assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(0.9), f(1.0), None, None,
-                                     None, None) == 1
+                                     None, None, None) == 1
     assert lib.atom_quantize_weights(None, 4, 250, None, 256, 128, f(0.85), f(1.0), None, None,
                                      None, None) == 2
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 4, 100, 256, 128, None, 128, 0,
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, 4, 100, 256, 128, None, 128, 0,
                               None, None, 0, None) == 2
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 4, 128, 256, 128, None, 128, 3,
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, 4, 128, 256, 128, None, 128, 3,
                               None, None, 0, None) == 4
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 4, 128, 256, 128, None, 128, 0,
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, 4, 128, 256, 128, None, 128, 0,
                               None, None, 0, None) == 1
     assert lib.atom_w4a4_gemm_workspace_size(1024, 28672, 8192, 128) == 0
     # M == 0 is a no-op that succeeds without a device
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
+    assert lib.atom_w4a4_gemm(None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
                               None, None, 0, None) == 0
     assert lib.atom_last_launch_count() == 0
 
