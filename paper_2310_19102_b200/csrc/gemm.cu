@@ -44,32 +44,37 @@
 namespace atom {
 
 // Warp roles (16 warps, 4 warpgroups):
-//   WG0: warp 0 producer (scales via cp.async + TMA), warp 1 MMA issuer, warps 2-3 unpack
-//   WG1-WG3: warps 4-15 epilogue (warp % 4 = TMEM lane quarter, (warp - 4) / 4 = column third)
-// setmaxnreg moves registers from WG0 (56 each) to the epilogue warpgroups (152 each), which
-// hold the fp32 accumulators of a 128 x BT tile (BT/3 per thread).
+//   WG0: warp 0 producer (scales via cp.async, packed weights via TMA), warp 1 MMA issuer,
+//        warp 2 activation-tile loader (TMA), warp 3 idle
+//   WG1: warps 4-7 unpack (one per SM sub-partition, so it never queues behind 2 others)
+//   WG2-WG3: warps 8-15 epilogue (warp % 4 = TMEM lane quarter, (warp - 8) / 4 = column half)
+// setmaxnreg moves registers from WG0/WG1 (56 each) to the epilogue warpgroups (200 each),
+// which hold the fp32 accumulators of a 128 x BT tile (BT/2 per thread).
 constexpr int kThreads = 512;
-constexpr int kUnpackWarp0 = 2;
-constexpr int kNumUnpackWarps = 2;
-constexpr int kEpiWarp0 = 4;
-constexpr int kNumEpiWarps = 12;
+constexpr int kALoaderWarp = 2;
+constexpr int kUnpackWarp0 = 4;
+constexpr int kNumUnpackWarps = 4;
+constexpr int kEpiWarp0 = 8;
+constexpr int kNumEpiWarps = 8;
+constexpr int kEpiPerQuarter = kNumEpiWarps / 4;   // warps sharing one TMEM lane quarter
 constexpr int kEpiThreads = kNumEpiWarps * 32;
-constexpr int kRegsLow = 56, kRegsHigh = 152;           // 4*32*56 + 12*32*152 = 65536
+constexpr int kRegsLow = 56, kRegsHigh = 200;           // 8*32*56 + 8*32*200 = 65536
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
 constexpr int kSRing = 8;       // group-scale ring depth
 
 template <int BT> struct Cfg {
   static constexpr int RT = BT >= 256 ? 2 : 4;          // TMEM accumulator buffers
-  static constexpr int RS = BT >= 256 ? 3 : 4;          // operand slots (unpacked W + A tile)
-  static constexpr int kStages = BT >= 256 ? 6 : 8;     // packed weight TMA ring depth
+  static constexpr int RS = 4;                          // activation slots (= go / mdone ring)
+  static constexpr int RW = BT >= 256 ? 2 : 4;          // unpacked weight slots
+  static constexpr int kStages = BT >= 256 ? 5 : 8;     // packed weight TMA ring depth
   static constexpr uint32_t kTmemCols = RT * BT <= 32 ? 32 : RT * BT <= 64 ? 64
                                       : RT * BT <= 128 ? 128 : RT * BT <= 256 ? 256 : 512;
   static constexpr int NC = BT / 8;                     // 8-column chunks of the tile
-  static constexpr int NJ = (NC + 2) / 3;               // chunks per epilogue warp (max)
-  // split-tile partial of one CTA: thread-linear, [12 warps][NJ*8/4 column quads][32 lanes] float4
+  static constexpr int NJ = (NC + kEpiPerQuarter - 1) / kEpiPerQuarter;   // chunks per warp
+  // split-tile partial of one CTA: thread-linear, [epi warps][NJ*8/4 column quads][32 lanes] float4
   static constexpr size_t kSlotFloats = static_cast<size_t>(kNumEpiWarps) * NJ * 8 * 32;
   static_assert(RT * BT <= 512, "TMEM holds at most 512 columns");
-  static_assert(RS >= RT, "an operand slot must outlive its accumulator");
+  static_assert(RS >= RT && RS >= RW, "ring sizes");
 };
 
 constexpr uint32_t kMagicBits = 0x4B400000u;   // bit pattern of 1.5*2^23
@@ -101,8 +106,9 @@ constexpr int kTraceN = 512;
 template <int BT>
 struct __align__(1024) GemmSmem {
   static constexpr int RS = Cfg<BT>::RS;
+  static constexpr int RW = Cfg<BT>::RW;
   static constexpr int RT = Cfg<BT>::RT;
-  uint8_t ubuf_w[RS][kTileN * 128];     // unpacked weight group, SW128 K-major
+  uint8_t ubuf_w[RW][kTileN * 128];     // unpacked weight group, SW128 K-major
   uint8_t ubuf_a[RS][BT * 128];         // activation group (x8), SW128 K-major, written by TMA
   uint8_t stage_w[Cfg<BT>::kStages][kTileN * 64];   // packed weight group (or INT8 half)
   float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
@@ -241,7 +247,7 @@ __device__ __forceinline__ Item get_item(const GemmParams& p, const Sched& s, in
 // Walks this CTA's (item, group) sequence one group at a time.
 template <int BT>
 struct GroupCursor {
-  int k, t, t1, m0;
+  int k, t, t1, m0, tile;
   __device__ __forceinline__ bool valid(const Sched& s) const { return k < s.count(); }
   __device__ __forceinline__ void load(const GemmParams& p, const Sched& s) {
     if (k < s.count()) {
@@ -249,6 +255,7 @@ struct GroupCursor {
       t = w.t0;
       t1 = w.t1;
       m0 = w.m0;
+      tile = w.tile;
     }
   }
   __device__ __forceinline__ void next(const GemmParams& p, const Sched& s) {
@@ -282,7 +289,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                  const __grid_constant__ CUtensorMap tm_ax8, const GemmParams p) {
   static_assert(BT % 32 == 0 && BT >= 32 && BT <= 256, "token tile");
   using C = Cfg<BT>;
-  constexpr int RS = C::RS, RT = C::RT, NJ = C::NJ, NC = C::NC, KS = C::kStages;
+  constexpr int RS = C::RS, RW = C::RW, RT = C::RT, NJ = C::NJ, NC = C::NC, KS = C::kStages;
   constexpr uint32_t kTmemCols = C::kTmemCols;
   extern __shared__ uint8_t smem_raw[];
   GemmSmem<BT>& sm = *reinterpret_cast<GemmSmem<BT>*>(
@@ -327,8 +334,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   if (warp < kEpiWarp0) setmaxnreg_dec<kRegsLow>();
   if (warp == 0) {
     // ===================== producer warp: group scales (cp.async) + packed weights (TMA) =====
-    // Not tied to the operand slots, so the weight stream runs up to KS stages ahead.  (The
-    // activation tiles are issued by the epilogue as slots free up, see below.)
+    // Not tied to the operand slots, so the weight stream runs up to KS stages ahead of the
+    // unpack warps.  (Activation tiles have their own loader warp.)
     Ring<KS> st;
     Ring<kSRing> sr;
     int gp = 0;
@@ -363,6 +370,25 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         }
       }
     }
+  } else if (warp == kALoaderWarp) {
+    // ===================== activation-tile loader (single thread) =====================
+    // Slot u is free exactly when the MMAs of the group that used it complete; the tile of
+    // group g (x8, TMA, SWIZZLE_128B straight into the operand slot) is issued right then.
+    if (lane == 0) {
+      Ring<RS> u;
+      for (int k = 0; k < n_items; ++k) {
+        const Item w = get_item<BT>(p, sch, k);
+        for (int t = w.t0; t < w.t1; ++t, u.next()) {
+          wait_hot(&sm.mdone[u.i], u.ph ^ 1);
+          if constexpr ((kMode & 16) != 0) {
+            mbar_arrive(&sm.go[u.i]);
+          } else {
+            mbar_arrive_expect_tx(&sm.go[u.i], BT * 128);
+            tma_load_2d(sm.ubuf_a[u.i], &tm_ax8, &sm.go[u.i], t * 128, w.m0);
+          }
+        }
+      }
+    }
   } else if (warp == 1) {
     // ===================== MMA issuer (single thread) =====================
     // Every instruction this thread executes between dispatches idles the tensor pipe for as
@@ -378,6 +404,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       const uint64_t da0 = umma_desc_sw128(smem_u32(sm.ubuf_w[0]));
       const uint64_t db0 = umma_desc_sw128(smem_u32(sm.ubuf_a[0]));
       Ring<RS> u;
+      Ring<RW> uw;
       Ring<RT> b;
       for (int gm = 0; gm < total; ++gm) {
         wait_hot(&sm.go[u.i], u.ph);
@@ -385,7 +412,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         TRACE(3, gm);
         const uint32_t d = tmem + b.i * BT;
         // descriptor start address field counts 16-byte units: slot u, K step kk (32 bytes)
-        const uint64_t da = da0 + u.i * (kTileN * 128 / 16);
+        const uint64_t da = da0 + uw.i * (kTileN * 128 / 16);
         const uint64_t db = db0 + u.i * (BT * 128 / 16);
         const uint32_t acc0 = ((kMode & 4) != 0 && (b.i & 1u) == 0) ? 1u : 0u;
 #pragma unroll
@@ -397,36 +424,33 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if constexpr ((kMode & 256) != 0)   // probe: MMA latency (issue -> completion)
           mbar_wait_spin(&sm.mdone[u.i], u.ph);
         u.next();
+        uw.next();
         b.next();
       }
     }
-  } else if (warp < kEpiWarp0) {
+  } else if (warp >= kUnpackWarp0 && warp < kEpiWarp0) {
     // ===================== unpack warps: packed INT4 weights -> int8 (16*q), SW128 ============
-    // 64 threads: thread ut owns packed chunk (ut & 3) of rows (ut >> 2) + 16k, k < 8.
+    // 128 threads: thread ut owns packed chunk (ut & 3) of rows (ut >> 2) + 32k, k < 4.
     const int ut = threadIdx.x - kUnpackWarp0 * 32;
     const uint32_t r0 = static_cast<uint32_t>(ut) >> 2, c = static_cast<uint32_t>(ut) & 3u;
     Ring<KS> st;
-    Ring<RS> u;
+    Ring<RS> u;                          // go slot of group g
+    Ring<RS> lag;                        // mdone slot of group g - RW
+    Ring<RW> uw;                         // unpacked-weight slot of group g
     int gu = 0;
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
-      for (int t = w.t0; t < w.t1; ++t, u.next(), ++gu) {
-        mbar_wait(&sm.mdone[u.i], u.ph ^ 1);  // MMAs of group g - RS finished with this slot
-        if (ut == 0) {
-          // the activation tile of this group (x8, TMA, SWIZZLE_128B straight into the slot)
-          if constexpr ((kMode & 16) != 0) {
-            mbar_arrive(&sm.go[u.i]);
-          } else {
-            mbar_arrive_expect_tx(&sm.go[u.i], BT * 128);
-            tma_load_2d(sm.ubuf_a[u.i], &tm_ax8, &sm.go[u.i], t * 128, w.m0);
-          }
+      for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), ++gu) {
+        if (gu >= RW) {                  // MMAs of group g - RW finished with this weight slot
+          wait_hot(&sm.mdone[lag.i], lag.ph);
+          lag.next();
         }
         const bool int4 = t < G4;
         const int nh = int4 ? 1 : 2;
         for (int h = 0; h < nh; ++h, st.next()) {
-          mbar_wait(&sm.full[st.i], st.ph);
+          wait_hot(&sm.full[st.i], st.ph);
           if constexpr ((kMode & 64) == 0)
-            unpack_rows<8, 16>(sm.stage_w[st.i], sm.ubuf_w[u.i], r0, c, int4, h);
+            unpack_rows<4, 32>(sm.stage_w[st.i], sm.ubuf_w[uw.i], r0, c, int4, h);
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[st.i]);
         }
@@ -436,7 +460,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (lane == 0) mbar_arrive(&sm.go[u.i]);
       }
     }
-  } else {
+  } else if (warp >= kEpiWarp0) {
     // ===================== epilogue warps =====================
     // TMEM is read with the 32x32b shape: thread = TMEM lane = output channel n (its weight
     // scale is one scalar per group), consecutive registers = consecutive tokens of this warp's
@@ -447,8 +471,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     setmaxnreg_inc<kRegsHigh>();
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int third = e >> 2;
-    constexpr int kBase = NC / 3, kRem = NC % 3;
+    const int third = e >> 2;            // column part (kEpiPerQuarter parts)
+    constexpr int kBase = NC / kEpiPerQuarter, kRem = NC % kEpiPerQuarter;
     constexpr int NCOL = NJ * 8;         // columns of the widest third
     const int ncol = 8 * (kBase + (third < kRem ? 1 : 0));             // this warp (uniform)
     const int col0 = 8 * (third * kBase + (third < kRem ? third : kRem));
@@ -456,12 +480,15 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     const uint32_t magic = kMagicBits;
     const bool a_issuer = e == 0 && lane == 0;
     const int n_local = q * 32 + lane;   // output channel within the tile
+    uint32_t mg[8];                      // resident tcgen05.st sources for the magic re-arm
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mg[i] = magic;
+    asm volatile("" : "+r"(mg[0]), "+r"(mg[1]), "+r"(mg[2]), "+r"(mg[3]), "+r"(mg[4]),
+                 "+r"(mg[5]), "+r"(mg[6]), "+r"(mg[7]));
     auto rearm = [&](uint32_t taddr) {   // this warp's columns of one buffer := 1.5*2^23
 #pragma unroll
-      for (int j = 0; j < NCOL; j += 16) {
-        if (j + 16 <= ncol) tmem_st16_const(taddr + j, magic);
-        else if (j + 8 <= ncol) tmem_st8_const(taddr + j, magic);
-      }
+      for (int j = 0; j < NCOL; j += 8)
+        if (j + 8 <= ncol) tmem_st8(taddr + j, mg);
       tmem_st_wait();
     };
     if constexpr ((kMode & 4) != 0) {
@@ -486,7 +513,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       for (int j = 0; j < NCOL; ++j) acc[j] = 0.0f;
       for (int t = w.t0; t < w.t1; ++t, u.next(), b.next(), sr.next(), ++ge) {
         const bool int4 = t < G4;
-        mbar_wait(&sm.sready[sr.i], sr.ph);
+        wait_hot(&sm.sready[sr.i], sr.ph);
         if (a_issuer) TRACE(5, ge);
         // sw' = sw (x1/16 for INT4 groups, exact) with its 2 lowest mantissa bits cleared so
         // that 1.5*2^23*sw' is exact; see DESIGN.md "Epilogue arithmetic".

@@ -290,6 +290,15 @@ __device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* r) {
       : "memory");
 }
 
+// Warp-collective: 8 consecutive columns of this thread's lane from 8 caller-held registers.
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                   taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+               "r"(v[7])
+               : "memory");
+}
+
 // Warp-collective: store the same 32-bit value to 8 consecutive columns of this thread's lane.
 __device__ __forceinline__ void tmem_st8_const(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(

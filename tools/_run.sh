@@ -1,5 +1,5 @@
-timeout 30 python tools/shape_check.py 16 1024 1024; echo rc=$?
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "gemm or workspace or shard" 2>&1 | tail -2
-for m in 0 1; do ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg5; done
-ATOM_GEMM_TRACE=1 timeout 60 python tools/gemm_probe.py cfg5 > gpurun_out/trace5_g.log 2>&1
-tail -5 gpurun_out/trace5_g.log
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4 > gpurun_out/t9_pytest.log
+for c in cfg5 cfg2 cfg4 cfg3_up cfg3_down cfg1; do timeout 60 python tools/gemm_probe.py $c; done > gpurun_out/t9_probe.log 2>&1
+timeout 300 python bench.py > gpurun_out/t9_bench.log 2>&1
+timeout 300 python bench.py --config cfg2 > gpurun_out/t9_bench2.log 2>&1
+cat gpurun_out/t9_pytest.log gpurun_out/t9_probe.log; tail -c 300 gpurun_out/t9_bench.log

@@ -55,7 +55,11 @@ __global__ void __launch_bounds__(WPQ * 128 + 128, 1) drain(int iters, int mma, 
         uint32_t r[JB];
 #pragma unroll
         for (int j = j0; j < j0 + JB && j < NCOLMAX; j += 16) {
-          if (JB == 32 && j == j0 && j + 32 <= ncol) { tmem_ld32(tq + j, *reinterpret_cast<uint32_t(*)[32]>(r)); j += 16; continue; }
+          if (JB >= 32 && j == j0 && j + JB <= ncol) {
+#pragma unroll
+            for (int jj = 0; jj < JB; jj += 32) tmem_ld32(tq + j + jj, *reinterpret_cast<uint32_t(*)[32]>(r + jj));
+            j += JB - 16; continue;
+          }
           if (j + 16 <= ncol) tmem_ld16p(tq + j, r + (j - j0));
           else if (j + 8 <= ncol) tmem_ld8(tq + j, r + (j - j0));
         }
@@ -107,7 +111,8 @@ void run(int sms, int mma, long long* d) {
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   long long* d; cudaMalloc(&d, 512 * sizeof(long long));
-  run<3, 16, 1>(sms, 1, d); run<3, 32, 1>(sms, 1, d); run<3, 16, 0>(sms, 1, d);
-  run<4, 16, 1>(sms, 1, d); run<4, 32, 1>(sms, 1, d); run<4, 16, 0>(sms, 1, d);
+  run<3, 16, 1>(sms, 1, d);
+  run<2, 16, 1>(sms, 1, d); run<2, 32, 1>(sms, 1, d); run<2, 64, 1>(sms, 1, d);
+  run<2, 32, 0>(sms, 1, d); run<2, 64, 0>(sms, 1, d);
   return 0;
 }
