@@ -10,7 +10,8 @@
 // shared memory with 128-bit streaming loads (coalesced), the gather x'[j] = x[perm[j]] then
 // reads shared memory.  One half-warp per 128-channel group: each lane owns 8 reordered
 // channels (two 128-bit perm loads), the group |max| is a 4-step shuffle reduction, codes are
-// packed in registers and written as 64 contiguous bytes (INT4) or 128 bytes (INT8).
+// packed in registers and written as 64 contiguous bytes (INT4) or 128 bytes (INT8), plus the
+// GEMM operand form x8 (one byte per code, include/atom.h).
 // Numerics are pinned to the oracle's binary32 steps: __fdiv_rn / __fmul_rn / __frcp_rn are
 // IEEE round-to-nearest and never contracted; cvt.rni gives round-half-to-even.
 #include <cfloat>
@@ -61,15 +62,30 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
   const float alpha8 = __fdiv_rn(__fmul_rn(2.0f, clip8), 255.0f);
   const int64_t row4 = static_cast<int64_t>(G4) * 64;
 
-  // Each warp quantizes two groups at a time, one per half-warp; a lane owns 8 consecutive
-  // reordered channels (two 128-bit perm loads), the group |max| is a 4-step shuffle.
+  // Two groups per warp, one per half-warp; a lane owns 8 consecutive reordered channels (two
+  // 128-bit perm loads), the group |max| is a 4-step shuffle.  Codes: v = fl(x * fl(1/s)) (one
+  // RN multiply), clamped to the code range (clamping to integer bounds commutes with
+  // rounding), then rounded half-to-even by adding 1.5*2^23 in binary32 -- the sum's low bits
+  // ARE the two's-complement code (0x4B400000 is a multiple of 256), so no float->int
+  // conversion is needed; bytes are gathered with PRMT.
   const int hw = lane >> 4, hl = lane & 15;
+  constexpr float kRint = 12582912.0f;   // 1.5 * 2^23
+  // the perm slices are software-prefetched one iteration ahead (an L2 round trip per group
+  // would otherwise sit on the critical path)
+  auto perm_at = [&](int t0, int4& a, int4& b) {
+    const int t = t0 + hw;
+    const int tt = t < g_end ? t : t0;
+    a = __ldg(reinterpret_cast<const int4*>(perm + tt * 128 + 8 * hl));
+    b = __ldg(reinterpret_cast<const int4*>(perm + tt * 128 + 8 * hl + 4));
+  };
+  int4 pa_n, pb_n;
+  if (g_begin + 2 * warp < g_end) perm_at(g_begin + 2 * warp, pa_n, pb_n);
   for (int t0 = g_begin + 2 * warp; t0 < g_end; t0 += 2 * kQuantWarps) {
     const int t = t0 + hw;
     const bool valid = t < g_end;
     const int tt = valid ? t : t0;
-    const int4 pa = __ldg(reinterpret_cast<const int4*>(perm + tt * 128 + 8 * hl));
-    const int4 pb = __ldg(reinterpret_cast<const int4*>(perm + tt * 128 + 8 * hl + 4));
+    const int4 pa = pa_n, pb = pb_n;
+    if (t0 + 2 * kQuantWarps < g_end) perm_at(t0 + 2 * kQuantWarps, pa_n, pb_n);
     float v[8];
     v[0] = __half2float(srow[pa.x]); v[1] = __half2float(srow[pa.y]);
     v[2] = __half2float(srow[pa.z]); v[3] = __half2float(srow[pa.w]);
@@ -84,40 +100,34 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
     const bool is_int4 = tt < G4;
     const float s = (amax == 0.0f) ? FLT_MIN : __fmul_rn(amax, is_int4 ? alpha4 : alpha8);
     const float inv = __frcp_rn(s);
+    const float lo = is_int4 ? -8.0f : -128.0f, hi = is_int4 ? 7.0f : 127.0f;
+    uint32_t f[8];   // bit patterns of 1.5*2^23 + q: low byte = q (two's complement)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      f[k] = __float_as_uint(__fadd_rn(fminf(fmaxf(__fmul_rn(v[k], inv), lo), hi), kRint));
+    // even / odd channels, one byte each: E = [q0 q2 q4 q6], O = [q1 q3 q5 q7]
+    const uint32_t ev = __byte_perm(__byte_perm(f[0], f[2], 0x0040), __byte_perm(f[4], f[6], 0x0040),
+                                    0x5410);
+    const uint32_t od = __byte_perm(__byte_perm(f[1], f[3], 0x0040), __byte_perm(f[5], f[7], 0x0040),
+                                    0x5410);
     if (valid) {
       int8_t* xg = x8 ? x8 + row * K + t * 128 : nullptr;
       if (is_int4) {
-        int q[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) q[k] = quant_code(v[k], inv, -8, 7);
-        if (q4) {
-          uint32_t packed = 0;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) packed |= static_cast<uint32_t>(q[k] & 0xF) << (4 * k);
-          reinterpret_cast<uint32_t*>(q4 + row * row4 + t * 64)[hl] = packed;
-        }
+        // packed byte j = (q_2j & 0xF) | (q_2j+1 << 4)   (low nibble = even channel)
+        if (q4)
+          reinterpret_cast<uint32_t*>(q4 + row * row4 + t * 64)[hl] =
+              (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
         if (xg) {
           // GEMM operand order (atom.h "x8"): channel 32c + 8i + 2b + h of the group sits at
           // byte 32c + 16h + 4i + b -- the order in which the GEMM unpacks weight nibbles.
-          uint32_t ev = 0, od = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            ev |= static_cast<uint32_t>(q[2 * b] & 0xFF) << (8 * b);
-            od |= static_cast<uint32_t>(q[2 * b + 1] & 0xFF) << (8 * b);
-          }
           const int p = 32 * (hl >> 2) + 4 * (hl & 3);
           *reinterpret_cast<uint32_t*>(xg + p) = ev;
           *reinterpret_cast<uint32_t*>(xg + p + 16) = od;
         }
       } else {
-        uint32_t lo = 0, hi = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          lo |= static_cast<uint32_t>(quant_code(v[k], inv, -128, 127) & 0xFF) << (8 * k);
-          hi |= static_cast<uint32_t>(quant_code(v[k + 4], inv, -128, 127) & 0xFF) << (8 * k);
-        }
-        if (q8) reinterpret_cast<uint2*>(q8 + row * 128)[hl] = make_uint2(lo, hi);
-        if (xg) reinterpret_cast<uint2*>(xg)[hl] = make_uint2(lo, hi);
+        const uint32_t w0 = __byte_perm(ev, od, 0x5140), w1 = __byte_perm(ev, od, 0x7362);
+        if (q8) reinterpret_cast<uint2*>(q8 + row * 128)[hl] = make_uint2(w0, w1);
+        if (xg) reinterpret_cast<uint2*>(xg)[hl] = make_uint2(w0, w1);
       }
       if (hl == 0) scales[static_cast<int64_t>(t) * rows + row] = s;
     }

@@ -39,3 +39,15 @@ ts.sort()
 us = ts[len(ts) // 2] * 1e3
 print(f"{cfg} mode={os.environ.get('ATOM_GEMM_PROBE_MODE', '0')} gemm {us:.1f} us  "
       f"{2 * M * N * K / us / 1e6:.0f} TOPS")
+xd = torch.from_numpy(X).cuda()
+qt = []
+for _ in range(10):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    atom.reorder_quantize(xd, pd, out=aq)
+    e1.record()
+    torch.cuda.synchronize()
+    qt.append(e0.elapsed_time(e1))
+qt.sort()
+print(f"{cfg} quantize {qt[len(qt) // 2] * 1e3:.1f} us")
