@@ -60,7 +60,6 @@ constexpr int kEpiPerQuarter = kNumEpiWarps / 4;   // warps sharing one TMEM lan
 constexpr int kEpiThreads = kNumEpiWarps * 32;
 constexpr int kRegsLow = 56, kRegsHigh = 200;           // 8*32*56 + 8*32*200 = 65536
 constexpr int kTileN = 128;     // output channels per tile (MMA M)
-constexpr int kSRing = 8;       // group-scale ring depth
 
 template <int BT> struct Cfg {
   static constexpr int RT = BT >= 256 ? 2 : 4;          // TMEM accumulator buffers
@@ -96,6 +95,11 @@ struct GemmParams {
   long long* trace;          // development timeline probe (ATOM_GEMM_TRACE): [8][kTraceN] clocks
 };
 constexpr int kTraceN = 512;
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 // development probe: clock64 of event ev for group g of CTA 0 (no-op unless p.trace is set)
 #define TRACE(ev, g)                                                                          \
   do {                                                                                        \
@@ -111,8 +115,8 @@ struct __align__(1024) GemmSmem {
   uint8_t ubuf_w[RW][kTileN * 128];     // unpacked weight group, SW128 K-major
   uint8_t ubuf_a[RS][BT * 128];         // activation group (x8), SW128 K-major, written by TMA
   uint8_t stage_w[Cfg<BT>::kStages][kTileN * 64];   // packed weight group (or INT8 half)
-  float ssw[kSRing][kTileN];            // weight scales of a group (ring, filled by cp.async)
-  float ssa[kSRing][BT];                // activation scales of a group
+  float ssw[RS][kTileN];                // weight scales of group g in slot g % RS (cp.async)
+  float ssa[RS][BT];                    // activation scales of the same group
   uint8_t ostg[kNumEpiWarps][1024];     // per-warp output staging ([8 tokens][32 ch] fp32)
   uint64_t full[Cfg<BT>::kStages], empty[Cfg<BT>::kStages];
   // go[u]: group g (slot u = g % RS) may be issued -- its weights are unpacked (2 arrivals),
@@ -120,7 +124,7 @@ struct __align__(1024) GemmSmem {
   // arrivals, made when group g - RT was released).  One barrier, one probe per group.
   uint64_t go[RS];
   uint64_t mdone[RS];                   // MMAs of a group done: slot free + partial ready
-  uint64_t sready[kSRing], sfree[kSRing];
+  uint64_t sfree[RS];                   // epilogue done with the scales in slot g % RS
   uint32_t tmem_base;
 };
 
@@ -296,6 +300,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (p.trace != nullptr && threadIdx.x == 0)
+    p.trace[8 * kTraceN + blockIdx.x * 4 + 0] = globaltimer_ns();
   // waits on the MMA <-> epilogue critical loop: spin (bit 7 of kMode: suspend-hinted instead)
   auto wait_hot = [](uint64_t* bar, uint32_t parity) {
     if constexpr ((kMode & 128) != 0) mbar_wait(bar, parity);
@@ -308,13 +314,11 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       mbar_init(&sm.empty[s], kNumUnpackWarps);
     }
     for (int u = 0; u < RS; ++u) {
-      mbar_init(&sm.go[u], kNumUnpackWarps + 1 + kNumEpiWarps);   // unpack, A tile, epilogue
+      // unpack warps, activation tile, epilogue release, group scales (32 cp.async lanes)
+      mbar_init(&sm.go[u], kNumUnpackWarps + 1 + kNumEpiWarps + 32);   // unpack, A tile, epilogue
       mbar_init(&sm.mdone[u], 1);
     }
-    for (int r = 0; r < kSRing; ++r) {
-      mbar_init(&sm.sready[r], 32);  // one cp.async-arrive per producer-warp thread
-      mbar_init(&sm.sfree[r], kNumEpiWarps);
-    }
+    for (int r = 0; r < RS; ++r) mbar_init(&sm.sfree[r], kNumEpiWarps);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -337,7 +341,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     // Not tied to the operand slots, so the weight stream runs up to KS stages ahead of the
     // unpack warps.  (Activation tiles have their own loader warp.)
     Ring<KS> st;
-    Ring<kSRing> sr;
+    Ring<RS> sr;
     int gp = 0;
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
@@ -352,7 +356,9 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           // rows past M: any finite scale works, their partials are exactly zero (TMA
           // zero-fills out-of-range activation rows) and they are never stored
           cp_async_4(&sm.ssa[sr.i][j], as + min(w.m0 + j, p.M - 1));
-        cp_async_mbar_arrive(&sm.sready[sr.i]);
+        // the scales complete group g's go barrier: the MMA (and hence the epilogue, which
+        // waits for the MMA) never sees the group before they landed
+        cp_async_mbar_arrive(&sm.go[sr.i]);
         const int nh = t < G4 ? 1 : 2;      // the INT8 outlier group arrives in two halves
         for (int h = 0; h < nh; ++h, st.next()) {
           mbar_wait(&sm.empty[st.i], st.ph ^ 1);
@@ -502,7 +508,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     uint8_t* stg = sm.ostg[e];           // per-warp staging for the transposed output
     Ring<RS> u;
     Ring<RT> b;
-    Ring<kSRing> sr;
+    Ring<RS> sr;
     int ge = 0;
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
@@ -513,8 +519,11 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       for (int j = 0; j < NCOL; ++j) acc[j] = 0.0f;
       for (int t = w.t0; t < w.t1; ++t, u.next(), b.next(), sr.next(), ++ge) {
         const bool int4 = t < G4;
-        wait_hot(&sm.sready[sr.i], sr.ph);
         if (a_issuer) TRACE(5, ge);
+        wait_hot(&sm.mdone[u.i], u.ph);      // also implies the group's scales have landed
+        if (a_issuer) TRACE(6, ge);
+        if (p.trace != nullptr && a_issuer && ge == 0)
+          p.trace[8 * kTraceN + blockIdx.x * 4 + 1] = globaltimer_ns();
         // sw' = sw (x1/16 for INT4 groups, exact) with its 2 lowest mantissa bits cleared so
         // that 1.5*2^23*sw' is exact; see DESIGN.md "Epilogue arithmetic".
         float sw = sm.ssw[sr.i][n_local];
@@ -523,8 +532,6 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         const float2 sw2 = make_float2(swh, swh);
         const float2 nc2 = make_float2(-kMagic * swh, -kMagic * swh);
         const float* sa = &sm.ssa[sr.i][col0];
-        wait_hot(&sm.mdone[u.i], u.ph);
-        if (a_issuer) TRACE(6, ge);
         tc_fence_after();
         const uint32_t taddr = tq + b.i * BT;
         const uint32_t go_next = u.i + RT >= RS ? u.i + RT - RS : u.i + RT;   // slot of g + RT
@@ -690,8 +697,12 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     }
   }
 
+  if (p.trace != nullptr && threadIdx.x == kEpiWarp0 * 32)
+    p.trace[8 * kTraceN + blockIdx.x * 4 + 2] = globaltimer_ns();
   tc_fence_before();
   __syncthreads();
+  if (p.trace != nullptr && threadIdx.x == 0)
+    p.trace[8 * kTraceN + blockIdx.x * 4 + 3] = globaltimer_ns();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -823,13 +834,14 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
   if (e != cudaSuccess) return e;
   static long long* trace = nullptr;
   static const bool want_trace = getenv("ATOM_GEMM_TRACE") != nullptr;   // development only
-  if (want_trace && trace == nullptr) cudaMalloc(&trace, 8 * kTraceN * sizeof(long long));
+  constexpr size_t kTraceBytes = (8 * kTraceN + 4 * 1024) * sizeof(long long);
+  if (want_trace && trace == nullptr) cudaMalloc(&trace, kTraceBytes);
   p.trace = want_trace ? trace : nullptr;
-  if (want_trace) cudaMemsetAsync(trace, 0, 8 * kTraceN * sizeof(long long), stream);
+  if (want_trace) cudaMemsetAsync(trace, 0, kTraceBytes, stream);
   kern<<<plan.grid, kThreads, smem, stream>>>(m_wq4, m_wq8, m_ax8, p);
   ++*launches;
   if (want_trace) {
-    static long long h[8 * kTraceN];
+    static long long h[8 * kTraceN + 4 * 1024];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "plan: BT=%d grid=%d dp_waves=%d sk_units=%lld tiles=%d\n", BT, plan.grid,
             plan.dp_waves, static_cast<long long>(plan.sk_units), p.num_tiles);
@@ -841,6 +853,14 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
               h[kTraceN + g] - t0, h[2 * kTraceN + g] - t0, h[3 * kTraceN + g] - t0,
               h[4 * kTraceN + g] - t0, h[5 * kTraceN + g] - t0, h[6 * kTraceN + g] - t0,
               h[7 * kTraceN + g] - t0);
+    }
+    long long c0 = h[8 * kTraceN];
+    for (int b = 0; b < plan.grid; ++b) c0 = h[8 * kTraceN + 4 * b] < c0 ? h[8 * kTraceN + 4 * b] : c0;
+    fprintf(stderr, "cta: start first_mdone epi_done end (ns rel. to first start)\n");
+    for (int b = 0; b < plan.grid; ++b) {
+      const long long* q = h + 8 * kTraceN + 4 * b;
+      fprintf(stderr, "%3d %7lld %7lld %7lld %7lld\n", b, q[0] - c0, q[1] - c0, q[2] - c0,
+              q[3] - c0);
     }
   }
   return cudaGetLastError();
