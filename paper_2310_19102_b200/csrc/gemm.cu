@@ -305,7 +305,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   // waits on the MMA <-> epilogue critical loop: spin (bit 7 of kMode: suspend-hinted instead)
   auto wait_hot = [](uint64_t* bar, uint32_t parity) {
     if constexpr ((kMode & 128) != 0) mbar_wait(bar, parity);
-    else mbar_wait_spin(bar, parity);
+    else if constexpr ((kMode & 4096) != 0) mbar_wait_spin(bar, parity);
+    else mbar_wait_test(bar, parity);
   };
 
   if (threadIdx.x == 0) {
@@ -343,6 +344,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     Ring<KS> st;
     Ring<RS> sr;
     int gp = 0;
+    const uint64_t pol_w = l2_policy_evict_first();
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
       for (int t = w.t0; t < w.t1; ++t, sr.next(), ++gp) {
@@ -359,6 +361,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         // the scales complete group g's go barrier: the MMA (and hence the epilogue, which
         // waits for the MMA) never sees the group before they landed
         cp_async_mbar_arrive(&sm.go[sr.i]);
+        if (lane == 0) TRACE(2, gp);
         const int nh = t < G4 ? 1 : 2;      // the INT8 outlier group arrives in two halves
         for (int h = 0; h < nh; ++h, st.next()) {
           mbar_wait(&sm.empty[st.i], st.ph ^ 1);
@@ -368,8 +371,11 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
               mbar_arrive(&sm.full[st.i]);
             } else {
               mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
-              if (t < G4) tma_load_2d(sm.stage_w[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0);
-              else tma_load_2d(sm.stage_w[st.i], &tm_wq8, &sm.full[st.i], h * 64, w.n0);
+              // weights: read by the 4 CTAs sharing the n-tile at about the same time, then dead
+              if (t < G4)
+                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
+              else
+                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq8, &sm.full[st.i], h * 64, w.n0, pol_w);
             }
           }
           __syncwarp();
@@ -382,15 +388,19 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     // group g (x8, TMA, SWIZZLE_128B straight into the operand slot) is issued right then.
     if (lane == 0) {
       Ring<RS> u;
+      const uint64_t pol_a = l2_policy_evict_last();
+      int ga = 0;
       for (int k = 0; k < n_items; ++k) {
         const Item w = get_item<BT>(p, sch, k);
-        for (int t = w.t0; t < w.t1; ++t, u.next()) {
+        for (int t = w.t0; t < w.t1; ++t, u.next(), ++ga) {
           wait_hot(&sm.mdone[u.i], u.ph ^ 1);
           if constexpr ((kMode & 16) != 0) {
             mbar_arrive(&sm.go[u.i]);
           } else {
             mbar_arrive_expect_tx(&sm.go[u.i], BT * 128);
-            tma_load_2d(sm.ubuf_a[u.i], &tm_ax8, &sm.go[u.i], t * 128, w.m0);
+            // activations: re-read by every n-tile, keep them in L2
+            TRACE(1, ga);
+            tma_load_2d_hint(sm.ubuf_a[u.i], &tm_ax8, &sm.go[u.i], t * 128, w.m0, pol_a);
           }
         }
       }
@@ -826,6 +836,7 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
       case 627: kern = w4a4_gemm_kernel<BT, false, 627>; break;
       case 515: kern = w4a4_gemm_kernel<BT, false, 515>; break;
       case 512: kern = w4a4_gemm_kernel<BT, false, 512>; break;
+      case 4096: kern = w4a4_gemm_kernel<BT, false, 4096>; break;
       default: break;
     }
   }
@@ -845,7 +856,7 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "plan: BT=%d grid=%d dp_waves=%d sk_units=%lld tiles=%d\n", BT, plan.grid,
             plan.dp_waves, static_cast<long long>(plan.sk_units), p.num_tiles);
-    fprintf(stderr, "g   W_tma  mma_tempty mma_ufull mma_afull unp_done epi_sready epi_mdone epi_tempty\n");
+    fprintf(stderr, "g   W_tma  A_issue scales_issue mma_issue unp_done epi_top epi_mdone epi_release\n");
     const long long t0 = h[0];
     for (int g = 0; g < kTraceN && (g < 40 || g % 25 == 0); ++g) {
       if (h[3 * kTraceN + g] == 0) break;

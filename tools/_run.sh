@@ -1,3 +1,4 @@
-timeout 30 python tools/shape_check.py 16 1024 1024; echo rc=$?
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "gemm or workspace or shard" 2>&1 | tail -1
-for c in cfg5 cfg2; do timeout 60 python tools/gemm_probe.py $c 2>&1 | head -1; done
+for m in 0 4096; do ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg5 > /tmp/o.txt 2>&1; head -1 /tmp/o.txt; done
+timeout 60 python tools/gemm_probe.py cfg2 2>&1 | head -1
+ATOM_GEMM_TRACE=1 timeout 60 python tools/gemm_probe.py cfg5 > gpurun_out/trace5_p.log 2>&1
+grep -A45 "^g " gpurun_out/trace5_p.log | tail -5
