@@ -44,14 +44,15 @@
 namespace atom {
 
 // Warp roles (16 warps, 4 warpgroups):
-//   WG0: warp 0 producer (scales via cp.async, packed weights via TMA), warp 1 MMA issuer,
-//        warp 2 activation-tile loader (TMA), warp 3 idle
+//   WG0: warp 0 packed-weight producer (TMA), warp 1 MMA issuer, warp 2 activation-tile
+//        loader (TMA), warp 3 group-scale loader (cp.async)
 //   WG1: warps 4-7 unpack (one per SM sub-partition, so it never queues behind 2 others)
 //   WG2-WG3: warps 8-15 epilogue (warp % 4 = TMEM lane quarter, (warp - 8) / 4 = column half)
 // setmaxnreg moves registers from WG0/WG1 (56 each) to the epilogue warpgroups (200 each),
 // which hold the fp32 accumulators of a 128 x BT tile (BT/2 per thread).
 constexpr int kThreads = 512;
 constexpr int kALoaderWarp = 2;
+constexpr int kScaleWarp = 3;
 constexpr int kUnpackWarp0 = 4;
 constexpr int kNumUnpackWarps = 4;
 constexpr int kEpiWarp0 = 8;
@@ -338,13 +339,41 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 
   if (warp < kEpiWarp0) setmaxnreg_dec<kRegsLow>();
   if (warp == 0) {
-    // ===================== producer warp: group scales (cp.async) + packed weights (TMA) =====
-    // Not tied to the operand slots, so the weight stream runs up to KS stages ahead of the
-    // unpack warps.  (Activation tiles have their own loader warp.)
-    Ring<KS> st;
+    // ===================== producer warp: packed weights (TMA) =====================
+    // Not tied to the operand or scale slots, so the weight stream runs up to KS stages ahead
+    // of the unpack warps.
+    if (lane == 0) {
+      Ring<KS> st;
+      int gp = 0;
+      const uint64_t pol_w = l2_policy_evict_first();
+      for (int k = 0; k < n_items; ++k) {
+        const Item w = get_item<BT>(p, sch, k);
+        for (int t = w.t0; t < w.t1; ++t, ++gp) {
+          const int nh = t < G4 ? 1 : 2;      // the INT8 outlier group arrives in two halves
+          for (int h = 0; h < nh; ++h, st.next()) {
+            mbar_wait(&sm.empty[st.i], st.ph ^ 1);
+            if (h == 0) TRACE(0, gp);
+            if constexpr ((kMode & 32) != 0) {
+              mbar_arrive(&sm.full[st.i]);
+            } else {
+              mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
+              // weights: read by the 4 CTAs sharing the n-tile at about the same time, then dead
+              if (t < G4)
+                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
+              else
+                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq8, &sm.full[st.i], h * 64, w.n0, pol_w);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == kScaleWarp) {
+    // ===================== scale loader warp: group scales (cp.async) =====================
+    // The scales complete group g's go barrier: the MMA (and hence the epilogue, which waits
+    // for the MMA) never sees a group before its scales landed.  Slot g % RS is reused once
+    // the epilogue is done with group g - RS.
     Ring<RS> sr;
     int gp = 0;
-    const uint64_t pol_w = l2_policy_evict_first();
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
       for (int t = w.t0; t < w.t1; ++t, sr.next(), ++gp) {
@@ -358,28 +387,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           // rows past M: any finite scale works, their partials are exactly zero (TMA
           // zero-fills out-of-range activation rows) and they are never stored
           cp_async_4(&sm.ssa[sr.i][j], as + min(w.m0 + j, p.M - 1));
-        // the scales complete group g's go barrier: the MMA (and hence the epilogue, which
-        // waits for the MMA) never sees the group before they landed
         cp_async_mbar_arrive(&sm.go[sr.i]);
         if (lane == 0) TRACE(2, gp);
-        const int nh = t < G4 ? 1 : 2;      // the INT8 outlier group arrives in two halves
-        for (int h = 0; h < nh; ++h, st.next()) {
-          mbar_wait(&sm.empty[st.i], st.ph ^ 1);
-          if (lane == 0) {
-            if (h == 0) TRACE(0, gp);
-            if constexpr ((kMode & 32) != 0) {
-              mbar_arrive(&sm.full[st.i]);
-            } else {
-              mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
-              // weights: read by the 4 CTAs sharing the n-tile at about the same time, then dead
-              if (t < G4)
-                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
-              else
-                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq8, &sm.full[st.i], h * 64, w.n0, pol_w);
-            }
-          }
-          __syncwarp();
-        }
       }
     }
   } else if (warp == kALoaderWarp) {

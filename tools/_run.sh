@@ -1,4 +1,3 @@
-for m in 0 4096; do ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg5 > /tmp/o.txt 2>&1; head -1 /tmp/o.txt; done
-timeout 60 python tools/gemm_probe.py cfg2 2>&1 | head -1
-ATOM_GEMM_TRACE=1 timeout 60 python tools/gemm_probe.py cfg5 > gpurun_out/trace5_p.log 2>&1
-grep -A45 "^g " gpurun_out/trace5_p.log | tail -5
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "gemm or workspace or shard" 2>&1 | tail -1 > gpurun_out/t.txt
+for c in cfg5 cfg2 cfg4; do timeout 60 python tools/gemm_probe.py $c 2>&1 | head -1 >> gpurun_out/t.txt; done
+cat gpurun_out/t.txt
