@@ -1,3 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "gemm or workspace or shard" 2>&1 | tail -1 > gpurun_out/t.txt
-for c in cfg5 cfg2 cfg4; do timeout 60 python tools/gemm_probe.py $c 2>&1 | head -1 >> gpurun_out/t.txt; done
+for m in 115 8307; do ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg2 2>&1 | head -1; ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg5 2>&1 | head -1; done > gpurun_out/t.txt
 cat gpurun_out/t.txt
