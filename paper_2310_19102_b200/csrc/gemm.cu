@@ -146,6 +146,14 @@ __device__ __forceinline__ uint4 unpack_hi(uint4 v) {  // odd channels -> 16*q b
 __device__ __forceinline__ float biased(uint32_t r, uint32_t magic) {
   return __uint_as_float(and_xor(r, 0x007FFFFFu, magic));
 }
+// The same value as an integer multiply-add, R * 1 + 0x4B400000 (= the LOP3 result for
+// |R| < 2^22), which issues to the FMA pipe instead of the ALU pipe; `one` is an opaque 1 so
+// ptxas keeps the IMAD.  Used for part of the columns to balance the two pipes.
+__device__ __forceinline__ float biased_fma(uint32_t r, uint32_t one, uint32_t magic) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(r), "r"(one), "r"(magic));
+  return __uint_as_float(d);
+}
 
 // KR rows of the weight tile, ROW_STEP apart (a multiple of 8, so all share one swizzle phase):
 // packed stage [rows][64 B] -> unpacked SW128 [rows][128 B].  This thread owns the 16-byte
@@ -503,6 +511,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     const int col0 = 8 * (third * kBase + (third < kRem ? third : kRem));
     const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + col0;
     const uint32_t magic = kMagicBits;
+    uint32_t one = 1u;
+    asm volatile("" : "+r"(one));        // opaque to ptxas (see biased_fma)
     const bool a_issuer = e == 0 && lane == 0;
     const int n_local = q * 32 + lane;   // output channel within the tile
     uint32_t mg[8];                      // resident tcgen05.st sources for the magic re-arm
@@ -593,7 +603,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                 uint32_t* rv = r[bi & 1] + jj;
                 if constexpr (!kPre) {
 #pragma unroll
-                  for (int v = 0; v < 4; ++v) rv[v] = __float_as_uint(biased(rv[v], magic));
+                  for (int v = 0; v < 4; ++v)
+                    rv[v] = __float_as_uint(((kMode & 8192) == 0 && (jj & 4) != 0)
+                                                ? biased_fma(rv[v], one, magic)
+                                                : biased(rv[v], magic));
                 }
                 if constexpr (kDebug) {
 #pragma unroll
@@ -846,6 +859,7 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
       case 515: kern = w4a4_gemm_kernel<BT, false, 515>; break;
       case 512: kern = w4a4_gemm_kernel<BT, false, 512>; break;
       case 4096: kern = w4a4_gemm_kernel<BT, false, 4096>; break;
+      case 8192: kern = w4a4_gemm_kernel<BT, false, 8192>; break;
       default: break;
     }
   }

@@ -1,2 +1,2 @@
-for m in 115 8307; do ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg2 2>&1 | head -1; ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg5 2>&1 | head -1; done > gpurun_out/t.txt
+for m in 0 8192; do ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg5 2>&1 | head -1; done > gpurun_out/t.txt
 cat gpurun_out/t.txt
