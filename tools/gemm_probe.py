@@ -14,7 +14,10 @@ import synth  # noqa: E402
 from bench import CONFIGS  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
-M, N, K, _ = CONFIGS[cfg]
+if "," in cfg:                       # an explicit shape "M,N,K"
+    M, N, K = (int(v) for v in cfg.split(","))
+else:
+    M, N, K, _ = CONFIGS[cfg]
 X, perm = synth.activations(M, K, 0), synth.perm_for(K, 0)
 W = synth.weights(N, K, 0)
 pd = torch.from_numpy(perm).cuda()
