@@ -396,7 +396,6 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           // zero-fills out-of-range activation rows) and they are never stored
           cp_async_4(&sm.ssa[sr.i][j], as + min(w.m0 + j, p.M - 1));
         cp_async_mbar_arrive(&sm.go[sr.i]);
-        if (lane == 0) TRACE(2, gp);
       }
     }
   } else if (warp == kALoaderWarp) {
@@ -482,6 +481,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         const int nh = int4 ? 1 : 2;
         for (int h = 0; h < nh; ++h, st.next()) {
           wait_hot(&sm.full[st.i], st.ph);
+          if (ut == 0 && h == 0) TRACE(2, gu);
           if constexpr ((kMode & 64) == 0)
             unpack_rows<4, 32>(sm.stage_w[st.i], sm.ubuf_w[uw.i], r0, c, int4, h);
           __syncwarp();
@@ -843,22 +843,12 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
       case 3: kern = w4a4_gemm_kernel<BT, false, 3>; break;
       case 4: kern = w4a4_gemm_kernel<BT, false, 4>; break;
       case 8: kern = w4a4_gemm_kernel<BT, false, 8>; break;
-      case 11: kern = w4a4_gemm_kernel<BT, false, 11>; break;
-      case 19: kern = w4a4_gemm_kernel<BT, false, 19>; break;
-      case 35: kern = w4a4_gemm_kernel<BT, false, 35>; break;
-      case 51: kern = w4a4_gemm_kernel<BT, false, 51>; break;
-      case 67: kern = w4a4_gemm_kernel<BT, false, 67>; break;
+      case 16: kern = w4a4_gemm_kernel<BT, false, 16>; break;
+      case 32: kern = w4a4_gemm_kernel<BT, false, 32>; break;
+      case 64: kern = w4a4_gemm_kernel<BT, false, 64>; break;
       case 115: kern = w4a4_gemm_kernel<BT, false, 115>; break;
-      case 119: kern = w4a4_gemm_kernel<BT, false, 119>; break;
-      case 117: kern = w4a4_gemm_kernel<BT, false, 117>; break;
-      case 128: kern = w4a4_gemm_kernel<BT, false, 128>; break;
-      case 131: kern = w4a4_gemm_kernel<BT, false, 131>; break;
-      case 243: kern = w4a4_gemm_kernel<BT, false, 243>; break;
-      case 371: kern = w4a4_gemm_kernel<BT, false, 371>; break;
-      case 627: kern = w4a4_gemm_kernel<BT, false, 627>; break;
-      case 515: kern = w4a4_gemm_kernel<BT, false, 515>; break;
       case 512: kern = w4a4_gemm_kernel<BT, false, 512>; break;
-      case 4096: kern = w4a4_gemm_kernel<BT, false, 4096>; break;
+      case 1024: kern = w4a4_gemm_kernel<BT, false, 1024>; break;
       case 8192: kern = w4a4_gemm_kernel<BT, false, 8192>; break;
       default: break;
     }
@@ -879,7 +869,7 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "plan: BT=%d grid=%d dp_waves=%d sk_units=%lld tiles=%d\n", BT, plan.grid,
             plan.dp_waves, static_cast<long long>(plan.sk_units), p.num_tiles);
-    fprintf(stderr, "g   W_tma  A_issue scales_issue mma_issue unp_done epi_top epi_mdone epi_release\n");
+    fprintf(stderr, "g   W_tma  A_issue W_landed mma_issue unp_done epi_top epi_mdone epi_release\n");
     const long long t0 = h[0];
     for (int g = 0; g < kTraceN && (g < 40 || g % 25 == 0); ++g) {
       if (h[3 * kTraceN + g] == 0) break;
