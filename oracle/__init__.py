@@ -49,6 +49,8 @@ def lib():
         L.oracle_group_partials.argtypes = [P, P, P, P, i64, i64, i64, i32, P]
         L.oracle_gemm_output.argtypes = [P, P, P, i64, i64, i64, P]
         L.oracle_output_rows.argtypes = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, P]
+        L.oracle_rmsnorm_rows.argtypes = [P, i64, i64, i64, P, f32, P]
+        L.oracle_rmsnorm_rows.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_max_threads.restype = ctypes.c_int
         for f in (L.oracle_quantize_rows, L.oracle_group_partials, L.oracle_gemm_output,
@@ -99,6 +101,29 @@ def quantize_rows(x, perm, K: int, k_outlier: int = 128, clip_int4: float = 0.9,
                                     _ptr(q4), _ptr(q8), _ptr(sc))
     _check(st, "oracle_quantize_rows")
     return q4, q8, sc
+
+
+def rmsnorm_rows(x, gamma, eps: float = 1e-6, C: int = None):
+    """N1: fp16 RMSNorm of every row of x over its first C channels (default: all), pinned as
+    documented in atom_oracle.c; returns fp16 [rows][C] (the fp32 result rounded to nearest-even
+    by numpy's float32 -> float16 conversion)."""
+    x32 = np.ascontiguousarray(np.asarray(x).astype(np.float32))
+    rows, ldx = x32.shape
+    C = ldx if C is None else int(C)
+    g32 = np.ascontiguousarray(np.asarray(gamma).astype(np.float32))
+    assert g32.shape == (C,)
+    y32 = np.zeros((rows, C), dtype=np.float32)
+    st = lib().oracle_rmsnorm_rows(_ptr(x32), rows, ldx, C, _ptr(g32), ctypes.c_float(eps),
+                                   _ptr(y32))
+    _check(st, "oracle_rmsnorm_rows")
+    return y32.astype(np.float16)
+
+
+def rmsnorm_quantize_rows(x, gamma, perm, K: int, k_outlier: int = 128, eps: float = 1e-6,
+                          clip_int4: float = 0.9, clip_int8: float = 1.0):
+    """N1 followed by O2-O6: what the fused RMSNorm + reorder + quantize kernel must produce."""
+    y = rmsnorm_rows(x, gamma, eps)
+    return quantize_rows(y, perm, K, k_outlier, clip_int4, clip_int8)
 
 
 def group_partials(a_q4, a_q8, w_q4, w_q8, M: int, N: int, K: int, k_outlier: int = 128):

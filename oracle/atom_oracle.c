@@ -151,6 +151,37 @@ int oracle_quantize_rows(const float* x, int64_t rows, int64_t ldx, const int32_
   return ORC_OK;
 }
 
+/*
+ * N1 (NEXT-1, the "prior operator" the paper fuses reordering and quantization into: "fuses
+ * the activation matrix reordering operators into the prior operator", "we fuse the
+ * quantization operator into the prior operator (e.g., LayerNorm)").  The paper does not define
+ * the norm; the Llama models it evaluates use RMSNorm (reading G19):
+ *     y_c = x_c / sqrt(mean_c(x_c^2) + eps) * gamma_c,   c in [0, C)
+ * with the arithmetic pinned as follows (x and gamma are fp16 values widened exactly to fp32):
+ *     ss = sum_c (double)x_c * (double)x_c      (each square exact in double; c ascending)
+ *     r  = RN32( 1.0 / sqrt(ss / C + (double)eps) )   (double ops, one final rounding to fp32)
+ *     y_c = RN32( RN32(x_c * r) * gamma_c )      (two binary32 multiplies, in this order)
+ * The caller rounds y to fp16 (round-to-nearest-even) before the quantizer, as an fp16 RMSNorm
+ * layer followed by a quantized linear layer would.  Output: y32 fp32 [rows][C].
+ */
+int oracle_rmsnorm_rows(const float* x, int64_t rows, int64_t ldx, int64_t C, const float* gamma,
+                        float eps, float* y32) {
+  if (!x || !gamma || !y32) return ORC_ERR_NULL;
+  if (C <= 0 || C > ldx || !(eps >= 0.0f)) return ORC_ERR_ARG;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    const float* xr = x + r * ldx;
+    double ss = 0.0;
+    for (int64_t c = 0; c < C; ++c) ss += (double)xr[c] * (double)xr[c];
+    const float rinv = (float)(1.0 / sqrt(ss / (double)C + (double)eps));
+    for (int64_t c = 0; c < C; ++c) {
+      const float t = xr[c] * rinv;              /* one IEEE multiply */
+      y32[r * C + c] = t * gamma[c];             /* one IEEE multiply */
+    }
+  }
+  return ORC_OK;
+}
+
 /* Decode one signed nibble (two's complement). */
 static int oracle_nibble(uint8_t byte, int high) {
   int v = high ? (byte >> 4) & 0xF : byte & 0xF;

@@ -469,3 +469,71 @@ def test_oracle_rejects_bad_shapes():
         oracle.quantize_rows(x, np.arange(256), 256, 64)         # k_o not in {0,128}
     with pytest.raises(oracle.OracleError):
         oracle.quantize_rows(x, np.arange(256), 256, 128, clip_int4=1.5)
+
+
+# ----------------------------------------------------------------------------------------------
+# N1 (NEXT-1): RMSNorm, the prior operator the paper fuses reorder + quantize into
+# ----------------------------------------------------------------------------------------------
+def test_n1_single_nonzero_closed_form():
+    """x = [v, 0, ..., 0], gamma = 1, eps = 0 over C = 1024 channels: mean(x^2) = v^2/1024, so
+    y_0 = v / (|v|/32) = 32*sign(v) exactly (powers of two) and every other y_c = 0.  Catches a
+    sum instead of a mean (y_0 = 1), a missing square root (y_0 = 1024/v) and dropped channels."""
+    C = 1024
+    for v in (4.0, -0.25, 1024.0):
+        x = np.zeros((1, C), np.float16)
+        x[0, 5] = v
+        y = oracle.rmsnorm_rows(x, np.ones(C, np.float16), eps=0.0)
+        want = np.zeros((1, C), np.float16)
+        want[0, 5] = 32.0 * np.sign(v)
+        np.testing.assert_array_equal(y, want)
+
+
+def test_n1_constant_row_and_gamma():
+    """A constant row normalizes to +-1 times gamma; gamma is applied per channel (a
+    power-of-two gamma gives an exact power-of-two output)."""
+    C = 256
+    g = (2.0 ** (np.arange(C) % 7 - 3)).astype(np.float16)
+    for a in (3.0, -0.5):
+        x = np.full((2, C), a, np.float16)
+        y = oracle.rmsnorm_rows(x, g, eps=0.0)
+        np.testing.assert_array_equal(y, np.tile(np.sign(a) * g, (2, 1)).astype(np.float16))
+
+
+def test_n1_pow2_scale_invariance():
+    """RMSNorm(2^k x) == RMSNorm(x) bit for bit when eps = 0 (every pinned operation commutes
+    with exact power-of-two scaling)."""
+    rng = np.random.default_rng(3)
+    # magnitudes in [0.5, 4): inputs and outputs stay fp16-normal under the 2^k scalings
+    x = (np.sign(rng.standard_normal((8, 512))) * rng.uniform(0.5, 4, (8, 512))).astype(np.float16)
+    g = (1 + 0.1 * rng.standard_normal(512)).astype(np.float16)
+    y = oracle.rmsnorm_rows(x, g, eps=0.0)
+    for k in (-3, 2):
+        np.testing.assert_array_equal(oracle.rmsnorm_rows(x * np.float16(2.0 ** k), g, 0.0), y)
+
+
+def test_n1_eps_and_float64_reference():
+    """Against a float64 textbook RMSNorm: within fp16 rounding (plus the fp32 steps); eps counts
+    (tiny inputs with eps = 1 are left almost unscaled)."""
+    rng = np.random.default_rng(4)
+    x = (rng.standard_normal((16, 768)) * np.exp(rng.standard_normal((16, 1)))).astype(np.float16)
+    g = (1 + 0.2 * rng.standard_normal(768)).astype(np.float16)
+    eps = 1e-6
+    x64, g64 = x.astype(np.float64), g.astype(np.float64)
+    ref = x64 / np.sqrt((x64 ** 2).mean(1, keepdims=True) + eps) * g64
+    y = oracle.rmsnorm_rows(x, g, eps).astype(np.float64)
+    assert np.all(np.abs(y - ref) <= 2.0 ** -10 * np.abs(ref) + 2.0 ** -24)
+    tiny = np.full((1, 128), 1e-3, np.float16)
+    yt = oracle.rmsnorm_rows(tiny, np.ones(128, np.float16), eps=1.0).astype(np.float64)
+    assert np.allclose(yt, 1e-3 / np.sqrt(1.0 + 1e-6), rtol=2e-3)
+
+
+def test_n1_fused_oracle_is_norm_then_quantize():
+    rng = np.random.default_rng(5)
+    K = 1024
+    x = rng.standard_normal((6, K)).astype(np.float16)
+    g = (1 + 0.1 * rng.standard_normal(K)).astype(np.float16)
+    perm = synth.perm_for(K, seed=5)
+    a = oracle.rmsnorm_quantize_rows(x, g, perm, K)
+    b = oracle.quantize_rows(oracle.rmsnorm_rows(x, g), perm, K)
+    for u, v in zip(a, b):
+        np.testing.assert_array_equal(u, v)
