@@ -377,6 +377,28 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
                "d2h_bytes_per_step": int(P * c_h.numel() * c_h.element_size()),
                "ms_per_step": e_ms}
 
+    # ---------------- NEXT-1: the fused RMSNorm + reorder + quantize kernel (not in the step) ----
+    norm_us = None
+    if not args.no_graph and P == 1:
+        gamma = torch.from_numpy(
+            (1 + 0.1 * np.random.default_rng(args.seed).standard_normal(K)).astype(np.float16)).to(dev)
+        g_norm = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            atom.rmsnorm_reorder_quantize(xd, gamma, layer.perm, out=aq)
+            with torch.cuda.graph(g_norm, stream=side):
+                atom.rmsnorm_reorder_quantize(xd, gamma, layer.perm, out=aq)
+        torch.cuda.current_stream().wait_stream(side)
+        en = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(10)]
+        for i in range(10):
+            flush_l2()
+            en[i][0].record()
+            g_norm.replay()
+            en[i][1].record()
+        torch.cuda.synchronize()
+        norm_us = 1e3 * sum(a.elapsed_time(b) for a, b in en) / len(en)
+
     if rank != 0:
         return
     peaks, peak_src = load_peaks()
@@ -417,6 +439,10 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
             "reorder_quantize": {"us": q_avg * 1e3, "GB/s": qb / (q_avg * 1e-3) / 1e9,
                                  "frac_hbm": qb / (q_avg * 1e-3) / 1e9 / peaks["hbm_gbs"]},
             "w4a4_gemm": {"us": g_avg * 1e3, "TOPS": achieved},
+            "rmsnorm_reorder_quantize": None if norm_us is None else {
+                "us": norm_us, "GB/s": qb / (norm_us * 1e-6) / 1e9,
+                "note": "NEXT-1 fused RMSNorm + a1 (same bytes as reorder_quantize); not part of "
+                        "the step"},
             "collective": {"us": c_avg * 1e3},
         },
         "gpu_launches": gpu_launches,

@@ -103,6 +103,23 @@ atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
                                     void* stream);
 
 /*
+ * NEXT-1: RMSNorm fused with a1 -- the "prior operator" the paper fuses reordering and
+ * quantization into ("fuses the activation matrix reordering operators into the prior
+ * operator"; "we fuse the quantization operator into the prior operator (e.g., LayerNorm)").
+ * Every row of x_f16 [M][ldx] is first normalized over its ldx channels (the hidden size; rows
+ * must be dense):  y_c = fp16_rn( RN32( RN32(x_c * r) * gamma[c] ) ),
+ *   r = RN32( 1 / sqrt(sum_c x_c^2 / ldx + eps) )   (sum of squares in double, reading G19),
+ * and y is then reordered and quantized exactly as atom_reorder_quantize does (same arguments,
+ * formats and errors).  gamma_f16: fp16 [ldx], device; eps >= 0.  y itself is not written.
+ */
+atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
+                                            const void* gamma_f16, float eps,
+                                            const int32_t* perm, int64_t K, int32_t k_outlier,
+                                            float clip_int4, float clip_int8,
+                                            uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
+                                            void* stream);
+
+/*
  * a0: offline weight reorder + quantize (Fig 4 P:237 "The weight matrix (W) is statically
  * reordered"; P:299 RTN stands in for GPTQ, which only changes the codes offline).  Same math
  * and formats as atom_reorder_quantize with rows = output channels n of W [N][ldw] (nn.Linear

@@ -27,7 +27,8 @@ STATUS_NAMES = {0: "ATOM_OK", 1: "ATOM_ERR_NULL", 2: "ATOM_ERR_SHAPE", 3: "ATOM_
 ATOM_F16, ATOM_F32 = 0, 1
 
 # every symbol include/atom.h declares
-ABI_SYMBOLS = ("atom_reorder_quantize", "atom_quantize_weights", "atom_w4a4_gemm",
+ABI_SYMBOLS = ("atom_reorder_quantize", "atom_rmsnorm_reorder_quantize", "atom_quantize_weights",
+               "atom_w4a4_gemm",
                "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_counter_bytes",
                "atom_validate_perm", "atom_status_string",
                "atom_abi_version", "atom_last_launch_count")
@@ -55,6 +56,9 @@ def _lib():
         q_args = [P, i64, i64, P, i64, i32, f32, f32, P, P, P, P]
         L.atom_reorder_quantize.argtypes = q_args[:10] + [P] + q_args[10:]
         L.atom_quantize_weights.argtypes = q_args
+        L.atom_rmsnorm_reorder_quantize.argtypes = [P, i64, i64, P, f32] + q_args[3:10] + \
+            [P] + q_args[10:]
+        L.atom_rmsnorm_reorder_quantize.restype = ctypes.c_int
         L.atom_w4a4_gemm.argtypes = [P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int,
                                      P, P, ctypes.c_size_t, P]
         L.atom_w4a4_gemm_workspace_size.argtypes = [i64, i64, i64, i32]
@@ -119,7 +123,7 @@ class Quantized:
 
 
 def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream, x8=False,
-              packed=True):
+              packed=True, norm=None):
     import torch
     if x.dtype != torch.float16 or x.dim() != 2 or not x.is_cuda:
         raise TypeError("expected a 2-D CUDA fp16 tensor")
@@ -139,9 +143,18 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
         xx = torch.empty((rows, K), dtype=torch.int8, device=dev) if x8 else None
         out = Quantized(q4, q8, sc, K, k_outlier, xx)
     codes = (_ptr(out.q4), _ptr(out.q8))
-    if fn_name == "atom_reorder_quantize":
+    if fn_name != "atom_quantize_weights":
         codes = codes + (_ptr(out.x8),)
-    st = getattr(_lib(), fn_name)(_ptr(x), rows, ld, _ptr(perm), K, k_outlier,
+    head = (_ptr(x), rows, ld)
+    if norm is not None:                      # (gamma, eps) of the fused RMSNorm
+        gamma, eps = norm
+        if gamma.dtype != torch.float16 or not gamma.is_cuda or gamma.numel() != ld \
+                or not gamma.is_contiguous():
+            raise TypeError("gamma must be a contiguous CUDA fp16 tensor of the row length")
+        if x.stride(0) != x.shape[1]:
+            raise ValueError("the fused RMSNorm needs dense rows (ldx == hidden size)")
+        head = head + (_ptr(gamma), ctypes.c_float(eps))
+    st = getattr(_lib(), fn_name)(*head, _ptr(perm), K, k_outlier,
                                   ctypes.c_float(clip_int4), ctypes.c_float(clip_int8),
                                   *codes, _ptr(out.scales), _stream(stream))
     _check(st, fn_name)
@@ -156,6 +169,15 @@ def reorder_quantize(x, perm, K: Optional[int] = None, k_outlier: int = 128,
     Writes the GEMM operand form x8 and, unless ``packed=False``, the canonical packed q4/q8."""
     return _quantize("atom_reorder_quantize", x, perm, K, k_outlier, clip_int4, clip_int8, out,
                      stream, x8=True, packed=packed)
+
+
+def rmsnorm_reorder_quantize(x, gamma, perm, eps: float = 1e-6, K: Optional[int] = None,
+                             k_outlier: int = 128, clip_int4: float = 0.9, clip_int8: float = 1.0,
+                             out: Quantized = None, stream=None, packed: bool = True) -> Quantized:
+    """NEXT-1: fp16 RMSNorm of x [M][hidden] (weight gamma fp16 [hidden]) fused with the reorder
+    + dynamic quantize of a1 -- the paper's fusion into the prior operator."""
+    return _quantize("atom_rmsnorm_reorder_quantize", x, perm, K, k_outlier, clip_int4,
+                     clip_int8, out, stream, x8=True, packed=packed, norm=(gamma, eps))
 
 
 def quantize_weights(w, perm, K: Optional[int] = None, k_outlier: int = 128,

@@ -38,12 +38,17 @@ __device__ __forceinline__ int quant_code(float x, float inv, int lo, int hi) {
   return min(max(q, lo), hi);
 }
 
+// kNorm (NEXT-1): the RMSNorm the paper fuses the quantizer into is applied to the
+// staged row first: r = RN32(1/sqrt(sum(x^2)/ldx + eps)) from a double sum of squares, and the
+// gathered value becomes y = fp16_rn(RN32(RN32(x*r) * gamma)) (oracle N1, reading G19).
+template <bool kNorm>
 __global__ void __launch_bounds__(kQuantThreads)
 reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                         const int32_t* __restrict__ perm, int32_t G, int32_t G4,
                         int32_t groups_per_cta, float clip4, float clip8,
                         uint8_t* __restrict__ q4, int8_t* __restrict__ q8,
-                        int8_t* __restrict__ x8, int64_t K, float* __restrict__ scales) {
+                        int8_t* __restrict__ x8, int64_t K, float* __restrict__ scales,
+                        const __half* __restrict__ gamma, float eps) {
   extern __shared__ uint4 srow4[];
   const __half* srow = reinterpret_cast<const __half*>(srow4);
   const int64_t row = blockIdx.x;
@@ -53,8 +58,41 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
   // Stage the whole source row (the gather may touch any channel).
   const uint4* src = reinterpret_cast<const uint4*>(x + row * ldx);
   const int n16 = static_cast<int>(ldx / 8);
-  for (int i = threadIdx.x; i < n16; i += kQuantThreads) srow4[i] = ld_stream_u4(src + i);
-  __syncthreads();
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < n16; i += kQuantThreads) {
+    const uint4 v = ld_stream_u4(src + i);
+    srow4[i] = v;
+    if constexpr (kNorm) {
+      const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(h[k]);
+        ss = __fma_rn(static_cast<double>(f.x), static_cast<double>(f.x), ss);
+        ss = __fma_rn(static_cast<double>(f.y), static_cast<double>(f.y), ss);
+      }
+    }
+  }
+  float rinv = 1.0f;
+  if constexpr (kNorm) {
+    // squares of fp16 values are exact in double, so the fused multiply-adds above are plain sums
+    __shared__ double red[kQuantThreads / 32];
+    __shared__ float rs;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kQuantThreads / 32; ++w) t += red[w];
+      rs = __double2float_rn(
+          __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(t, static_cast<double>(ldx)),
+                                              static_cast<double>(eps)))));
+    }
+    __syncthreads();
+    rinv = rs;
+  } else {
+    __syncthreads();
+  }
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // alpha = fl(fl(2c) / (2^n - 1))
@@ -91,6 +129,13 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
     v[2] = __half2float(srow[pa.z]); v[3] = __half2float(srow[pa.w]);
     v[4] = __half2float(srow[pb.x]); v[5] = __half2float(srow[pb.y]);
     v[6] = __half2float(srow[pb.z]); v[7] = __half2float(srow[pb.w]);
+    if constexpr (kNorm) {
+      const int src_c[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        v[k] = __half2float(__float2half_rn(
+            __fmul_rn(__fmul_rn(v[k], rinv), __half2float(__ldg(gamma + src_c[k])))));
+    }
     float amax = fabsf(v[0]);
 #pragma unroll
     for (int k = 1; k < 8; ++k) amax = fmaxf(amax, fabsf(v[k]));
@@ -137,7 +182,8 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    int8_t* x8, float* scales, cudaStream_t stream, int num_sms) {
+                                    int8_t* x8, float* scales, cudaStream_t stream, int num_sms,
+                                    const void* gamma, float eps) {
   const int G = static_cast<int>(K / 128);
   const int G4 = static_cast<int>((K - k_outlier) / 128);
   // Enough CTAs to cover the SMs ~4 times; each extra split re-stages the row (from L2).
@@ -147,15 +193,16 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
   const int gpc = (G + splits - 1) / splits;
   splits = (G + gpc - 1) / gpc;
   const size_t smem = static_cast<size_t>(ldx) * sizeof(__half);
+  auto kern = gamma ? reorder_quantize_kernel<true> : reorder_quantize_kernel<false>;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(reorder_quantize_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
-  reorder_quantize_kernel<<<grid, kQuantThreads, smem, stream>>>(
-      static_cast<const __half*>(x), rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, x8, K, scales);
+  kern<<<grid, kQuantThreads, smem, stream>>>(
+      static_cast<const __half*>(x), rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, x8, K, scales,
+      static_cast<const __half*>(gamma), eps);
   return cudaGetLastError();
 }
 

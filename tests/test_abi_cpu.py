@@ -82,6 +82,11 @@ def test_host_validation_without_device(lib):
     assert lib.atom_w4a4_gemm(None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
                               None, None, 0, None) == 0
     assert lib.atom_last_launch_count() == 0
+    # fused RMSNorm variant: eps < 0 is an argument error, M == 0 a no-op
+    assert lib.atom_rmsnorm_reorder_quantize(None, 4, 256, None, f(-1.0), None, 256, 128, f(0.9),
+                                             f(1.0), None, None, None, None, None) == 4
+    assert lib.atom_rmsnorm_reorder_quantize(None, 0, 256, None, f(1e-6), None, 256, 128, f(0.9),
+                                             f(1.0), None, None, None, None, None) == 0
 
 
 def test_product_package_does_not_import_oracle():

@@ -171,6 +171,32 @@ def test_quantize_strided_rows(atom):
 
 
 # ----------------------------------------------------------------------------------------------
+# NEXT-1: RMSNorm fused into reorder + quantize, bit-exact against oracle N1 + O2-O6
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("M,K,eps", [(1, 1024, 1e-6), (7, 4096, 1e-5), (130, 4096, 1e-6),
+                                     (33, 8192, 0.0), (16, 11008, 1e-6)])
+def test_rmsnorm_reorder_quantize_bitexact(atom, M, K, eps):
+    rng = np.random.default_rng(M + K)
+    x = synth.activations(M, K, seed=M + K)
+    g = (1 + 0.1 * rng.standard_normal(K)).astype(np.float16)
+    perm = synth.perm_for(K, seed=M + K)
+    q = atom.rmsnorm_reorder_quantize(dev(x), dev(g), dev(perm), eps=eps)
+    assert_quant_equal(q, oracle.rmsnorm_quantize_rows(x, g, perm, K, 128, eps))
+
+
+def test_rmsnorm_fused_layer_output(atom):
+    """Fused norm + quantize feeding the GEMM equals the oracle's norm -> quantized linear."""
+    M, N, K = 64, 512, 2048
+    X, W, perm = synth.problem(M, N, K, seed=11)
+    g = (1 + 0.1 * np.random.default_rng(11).standard_normal(K)).astype(np.float16)
+    pd = dev(perm)
+    aq = atom.rmsnorm_reorder_quantize(dev(X), dev(g), pd)
+    c = atom.w4a4_gemm(aq, atom.quantize_weights(dev(W), pd))
+    ref = oracle.quantized_linear(oracle.rmsnorm_rows(X, g), perm, W, K)
+    assert_close_tol(host(c.float()), ref["c"], "norm+W4A4")
+
+
+# ----------------------------------------------------------------------------------------------
 # a2-a5: GEMM -- exact partials (debug mode) and tolerance outputs
 # ----------------------------------------------------------------------------------------------
 def run_gemm(atom, X, W, perm, K, k_o, debug=False, out_dtype=None):

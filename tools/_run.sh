@@ -1,2 +1,2 @@
-for m in 0 2048 0 2048; do ATOM_GEMM_PROBE_MODE=$m timeout 60 python tools/gemm_probe.py cfg5 2>&1 | head -1; done > gpurun_out/t.txt
-cat gpurun_out/t.txt
+timeout 300 python bench.py --no-cpu-baseline > gpurun_out/b11.log 2>&1
+tail -c 1500 gpurun_out/b11.log | python -c "import sys,json; l=[x for x in sys.stdin.read().splitlines() if x.startswith('{')]; d=json.loads(l[-1]); print(d['value'], d['kernels'])"
