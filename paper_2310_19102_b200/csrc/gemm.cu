@@ -66,7 +66,7 @@ template <int BT> struct Cfg {
   static constexpr int RT = BT >= 256 ? 2 : 4;          // TMEM accumulator buffers
   static constexpr int RS = 4;                          // activation slots (= go / mdone ring)
   static constexpr int RW = BT >= 256 ? 2 : 4;          // unpacked weight slots
-  static constexpr int kStages = BT >= 256 ? 5 : 8;     // packed weight TMA ring depth
+  static constexpr int kStages = BT >= 256 ? 3 : 4;     // weight TMA ring depth (16 KB stages)
   static constexpr uint32_t kTmemCols = RT * BT <= 32 ? 32 : RT * BT <= 64 ? 64
                                       : RT * BT <= 128 ? 128 : RT * BT <= 256 ? 256 : 512;
   static constexpr int NC = BT / 8;                     // 8-column chunks of the tile
@@ -115,7 +115,7 @@ struct __align__(1024) GemmSmem {
   static constexpr int RT = Cfg<BT>::RT;
   uint8_t ubuf_w[RW][kTileN * 128];     // unpacked weight group, SW128 K-major
   uint8_t ubuf_a[RS][BT * 128];         // activation group (x8), SW128 K-major, written by TMA
-  uint8_t stage_w[Cfg<BT>::kStages][kTileN * 64];   // packed weight group (or INT8 half)
+  uint8_t stage_w[Cfg<BT>::kStages][kTileN * 128];  // packed weights: 2 INT4 groups or INT8
   float ssw[RS][kTileN];                // weight scales of group g in slot g % RS (cp.async)
   float ssa[RS][BT];                    // activation scales of the same group
   uint8_t ostg[kNumEpiWarps][1024];     // per-warp output staging ([8 tokens][32 ch] fp32)
@@ -156,21 +156,23 @@ __device__ __forceinline__ float biased_fma(uint32_t r, uint32_t one, uint32_t m
 }
 
 // KR rows of the weight tile, ROW_STEP apart (a multiple of 8, so all share one swizzle phase):
-// packed stage [rows][64 B] -> unpacked SW128 [rows][128 B].  This thread owns the 16-byte
-// packed chunk c of rows r0 + k*ROW_STEP; every address is a per-thread base plus an immediate.
-// Packed chunk c holds channels 32c..32c+31; its low nibbles (even channels) become 16-byte
-// chunk 2c and its high nibbles (odd channels) chunk 2c+1 -- the x8 order of atom.h.
+// packed stage [rows][128 B] (two INT4 groups, or the INT8 group) -> unpacked SW128 [rows][128 B].
+// This thread owns the 16-byte packed chunk c (< 4) of group `sub` of rows r0 + k*ROW_STEP;
+// every address is a per-thread base plus an immediate.  Packed chunk c holds channels
+// 32c..32c+31; its low nibbles (even channels) become 16-byte chunk 2c and its high nibbles (odd
+// channels) chunk 2c+1 -- the x8 order of atom.h.  The INT8 group is copied as is (chunks c and
+// c + 4 of the 128-byte row).
 template <int KR, int ROW_STEP>
 __device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf, uint32_t r0,
-                                            uint32_t c, bool int4, int h) {
+                                            uint32_t c, bool int4, int sub) {
   static_assert(ROW_STEP % 8 == 0, "rows must share the swizzle phase");
   const uint32_t r7 = r0 & 7u;
-  const uint8_t* src = stage + r0 * 64 + c * 16;
-  uint4 v[KR];
-#pragma unroll
-  for (int k = 0; k < KR; ++k) v[k] = *reinterpret_cast<const uint4*>(src + k * ROW_STEP * 64);
   uint8_t* dst = ubuf + r0 * 128;
   if (int4) {
+    const uint8_t* src = stage + r0 * 128 + sub * 64 + c * 16;
+    uint4 v[KR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) v[k] = *reinterpret_cast<const uint4*>(src + k * ROW_STEP * 128);
     const uint32_t olo = ((2 * c) ^ r7) << 4, ohi = ((2 * c + 1) ^ r7) << 4;
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
@@ -178,10 +180,23 @@ __device__ __forceinline__ void unpack_rows(const uint8_t* stage, uint8_t* ubuf,
       *reinterpret_cast<uint4*>(dst + k * ROW_STEP * 128 + ohi) = unpack_hi(v[k]);
     }
   } else {
-    const uint32_t o = ((4 * h + c) ^ r7) << 4;
+    const uint8_t* src = stage + r0 * 128 + c * 16;
+    const uint32_t o0 = (c ^ r7) << 4, o1 = ((c + 4) ^ r7) << 4;
 #pragma unroll
-    for (int k = 0; k < KR; ++k) *reinterpret_cast<uint4*>(dst + k * ROW_STEP * 128 + o) = v[k];
+    for (int k = 0; k < KR; ++k) {
+      const uint4 a = *reinterpret_cast<const uint4*>(src + k * ROW_STEP * 128);
+      const uint4 b = *reinterpret_cast<const uint4*>(src + k * ROW_STEP * 128 + 64);
+      *reinterpret_cast<uint4*>(dst + k * ROW_STEP * 128 + o0) = a;
+      *reinterpret_cast<uint4*>(dst + k * ROW_STEP * 128 + o1) = b;
+    }
   }
+}
+
+// Weight stages: 128-byte packed rows = two consecutive INT4 groups of the same work item (or a
+// single one at an item / INT4-region boundary), or the INT8 outlier group.  Producer and unpack
+// warps walk an item's groups in these stage units.
+__device__ __forceinline__ int stage_groups(int t, int t1, int G4) {
+  return (t < G4 && t + 1 < t1 && t + 1 < G4) ? 2 : 1;
 }
 
 // ---- schedule ("data-parallel waves + stream-K tail"): the first dp_waves * gridDim.x tiles are
@@ -356,22 +371,24 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       const uint64_t pol_w = l2_policy_evict_first();
       for (int k = 0; k < n_items; ++k) {
         const Item w = get_item<BT>(p, sch, k);
-        for (int t = w.t0; t < w.t1; ++t, ++gp) {
-          const int nh = t < G4 ? 1 : 2;      // the INT8 outlier group arrives in two halves
-          for (int h = 0; h < nh; ++h, st.next()) {
-            mbar_wait(&sm.empty[st.i], st.ph ^ 1);
-            if (h == 0) TRACE(0, gp);
-            if constexpr ((kMode & 32) != 0) {
-              mbar_arrive(&sm.full[st.i]);
-            } else {
-              mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
-              // weights: read by the 4 CTAs sharing the n-tile at about the same time, then dead
-              if (t < G4)
-                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
-              else
-                tma_load_2d_hint(sm.stage_w[st.i], &tm_wq8, &sm.full[st.i], h * 64, w.n0, pol_w);
-            }
+        for (int t = w.t0; t < w.t1; st.next()) {
+          const int n = stage_groups(t, w.t1, G4);
+          mbar_wait(&sm.empty[st.i], st.ph ^ 1);
+          TRACE(0, gp);
+          if constexpr ((kMode & 32) != 0) {
+            mbar_arrive(&sm.full[st.i]);
+          } else {
+            mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 128);
+            // weights: read by the 4 CTAs sharing the n-tile at about the same time, then dead.
+            // A single INT4 group at the end of the INT4 region reads 64 bytes past the row
+            // (zero-filled by TMA, unused).
+            if (t < G4)
+              tma_load_2d_hint(sm.stage_w[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
+            else
+              tma_load_2d_hint(sm.stage_w[st.i], &tm_wq8, &sm.full[st.i], 0, w.n0, pol_w);
           }
+          t += n;
+          gp += n;
         }
       }
     }
@@ -472,20 +489,25 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     int gu = 0;
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
+      int sub = 0, n = 0;                // position inside the current weight stage
       for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), ++gu) {
         if (gu >= RW) {                  // MMAs of group g - RW finished with this weight slot
           wait_hot(&sm.mdone[lag.i], lag.ph);
           lag.next();
         }
         const bool int4 = t < G4;
-        const int nh = int4 ? 1 : 2;
-        for (int h = 0; h < nh; ++h, st.next()) {
+        if (sub == 0) {                  // first group of a stage: wait for its TMA
+          n = stage_groups(t, w.t1, G4);
           wait_hot(&sm.full[st.i], st.ph);
-          if (ut == 0 && h == 0) TRACE(2, gu);
-          if constexpr ((kMode & 64) == 0)
-            unpack_rows<4, 32>(sm.stage_w[st.i], sm.ubuf_w[uw.i], r0, c, int4, h);
+          if (ut == 0) TRACE(2, gu);
+        }
+        if constexpr ((kMode & 64) == 0)
+          unpack_rows<4, 32>(sm.stage_w[st.i], sm.ubuf_w[uw.i], r0, c, int4, sub);
+        if (++sub == n) {                // stage consumed
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[st.i]);
+          st.next();
+          sub = 0;
         }
         if constexpr ((kMode & 512) == 0) fence_proxy_async_smem();
         __syncwarp();
@@ -804,8 +826,8 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
   const void* w4 = kp ? static_cast<const void*>(a.w_q4) : static_cast<const void*>(a.w_q8);
   const void* w8 = k_o ? static_cast<const void*>(a.w_q8) : static_cast<const void*>(a.w_q4);
   const uint64_t c4 = kp ? kp : 128, c8 = k_o ? 128 : kp;
-  if (!make_map_u8(&m_wq4, w4, c4, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_map_u8(&m_wq8, w8, c8, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+  if (!make_map_u8(&m_wq4, w4, c4, N, 128, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map_u8(&m_wq8, w8, c8, N, 128, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
       !make_map_u8(&m_ax8, a.a_x8, K, M, 128, BT, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
 
