@@ -220,6 +220,9 @@ def run_gemm(atom, X, W, perm, K, k_o, debug=False, out_dtype=None):
     (129, 128, 1024, 128),   # ragged token tail across two tiles
     (256, 256, 1024, 128),
     (300, 384, 640, 128),
+    (512, 1536, 2048, 128),  # BT = 256, all tiles stream-K split (24 tiles, 148 CTAs)
+    (1024, 3200, 1152, 128), # data-parallel waves + stream-K tail, ragged K split points
+    (40, 11008, 640, 0),     # BT = 64, many n-tiles, pure INT4, tail segments
 ])
 def test_gemm_partials_bitexact(atom, M, N, K, k_o):
     X, W, perm = synth.problem(M, N, K, seed=M * 7 + N, k_outlier=k_o)
@@ -348,6 +351,50 @@ def test_n_shard_columns(atom):
         assert torch.equal(out[:, sl], alone[r])
     ref = oracle.quantized_linear(X, perm, W, K)
     assert_close_tol(host(out.float()), ref["c"], "N-shard")
+
+
+def test_gemm_cuda_graph_replay(atom):
+    """The GEMM (and the quantize kernel) captured in a CUDA graph and replayed: identical to
+    eager launches (the split-tile counters are self-cleaning, so replays need no memset)."""
+    import torch
+    M, N, K = 320, 2048, 2048
+    X, W, perm = synth.problem(M, N, K, seed=23)
+    pd = dev(perm)
+    xd = dev(X)
+    wq = atom.quantize_weights(dev(W), pd)
+    aq = atom.reorder_quantize(xd, pd)
+    eager = atom.w4a4_gemm(aq, wq).clone()
+    out = torch.empty_like(eager)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        atom.w4a4_gemm(aq, wq, out=out, stream=s)       # workspace for this stream
+        with torch.cuda.graph(g, stream=s):
+            atom.reorder_quantize(xd, pd, out=aq, stream=s)
+            atom.w4a4_gemm(aq, wq, out=out, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, eager)
+
+
+def test_gemm_fp32_split_into_wide_buffer(atom):
+    """fp32 partial output of a split-tile shape written as a column block of a wider buffer."""
+    import torch
+    M, N, K = 200, 1024, 3072
+    X, W, perm = synth.problem(M, N, K, seed=29)
+    pd = dev(perm)
+    aq = atom.reorder_quantize(dev(X), pd)
+    wq = atom.quantize_weights(dev(W), pd)
+    big = torch.full((M, N + 256), 7.0, dtype=torch.float32, device="cuda")
+    atom.w4a4_gemm(aq, wq, out=big[:, 128:128 + N])
+    torch.cuda.synchronize()
+    ref = oracle.quantized_linear(X, perm, W, K)
+    np.testing.assert_allclose(host(big[:, 128:128 + N]), ref["c"], rtol=1e-5, atol=1e-5)
+    assert torch.all(big[:, :128] == 7.0) and torch.all(big[:, 128 + N:] == 7.0)
 
 
 def test_gemm_deterministic(atom):
