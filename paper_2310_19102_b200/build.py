@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     tmp = LIB.with_name(f"libatom.so.tmp{os.getpid()}")
-    cmd = [NVCC, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+    extra = os.environ.get("ATOM_NVCC_EXTRA", "").split()   # development variants (A/B runs)
+    cmd = [NVCC, *FLAGS, *extra, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / "build.log"
     log.write_text(" ".join(cmd) + "\n" + r.stdout + r.stderr)

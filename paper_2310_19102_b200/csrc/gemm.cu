@@ -360,6 +360,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   const Sched sch = make_sched(p);
   const int n_items = sch.count();
 
+  if (threadIdx.x == 0) griddep_launch();   // the next kernel still waits for this grid's end
   if (warp < kEpiWarp0) setmaxnreg_dec<kRegsLow>();
   if (warp == 0) {
     // ===================== producer warp: packed weights (TMA) =====================
@@ -369,6 +370,14 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       Ring<KS> st;
       int gp = 0;
       const uint64_t pol_w = l2_policy_evict_first();
+      if (n_items > 0) {   // PDL: warm L2 with the first weight stages while the previous kernel ends
+        const Item w = get_item<BT>(p, sch, 0);
+        for (int t = w.t0, s = 0; t < w.t1 && s < KS; t += stage_groups(t, w.t1, G4), ++s) {
+          if (t < G4) tma_prefetch_2d(&tm_wq4, t * 64, w.n0);
+          else tma_prefetch_2d(&tm_wq8, 0, w.n0);
+        }
+      }
+      griddep_wait();
       for (int k = 0; k < n_items; ++k) {
         const Item w = get_item<BT>(p, sch, k);
         for (int t = w.t0; t < w.t1; st.next()) {
@@ -399,6 +408,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     // the epilogue is done with group g - RS.
     Ring<RS> sr;
     int gp = 0;
+    griddep_wait();                      // scales may come from the previous kernel (quantize)
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
       for (int t = w.t0; t < w.t1; ++t, sr.next(), ++gp) {
@@ -422,6 +432,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     if (lane == 0) {
       Ring<RS> u;
       const uint64_t pol_a = l2_policy_evict_last();
+      griddep_wait();                    // the activation tiles come from the previous kernel
       int ga = 0;
       for (int k = 0; k < n_items; ++k) {
         const Item w = get_item<BT>(p, sch, k);
@@ -884,7 +895,8 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
   if (want_trace && trace == nullptr) cudaMalloc(&trace, kTraceBytes);
   p.trace = want_trace ? trace : nullptr;
   if (want_trace) cudaMemsetAsync(trace, 0, kTraceBytes, stream);
-  kern<<<plan.grid, kThreads, smem, stream>>>(m_wq4, m_wq8, m_ax8, p);
+  e = launch_pdl(kern, dim3(plan.grid), dim3(kThreads), smem, stream, m_wq4, m_wq8, m_ax8, p);
+  if (e != cudaSuccess) return e;
   ++*launches;
   if (want_trace) {
     static long long h[8 * kTraceN + 4 * 1024];

@@ -2,10 +2,33 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace atom {
+
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
+// previous kernel of the stream is finishing; every kernel of this library calls griddep_wait()
+// before touching global memory another kernel may write, so the semantics are those of a plain
+// launch.  ATOM_NO_PDL=1 (development A/B) launches without the attribute.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+  static const bool off = std::getenv("ATOM_NO_PDL") != nullptr;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,

@@ -99,6 +99,20 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Programmatic dependent launch.  griddep_wait: block until the grids this one depends on
+// (the previous kernels of the stream) have completed and their memory is visible; a no-op when
+// the kernel was launched without the programmatic-serialization attribute.  griddep_launch: let
+// the next kernel of the stream be scheduled (it still waits in its own griddep_wait).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// L2 prefetch of a 2D TMA box (no shared-memory destination, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const void* desc, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+               :: "l"(desc), "r"(c0), "r"(c1) : "memory");
+}
+
 // Make generic-proxy shared-memory writes visible to the async proxy (tensor core / TMA).
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

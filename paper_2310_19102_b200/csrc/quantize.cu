@@ -19,6 +19,7 @@
 #include <cuda_fp16.h>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace atom {
 
@@ -55,6 +56,9 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
   const int g_begin = blockIdx.y * groups_per_cta;
   const int g_end = min(G, g_begin + groups_per_cta);
 
+  // PDL: x (and the outputs) may belong to the previous kernel of the stream
+  griddep_wait();
+  griddep_launch();
   // Stage the whole source row (the gather may touch any channel).
   const uint4* src = reinterpret_cast<const uint4*>(x + row * ldx);
   const int n16 = static_cast<int>(ldx / 8);
@@ -200,10 +204,9 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
     if (e != cudaSuccess) return e;
   }
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
-  kern<<<grid, kQuantThreads, smem, stream>>>(
-      static_cast<const __half*>(x), rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, x8, K, scales,
-      static_cast<const __half*>(gamma), eps);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(kQuantThreads), smem, stream, static_cast<const __half*>(x),
+                    rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, x8, K, scales,
+                    static_cast<const __half*>(gamma), eps);
 }
 
 // ---------------------------------------------------------------------------------------------

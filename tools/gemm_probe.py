@@ -25,13 +25,22 @@ wq = atom.quantize_weights(torch.from_numpy(W).cuda(), pd)
 aq = atom.reorder_quantize(torch.from_numpy(X).cuda(), pd)
 c = torch.empty((M, N), dtype=torch.float16, device="cuda")
 flush = torch.empty(300 << 20, dtype=torch.uint8, device="cuda")
+clean = torch.ones(300 << 20, dtype=torch.uint8, device="cuda")
+FLUSH = os.environ.get("PROBE_FLUSH", "write")      # write | write+read | none
+
+
+def flush_l2():
+    if FLUSH != "none":
+        flush.zero_()
+    if FLUSH == "write+read":          # evict the flush's dirty lines (write-backs) before timing
+        clean.sum(dtype=torch.int32)
 for _ in range(3):
     atom.w4a4_gemm(aq, wq, out=c)
 if os.environ.get("ATOM_GEMM_TRACE"):
     sys.exit(0)
 ts = []
 for _ in range(10):
-    flush.zero_()
+    flush_l2()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     atom.w4a4_gemm(aq, wq, out=c)
@@ -45,7 +54,7 @@ print(f"{cfg} mode={os.environ.get('ATOM_GEMM_PROBE_MODE', '0')} gemm {us:.1f} u
 xd = torch.from_numpy(X).cuda()
 qt = []
 for _ in range(10):
-    flush.zero_()
+    flush_l2()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     atom.reorder_quantize(xd, pd, out=aq)
