@@ -381,6 +381,37 @@ def test_gemm_cuda_graph_replay(atom):
         assert torch.equal(out, eager)
 
 
+def test_pdl_back_to_back_reuse(atom):
+    """Kernels are launched with programmatic dependent launch: a chain of weight quantize ->
+    GEMM -> activation quantize (overwriting the GEMM's operand buffer) -> GEMM on one stream with
+    no host synchronisation must equal the same calls synchronised one by one."""
+    import torch
+    M, N, K = 96, 1536, 2048
+    X1, W, perm = synth.problem(M, N, K, seed=31)
+    X2 = synth.activations(M, K, 32)
+    pd = dev(perm)
+    x1, x2, wd = dev(X1), dev(X2), dev(W)
+    # reference: every call synchronised
+    wq_ref = atom.quantize_weights(wd, pd)
+    torch.cuda.synchronize()
+    ref = []
+    for x in (x1, x2):
+        aq = atom.reorder_quantize(x, pd)
+        torch.cuda.synchronize()
+        ref.append(atom.w4a4_gemm(aq, wq_ref).clone())
+        torch.cuda.synchronize()
+    # chained: the weights are written by the kernel right before the first GEMM, and the second
+    # quantize rewrites the operand buffer the first GEMM reads
+    for _ in range(3):
+        wq = atom.quantize_weights(wd, pd)
+        aq = atom.reorder_quantize(x1, pd)
+        c1 = atom.w4a4_gemm(aq, wq)
+        atom.reorder_quantize(x2, pd, out=aq)
+        c2 = atom.w4a4_gemm(aq, wq)
+        torch.cuda.synchronize()
+        assert torch.equal(c1, ref[0]) and torch.equal(c2, ref[1])
+
+
 def test_gemm_fp32_split_into_wide_buffer(atom):
     """fp32 partial output of a split-tile shape written as a column block of a wider buffer."""
     import torch
