@@ -498,6 +498,53 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     Ring<RS> lag;                        // mdone slot of group g - RW
     Ring<RW> uw;                         // unpacked-weight slot of group g
     int gu = 0;
+#ifndef ATOM_UNPACK_PAIRS
+#define ATOM_UNPACK_PAIRS 1
+#endif
+    // With 4 unpacked-weight slots (BT <= 128) a whole stage (two INT4 groups) is expanded in
+    // one pass: twice the loads in flight and one fence / warp sync for both groups.
+    if constexpr (RW >= 4 && ATOM_UNPACK_PAIRS != 0) {
+      for (int k = 0; k < n_items; ++k) {
+        const Item w = get_item<BT>(p, sch, k);
+        for (int t = w.t0; t < w.t1;) {
+          const int n = stage_groups(t, w.t1, G4);
+          for (int i = 0; i < n; ++i)
+            if (gu + i >= RW) {          // MMAs of group g + i - RW finished with its slot
+              wait_hot(&sm.mdone[lag.i], lag.ph);
+              lag.next();
+            }
+          wait_hot(&sm.full[st.i], st.ph);
+          if (ut == 0) TRACE(2, gu);
+          const bool int4 = t < G4;
+          Ring<RW> uw1 = uw;
+          uw1.next();
+          if constexpr ((kMode & 64) == 0) {
+            unpack_rows<4, 32>(sm.stage_w[st.i], sm.ubuf_w[uw.i], r0, c, int4, 0);
+            if (n == 2) unpack_rows<4, 32>(sm.stage_w[st.i], sm.ubuf_w[uw1.i], r0, c, int4, 1);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.empty[st.i]);
+          st.next();
+          if constexpr ((kMode & 512) == 0) fence_proxy_async_smem();
+          __syncwarp();
+          if (ut == 0) TRACE(4, gu);
+          if (lane == 0) {
+            mbar_arrive(&sm.go[u.i]);
+            if (n == 2) {
+              Ring<RS> u1 = u;
+              u1.next();
+              mbar_arrive(&sm.go[u1.i]);
+            }
+          }
+          for (int i = 0; i < n; ++i) {
+            u.next();
+            uw.next();
+          }
+          gu += n;
+          t += n;
+        }
+      }
+    } else
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item<BT>(p, sch, k);
       int sub = 0, n = 0;                // position inside the current weight stage

@@ -38,15 +38,34 @@ for _ in range(3):
     atom.w4a4_gemm(aq, wq, out=c)
 if os.environ.get("ATOM_GEMM_TRACE"):
     sys.exit(0)
+# PROBE_REPS > 1: one CUDA graph of REPS back-to-back launches (warm L2 after the first) per
+# sample, for shapes below the event timer's resolution and the host launch rate
+REPS = int(os.environ.get("PROBE_REPS", "1"))
+graph = None
+if REPS > 1:
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        atom.w4a4_gemm(aq, wq, out=c, stream=side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            for _ in range(REPS):
+                atom.w4a4_gemm(aq, wq, out=c, stream=side)
+    torch.cuda.current_stream().wait_stream(side)
+    graph.replay()
+    torch.cuda.synchronize()
 ts = []
 for _ in range(10):
     flush_l2()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    atom.w4a4_gemm(aq, wq, out=c)
+    if graph is not None:
+        graph.replay()
+    else:
+        atom.w4a4_gemm(aq, wq, out=c)
     e1.record()
     torch.cuda.synchronize()
-    ts.append(e0.elapsed_time(e1))
+    ts.append(e0.elapsed_time(e1) / REPS)
 ts.sort()
 us = ts[len(ts) // 2] * 1e3
 print(f"{cfg} mode={os.environ.get('ATOM_GEMM_PROBE_MODE', '0')} gemm {us:.1f} us  "
