@@ -415,6 +415,33 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
         torch.cuda.synchronize()
         norm_us = 1e3 * sum(a.elapsed_time(b) for a, b in en) / len(en)
 
+    # ---------------- NEXT-4 piece: fused SwiGLU + reorder + quantize of the down projection's
+    # input (gate / up outputs of width N, as the up/gate GEMM of this config produces) ----------
+    swiglu_us, swiglu_bytes = None, None
+    if not args.no_graph and P == 1 and N % 128 == 0:
+        rng = np.random.default_rng(args.seed + 7)
+        gate = torch.from_numpy(synth.activations(M, N, args.seed + 7)).to(dev)
+        upp = torch.from_numpy(rng.standard_normal((M, N)).astype(np.float16)).to(dev)
+        perm_i = torch.from_numpy(synth.perm_for(N, args.seed + 7)).to(dev)
+        hq = atom.silu_mul_reorder_quantize(gate, upp, perm_i)
+        g_swi = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            atom.silu_mul_reorder_quantize(gate, upp, perm_i, out=hq, stream=side)
+            with torch.cuda.graph(g_swi, stream=side):
+                atom.silu_mul_reorder_quantize(gate, upp, perm_i, out=hq, stream=side)
+        torch.cuda.current_stream().wait_stream(side)
+        es = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(10)]
+        for i in range(10):
+            flush_l2()
+            es[i][0].record()
+            g_swi.replay()
+            es[i][1].record()
+        torch.cuda.synchronize()
+        swiglu_us = 1e3 * sum(a.elapsed_time(b) for a, b in es) / len(es)
+        swiglu_bytes = quant_bytes(M, N) + M * N * 2        # a second fp16 input row
+
     if rank != 0:
         return
     peaks, peak_src = load_peaks()
@@ -459,6 +486,11 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
                 "us": norm_us, "GB/s": qb / (norm_us * 1e-6) / 1e9,
                 "note": "NEXT-1 fused RMSNorm + a1 (same bytes as reorder_quantize); not part of "
                         "the step"},
+            "silu_mul_reorder_quantize": None if swiglu_us is None else {
+                "us": swiglu_us, "GB/s": swiglu_bytes / (swiglu_us * 1e-6) / 1e9,
+                "shape": [M, N],
+                "note": "NEXT-4 piece: SwiGLU of gate/up [M][N] fused with a1 for the down "
+                        "projection; not part of the step"},
             "collective": {"us": c_avg * 1e3},
         },
         "gpu_launches": gpu_launches,

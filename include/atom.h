@@ -120,6 +120,21 @@ atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_
                                             void* stream);
 
 /*
+ * NEXT-4 piece: the SwiGLU of a Llama MLP fused with a1 for the down projection (the "prior
+ * operator" of the down projection's quantizer).  gate_f16 and up_f16 are the fp16
+ * outputs [M][ldx] of the gate and up projections (same row stride ldx, rows dense in the
+ * sense of atom_reorder_quantize).  The value reordered and quantized is
+ *   h_c = fp16_rn( RN32( RN32(silu(g_c)) * u_c ) ),  silu(g) = g / (1 + exp(-g)) in double
+ * (reading G20), with the same arguments, formats and errors as atom_reorder_quantize;
+ * up_f16 must be non-NULL (ATOM_ERR_NULL) and 16-byte aligned (ATOM_ERR_ALIGN).  h is not written.
+ */
+atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* up_f16, int64_t M,
+                                             int64_t ldx, const int32_t* perm, int64_t K,
+                                             int32_t k_outlier, float clip_int4, float clip_int8,
+                                             uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
+                                             void* stream);
+
+/*
  * a0: offline weight reorder + quantize (Fig 4 P:237 "The weight matrix (W) is statically
  * reordered"; P:299 RTN stands in for GPTQ, which only changes the codes offline).  Same math
  * and formats as atom_reorder_quantize with rows = output channels n of W [N][ldw] (nn.Linear

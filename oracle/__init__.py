@@ -51,6 +51,8 @@ def lib():
         L.oracle_output_rows.argtypes = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, P]
         L.oracle_rmsnorm_rows.argtypes = [P, i64, i64, i64, P, f32, P]
         L.oracle_rmsnorm_rows.restype = ctypes.c_int
+        L.oracle_silu_mul_rows.argtypes = [P, P, i64, i64, P]
+        L.oracle_silu_mul_rows.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_max_threads.restype = ctypes.c_int
         for f in (L.oracle_quantize_rows, L.oracle_group_partials, L.oracle_gemm_output,
@@ -124,6 +126,25 @@ def rmsnorm_quantize_rows(x, gamma, perm, K: int, k_outlier: int = 128, eps: flo
     """N1 followed by O2-O6: what the fused RMSNorm + reorder + quantize kernel must produce."""
     y = rmsnorm_rows(x, gamma, eps)
     return quantize_rows(y, perm, K, k_outlier, clip_int4, clip_int8)
+
+
+def silu_mul_rows(g, u):
+    """N4: h = fp16(RN32(RN32(silu(g)) * u)) for fp16 gate / up rows, silu in double (atom_oracle.c,
+    reading G20); returns fp16 [rows][C]."""
+    g32 = np.ascontiguousarray(np.asarray(g).astype(np.float32))
+    u32 = np.ascontiguousarray(np.asarray(u).astype(np.float32))
+    assert g32.shape == u32.shape and g32.ndim == 2
+    rows, ldx = g32.shape
+    h32 = np.zeros((rows, ldx), dtype=np.float32)
+    st = lib().oracle_silu_mul_rows(_ptr(g32), _ptr(u32), rows, ldx, _ptr(h32))
+    _check(st, "oracle_silu_mul_rows")
+    return h32.astype(np.float16)
+
+
+def silu_mul_quantize_rows(g, u, perm, K: int, k_outlier: int = 128, clip_int4: float = 0.9,
+                           clip_int8: float = 1.0):
+    """N4 followed by O2-O6: what the fused SwiGLU + reorder + quantize kernel must produce."""
+    return quantize_rows(silu_mul_rows(g, u), perm, K, k_outlier, clip_int4, clip_int8)
 
 
 def group_partials(a_q4, a_q8, w_q4, w_q8, M: int, N: int, K: int, k_outlier: int = 128):

@@ -182,6 +182,28 @@ int oracle_rmsnorm_rows(const float* x, int64_t rows, int64_t ldx, int64_t C, co
   return ORC_OK;
 }
 
+/*
+ * N4 (NEXT-4 piece: the down projection's prior operator in a Llama MLP, "we fuse the
+ * quantization operator into the prior operator").  The paper does not define the MLP; Llama's is
+ * down(silu(gate(x)) * up(x)) (reading G20), with the elementwise step pinned as
+ *     s_c = RN32( (double)g_c / (1.0 + exp(-(double)g_c)) )   (double ops, one rounding)
+ *     h_c = RN32( s_c * u_c )                                  (one binary32 multiply)
+ * g and u are the fp16 gate / up outputs widened exactly to fp32; the caller rounds h to fp16
+ * (round-to-nearest-even) before the quantizer.  Output: h32 fp32 [rows][C], C = ldx.
+ */
+int oracle_silu_mul_rows(const float* g, const float* u, int64_t rows, int64_t ldx, float* h32) {
+  if (!g || !u || !h32) return ORC_ERR_NULL;
+  if (ldx <= 0 || rows < 0) return ORC_ERR_ARG;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c = 0; c < ldx; ++c) {
+      const double gd = (double)g[r * ldx + c];
+      const float s = (float)(gd / (1.0 + exp(-gd)));
+      h32[r * ldx + c] = s * u[r * ldx + c];     /* one IEEE multiply */
+    }
+  return ORC_OK;
+}
+
 /* Decode one signed nibble (two's complement). */
 static int oracle_nibble(uint8_t byte, int high) {
   int v = high ? (byte >> 4) & 0xF : byte & 0xF;

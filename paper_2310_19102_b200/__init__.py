@@ -27,7 +27,8 @@ STATUS_NAMES = {0: "ATOM_OK", 1: "ATOM_ERR_NULL", 2: "ATOM_ERR_SHAPE", 3: "ATOM_
 ATOM_F16, ATOM_F32 = 0, 1
 
 # every symbol include/atom.h declares
-ABI_SYMBOLS = ("atom_reorder_quantize", "atom_rmsnorm_reorder_quantize", "atom_quantize_weights",
+ABI_SYMBOLS = ("atom_reorder_quantize", "atom_rmsnorm_reorder_quantize",
+               "atom_silu_mul_reorder_quantize", "atom_quantize_weights",
                "atom_w4a4_gemm",
                "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_counter_bytes",
                "atom_validate_perm", "atom_status_string",
@@ -59,6 +60,9 @@ def _lib():
         L.atom_rmsnorm_reorder_quantize.argtypes = [P, i64, i64, P, f32] + q_args[3:10] + \
             [P] + q_args[10:]
         L.atom_rmsnorm_reorder_quantize.restype = ctypes.c_int
+        L.atom_silu_mul_reorder_quantize.argtypes = [P, P, i64, i64] + q_args[3:10] + \
+            [P] + q_args[10:]
+        L.atom_silu_mul_reorder_quantize.restype = ctypes.c_int
         L.atom_w4a4_gemm.argtypes = [P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int,
                                      P, P, ctypes.c_size_t, P]
         L.atom_w4a4_gemm_workspace_size.argtypes = [i64, i64, i64, i32]
@@ -123,7 +127,7 @@ class Quantized:
 
 
 def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream, x8=False,
-              packed=True, norm=None):
+              packed=True, norm=None, up=None):
     import torch
     if x.dtype != torch.float16 or x.dim() != 2 or not x.is_cuda:
         raise TypeError("expected a 2-D CUDA fp16 tensor")
@@ -146,6 +150,11 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
     if fn_name != "atom_quantize_weights":
         codes = codes + (_ptr(out.x8),)
     head = (_ptr(x), rows, ld)
+    if up is not None:                        # the up projection of the fused SwiGLU
+        if up.dtype != torch.float16 or not up.is_cuda or up.shape != x.shape \
+                or up.stride() != x.stride():
+            raise TypeError("up must be a CUDA fp16 tensor with the gate's shape and strides")
+        head = (_ptr(x), _ptr(up), rows, ld)
     if norm is not None:                      # (gamma, eps) of the fused RMSNorm
         gamma, eps = norm
         if gamma.dtype != torch.float16 or not gamma.is_cuda or gamma.numel() != ld \
@@ -178,6 +187,16 @@ def rmsnorm_reorder_quantize(x, gamma, perm, eps: float = 1e-6, K: Optional[int]
     + dynamic quantize of a1 -- the paper's fusion into the prior operator."""
     return _quantize("atom_rmsnorm_reorder_quantize", x, perm, K, k_outlier, clip_int4,
                      clip_int8, out, stream, x8=True, packed=packed, norm=(gamma, eps))
+
+
+def silu_mul_reorder_quantize(gate, up, perm, K: Optional[int] = None, k_outlier: int = 128,
+                              clip_int4: float = 0.9, clip_int8: float = 1.0,
+                              out: Quantized = None, stream=None,
+                              packed: bool = True) -> Quantized:
+    """NEXT-4 piece: SwiGLU h = silu(gate) * up of a Llama MLP (fp16 [M][I] gate / up projection
+    outputs) fused with the reorder + dynamic quantize of the down projection's input."""
+    return _quantize("atom_silu_mul_reorder_quantize", gate, perm, K, k_outlier, clip_int4,
+                     clip_int8, out, stream, x8=True, packed=packed, up=up)
 
 
 def quantize_weights(w, perm, K: Optional[int] = None, k_outlier: int = 128,

@@ -79,7 +79,8 @@ atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const in
 atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
                               int64_t K, int32_t k_o, float clip4, float clip8, uint8_t* q4,
                               int8_t* q8, int8_t* x8, float* scales, bool packed_required,
-                              void* stream, const void* gamma = nullptr, float eps = 0.0f) {
+                              void* stream, const void* gamma = nullptr, float eps = 0.0f,
+                              const void* up = nullptr) {
   g_last_launches = 0;
   atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, x8, scales,
                                       packed_required);
@@ -88,7 +89,7 @@ atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   cudaError_t e = atom::launch_reorder_quantize(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8,
                                                 x8, scales, static_cast<cudaStream_t>(stream),
-                                                dev.num_sms, gamma, eps);
+                                                dev.num_sms, gamma, eps, up);
   if (e != cudaSuccess) return ATOM_ERR_CUDA;
   g_last_launches = 1;
   return ATOM_OK;
@@ -117,6 +118,18 @@ atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_
   if (gamma_f16 && !aligned16(gamma_f16)) return ATOM_ERR_ALIGN;
   return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, x8,
                          scales, false, stream, gamma_f16, eps);
+}
+
+atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* up_f16, int64_t M,
+                                             int64_t ldx, const int32_t* perm, int64_t K,
+                                             int32_t k_outlier, float clip_int4, float clip_int8,
+                                             uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
+                                             void* stream) {
+  g_last_launches = 0;
+  if (M > 0 && !up_f16) return ATOM_ERR_NULL;
+  if (up_f16 && !aligned16(up_f16)) return ATOM_ERR_ALIGN;
+  return quantize_common(gate_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, x8,
+                         scales, false, stream, nullptr, 0.0f, up_f16);
 }
 
 atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,

@@ -34,7 +34,8 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
                                     int8_t* x8, float* scales, cudaStream_t stream, int num_sms,
-                                    const void* gamma = nullptr, float eps = 0.0f);
+                                    const void* gamma = nullptr, float eps = 0.0f,
+                                    const void* up = nullptr);
 
 cudaError_t launch_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
                                  int32_t* ok, cudaStream_t stream);

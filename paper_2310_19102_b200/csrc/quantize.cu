@@ -42,14 +42,20 @@ __device__ __forceinline__ int quant_code(float x, float inv, int lo, int hi) {
 // kNorm (NEXT-1): the RMSNorm the paper fuses the quantizer into is applied to the
 // staged row first: r = RN32(1/sqrt(sum(x^2)/ldx + eps)) from a double sum of squares, and the
 // gathered value becomes y = fp16_rn(RN32(RN32(x*r) * gamma)) (oracle N1, reading G19).
-template <bool kNorm>
+// kPre: 0 = plain a1; 1 = RMSNorm first (NEXT-1); 2 = SwiGLU first (NEXT-4 piece): x is the
+// gate projection and `up` the up projection of a Llama MLP, and the staged value is
+// h = fp16_rn(RN32(RN32(silu(g)) * u)), silu(g) = g / (1 + exp(-g)) evaluated in double (reading
+// G20), i.e. the down projection's input, quantized without an fp16 round trip through HBM.
+template <int kPre>
 __global__ void __launch_bounds__(kQuantThreads)
 reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                         const int32_t* __restrict__ perm, int32_t G, int32_t G4,
                         int32_t groups_per_cta, float clip4, float clip8,
                         uint8_t* __restrict__ q4, int8_t* __restrict__ q8,
                         int8_t* __restrict__ x8, int64_t K, float* __restrict__ scales,
-                        const __half* __restrict__ gamma, float eps) {
+                        const __half* __restrict__ gamma, float eps,
+                        const __half* __restrict__ up) {
+  constexpr bool kNorm = kPre == 1;
   extern __shared__ uint4 srow4[];
   const __half* srow = reinterpret_cast<const __half*>(srow4);
   const int64_t row = blockIdx.x;
@@ -64,7 +70,20 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
   const int n16 = static_cast<int>(ldx / 8);
   double ss = 0.0;
   for (int i = threadIdx.x; i < n16; i += kQuantThreads) {
-    const uint4 v = ld_stream_u4(src + i);
+    uint4 v = ld_stream_u4(src + i);
+    if constexpr (kPre == 2) {
+      const uint4 w = ld_stream_u4(reinterpret_cast<const uint4*>(up + row * ldx) + i);
+      __half2* hg = reinterpret_cast<__half2*>(&v);
+      const __half2* hu = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 g = __half22float2(hg[k]), u = __half22float2(hu[k]);
+        const double gx = g.x, gy = g.y;
+        const float sx = __double2float_rn(__ddiv_rn(gx, __dadd_rn(1.0, exp(-gx))));
+        const float sy = __double2float_rn(__ddiv_rn(gy, __dadd_rn(1.0, exp(-gy))));
+        hg[k] = __floats2half2_rn(__fmul_rn(sx, u.x), __fmul_rn(sy, u.y));
+      }
+    }
     srow4[i] = v;
     if constexpr (kNorm) {
       const __half2* h = reinterpret_cast<const __half2*>(&v);
@@ -187,7 +206,7 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
                                     int8_t* x8, float* scales, cudaStream_t stream, int num_sms,
-                                    const void* gamma, float eps) {
+                                    const void* gamma, float eps, const void* up) {
   const int G = static_cast<int>(K / 128);
   const int G4 = static_cast<int>((K - k_outlier) / 128);
   // Enough CTAs to cover the SMs ~4 times; each extra split re-stages the row (from L2).
@@ -197,7 +216,8 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
   const int gpc = (G + splits - 1) / splits;
   splits = (G + gpc - 1) / gpc;
   const size_t smem = static_cast<size_t>(ldx) * sizeof(__half);
-  auto kern = gamma ? reorder_quantize_kernel<true> : reorder_quantize_kernel<false>;
+  auto kern = up ? reorder_quantize_kernel<2>
+                 : gamma ? reorder_quantize_kernel<1> : reorder_quantize_kernel<0>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -206,7 +226,7 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
   return launch_pdl(kern, grid, dim3(kQuantThreads), smem, stream, static_cast<const __half*>(x),
                     rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, x8, K, scales,
-                    static_cast<const __half*>(gamma), eps);
+                    static_cast<const __half*>(gamma), eps, static_cast<const __half*>(up));
 }
 
 // ---------------------------------------------------------------------------------------------

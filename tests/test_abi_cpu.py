@@ -89,6 +89,16 @@ def test_host_validation_without_device(lib):
                                              f(1.0), None, None, None, None, None) == 0
 
 
+def test_silu_mul_quantize_host_validation(lib):
+    f = ctypes.c_float
+    # missing up projection: a NULL error; M == 0: a no-op; both decided on the host
+    assert lib.atom_silu_mul_reorder_quantize(None, None, 4, 256, None, 256, 128, f(0.9), f(1.0),
+                                              None, None, None, None, None) == 1
+    assert lib.atom_silu_mul_reorder_quantize(None, None, 0, 256, None, 256, 128, f(0.9), f(1.0),
+                                              None, None, None, None, None) == 0
+    assert lib.atom_last_launch_count() == 0
+
+
 def test_product_package_does_not_import_oracle():
     pkg = ROOT / "paper_2310_19102_b200"
     for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + \

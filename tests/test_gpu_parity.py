@@ -196,6 +196,43 @@ def test_rmsnorm_fused_layer_output(atom):
     assert_close_tol(host(c.float()), ref["c"], "norm+W4A4")
 
 
+@pytest.mark.parametrize("M,I", [(1, 1024), (7, 4096), (130, 11008), (33, 5120), (16, 28672)])
+def test_silu_mul_reorder_quantize_bitexact(atom, M, I):
+    """NEXT-4 piece: fused SwiGLU + reorder + quantize equals oracle N4 then O2-O6, bit for bit."""
+    rng = np.random.default_rng(M + I)
+    gate = synth.activations(M, I, seed=M + I)           # outlier channels included
+    up = rng.standard_normal((M, I)).astype(np.float16)
+    perm = synth.perm_for(I, seed=M + I)
+    q = atom.silu_mul_reorder_quantize(dev(gate), dev(up), dev(perm))
+    assert_quant_equal(q, oracle.silu_mul_quantize_rows(gate, up, perm, I))
+
+
+def test_llama_mlp_w4a4_chain(atom):
+    """A whole Llama MLP on the W4A4 path: gate / up GEMMs -> fused SwiGLU + quantize -> down
+    GEMM.  The down projection's codes are bit-exact against the oracle fed with the GPU's fp16
+    gate / up outputs, and its output is within the GEMM tolerance of the oracle's."""
+    import torch
+    M, H, I = 64, 1024, 2816
+    X, Wg, perm_h = synth.problem(M, I, H, seed=41)
+    Wu = synth.weights(I, H, 42)
+    Wd = synth.weights(H, I, 43)
+    perm_i = synth.perm_for(I, 44)
+    ph, pi = dev(perm_h), dev(perm_i)
+    xq = atom.reorder_quantize(dev(X), ph)
+    g = atom.w4a4_gemm(xq, atom.quantize_weights(dev(Wg), ph))
+    u = atom.w4a4_gemm(xq, atom.quantize_weights(dev(Wu), ph))
+    hq = atom.silu_mul_reorder_quantize(g, u, pi)
+    wdq = atom.quantize_weights(dev(Wd), pi)
+    y = atom.w4a4_gemm(hq, wdq)
+    torch.cuda.synchronize()
+    gh, uh = host(g), host(u)
+    ref_q = oracle.silu_mul_quantize_rows(gh, uh, perm_i, I)
+    assert_quant_equal(hq, ref_q)
+    w4, w8, wsc = oracle.quantize_rows(Wd, perm_i, I, 128, 0.85, 1.0)
+    ref = oracle.output_rows(*ref_q, w4, w8, wsc, M, H, I, 128, np.arange(M))
+    assert_close_tol(host(y.float()), ref, "MLP down")
+
+
 # ----------------------------------------------------------------------------------------------
 # a2-a5: GEMM -- exact partials (debug mode) and tolerance outputs
 # ----------------------------------------------------------------------------------------------

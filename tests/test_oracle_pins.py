@@ -537,3 +537,55 @@ def test_n1_fused_oracle_is_norm_then_quantize():
     b = oracle.quantize_rows(oracle.rmsnorm_rows(x, g), perm, K)
     for u, v in zip(a, b):
         np.testing.assert_array_equal(u, v)
+
+
+# ----------------------------------------------------------------------------------------------
+# N4 (NEXT-4 piece): SwiGLU h = silu(gate) * up, the down projection's prior operator (P:270,
+# reading G20)
+# ----------------------------------------------------------------------------------------------
+def test_n4_special_values():
+    """silu(0) = 0; for g >= 17, exp(-g) < 2^-24 so RN32(silu(g)) = g exactly and h = fp16(g*u);
+    for g = -30, |silu(g)| < 1e-11 so h is a signed zero for any fp16 u; u = 0 gives 0."""
+    C = 256
+    rng = np.random.default_rng(11)
+    u = rng.uniform(-4, 4, (3, C)).astype(np.float16)
+    g = np.zeros((3, C), np.float16)
+    g[1] = 17.0
+    g[2] = -30.0
+    h = oracle.silu_mul_rows(g, u)
+    np.testing.assert_array_equal(h[0], np.zeros(C, np.float16))
+    np.testing.assert_array_equal(h[1], (np.float32(17.0) * u[1].astype(np.float32)).astype(np.float16))
+    assert np.all(h[2] == 0)
+    np.testing.assert_array_equal(oracle.silu_mul_rows(rng.standard_normal((2, C)).astype(np.float16),
+                                                       np.zeros((2, C), np.float16)) == 0, True)
+
+
+def test_n4_tanh_form_and_sign():
+    """Against the independent form silu(g) = g/2 * (1 + tanh(g/2)) in float64, rounded by the
+    same pinned steps: identical except where the two double results straddle a binary32
+    rounding boundary (never more than one fp16 ulp).  Catches exp(+g), a missing factor g, and
+    swapped gate / up."""
+    rng = np.random.default_rng(12)
+    g = (rng.standard_normal((64, 512)) * 3).astype(np.float16)
+    u = rng.standard_normal((64, 512)).astype(np.float16)
+    g64 = g.astype(np.float64)
+    s = (g64 / 2 * (1 + np.tanh(g64 / 2))).astype(np.float32)
+    want = (s * u.astype(np.float32)).astype(np.float16)
+    h = oracle.silu_mul_rows(g, u)
+    same = (h == want) | ((h == 0) & (want == 0))
+    assert same.mean() > 0.999
+    ulp = np.abs(h.astype(np.float64) - want.astype(np.float64))
+    assert np.all(ulp <= np.spacing(np.abs(want).astype(np.float16)).astype(np.float64) + 1e-30)
+    assert not np.array_equal(oracle.silu_mul_rows(u, g), h)   # not symmetric in (gate, up)
+
+
+def test_n4_fused_oracle_is_swiglu_then_quantize():
+    K = 1024
+    rng = np.random.default_rng(13)
+    g = (rng.standard_normal((5, K)) * 2).astype(np.float16)
+    u = rng.standard_normal((5, K)).astype(np.float16)
+    perm = synth.perm_for(K, 13)
+    a = oracle.silu_mul_quantize_rows(g, u, perm, K)
+    b = oracle.quantize_rows(oracle.silu_mul_rows(g, u), perm, K)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
