@@ -915,8 +915,11 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
 
   const size_t smem = sizeof(GemmSmem<BT>) + 1024;
   auto kern = p.debug ? w4a4_gemm_kernel<BT, true> : w4a4_gemm_kernel<BT, false>;
+#ifdef ATOM_DEV_PROBES
+  // development timing probes (results WRONG by design): only in builds made with
+  // ATOM_NVCC_EXTRA=-DATOM_DEV_PROBES, never in the shipped library
   if constexpr (BT == 256 || BT == 128) {
-    static const char* mode_env = getenv("ATOM_GEMM_PROBE_MODE");   // development probe only
+    static const char* mode_env = getenv("ATOM_GEMM_PROBE_MODE");
     switch (mode_env ? atoi(mode_env) : 0) {
       case 1: kern = w4a4_gemm_kernel<BT, false, 1>; break;
       case 2: kern = w4a4_gemm_kernel<BT, false, 2>; break;
@@ -933,6 +936,7 @@ static cudaError_t launch_bt(const GemmArgs& a, const GemmPlan& plan, void* work
       default: break;
     }
   }
+#endif
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -1,5 +1,6 @@
 """Time the GEMM kernel alone (CUDA events, L2 flushed) for a config, optionally in a probe mode
-(ATOM_GEMM_PROBE_MODE: 1 = no epilogue math, 2 = no unpack, 3 = neither).  Development tool."""
+(ATOM_GEMM_PROBE_MODE: 1 = no epilogue math, 2 = no TMEM loads, ...; only honoured by a library
+built with ATOM_NVCC_EXTRA=-DATOM_DEV_PROBES).  Development tool."""
 import os
 import sys
 import time
