@@ -107,3 +107,67 @@ class TensorParallelLinear:
 
     def __call__(self, x):
         return self.combine(self.gemm(self.quantize(x)))
+
+
+class TensorParallelMLP:
+    """NEXT-4: a Llama MLP  y = down(silu(gate(x)) * up(x))  on the W4A4 path, Megatron-paired
+    over the default process group: gate / up are column parallel WITHOUT a gather, the SwiGLU is
+    fused into the down projection's quantizer (atom_silu_mul_reorder_quantize), and down is row
+    parallel, so the only collective is one fp32 all-reduce of [M][H] partials per MLP (the
+    reduce-scatter of a sequence-parallel layer moves the same bytes).
+
+    The down projection's reorder is folded into the ROW order of W_gate / W_up offline (the
+    paper's static weight reorder): their outputs come out already in the reordered
+    channel order, so rank r's gate / up shard [i0, i1) is exactly the down projection's K-shard
+    of reordered groups k_shard_groups(I, P, r) -- contiguous, with an identity perm inside the
+    shard and the INT8 outlier group on the last rank.  Every rank holds the same perm_h (input
+    reorder of gate / up) and perm_i (reorder of the intermediate channels)."""
+
+    def __init__(self, w_gate, w_up, w_down, perm_h, perm_i, k_outlier: int = 128,
+                 clip_w: float = 0.85, clip_a: float = 0.9, clip_int8: float = 1.0):
+        import torch
+        import torch.distributed as dist
+
+        import paper_2310_19102_b200 as atom
+        self.atom, self.dist, self.torch = atom, dist, torch
+        init = dist.is_available() and dist.is_initialized()
+        self.P, self.r = (dist.get_world_size(), dist.get_rank()) if init else (1, 0)
+        I, H = w_gate.shape
+        if w_up.shape != (I, H) or w_down.shape != (H, I):
+            raise ValueError("expected W_gate, W_up [I][H] and W_down [H][I]")
+        g0, g1 = k_shard_groups(I, self.P, self.r)
+        i0, i1 = g0 * GROUP, g1 * GROUP
+        rows = perm_i[i0:i1].long()                       # reordered channels of this rank
+        self.H, self.Ir = H, i1 - i0
+        self.ko = k_outlier if self.r == self.P - 1 else 0
+        self.perm_h = perm_h
+        self.ident = torch.arange(self.Ir, dtype=torch.int32, device=perm_i.device)
+        self.clip_a, self.clip_int8 = clip_a, clip_int8
+        q = dict(clip_int4=clip_w, clip_int8=clip_int8)
+        self.wg = atom.quantize_weights(w_gate[rows].contiguous(), perm_h, k_outlier=k_outlier, **q)
+        self.wu = atom.quantize_weights(w_up[rows].contiguous(), perm_h, k_outlier=k_outlier, **q)
+        self.wd = atom.quantize_weights(w_down[:, rows].contiguous(), self.ident, K=self.Ir,
+                                        k_outlier=self.ko, **q)
+        self.k_outlier = k_outlier
+
+    def local(self, x):
+        """This rank's fp32 partial of y [M][H] (and the quantized down-projection input)."""
+        atom = self.atom
+        xq = atom.reorder_quantize(x, self.perm_h, k_outlier=self.k_outlier,
+                                   clip_int4=self.clip_a, clip_int8=self.clip_int8)
+        g = atom.w4a4_gemm(xq, self.wg)
+        u = atom.w4a4_gemm(xq, self.wu)
+        hq = atom.silu_mul_reorder_quantize(g, u, self.ident, K=self.Ir, k_outlier=self.ko,
+                                            clip_int4=self.clip_a, clip_int8=self.clip_int8)
+        return atom.w4a4_gemm(hq, self.wd, out_dtype=self.torch.float32), (g, u, hq)
+
+    def __call__(self, x):
+        y, _ = self.local(x)
+        if self.P > 1:
+            if self.dist.get_backend() == "gloo":     # tests: several ranks on one GPU
+                h = y.cpu()
+                self.dist.all_reduce(h)
+                y.copy_(h)
+            else:
+                self.dist.all_reduce(y)
+        return y.half()

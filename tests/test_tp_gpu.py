@@ -70,3 +70,65 @@ def test_tp_two_ranks_one_gpu(shard):
     ref = oracle.quantized_linear(X, perm, W, K)["c"]
     err = np.abs(out.astype(np.float64) - ref)
     assert np.all(err <= 2.0 ** -10 + 1e-3 * np.abs(ref))
+
+
+def _mlp_worker(rank, world, port, M, H, I, q):
+    import torch.distributed as dist
+    from paper_2310_19102_b200 import tp
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        X, perm_h = synth.activations(M, H, 7), synth.perm_for(H, 7)
+        Wg, Wu, Wd = synth.weights(I, H, 71), synth.weights(I, H, 72), synth.weights(H, I, 73)
+        perm_i = synth.perm_for(I, 74)
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        mlp = tp.TensorParallelMLP(cu(Wg), cu(Wu), cu(Wd), cu(perm_h), cu(perm_i))
+        x = cu(X)
+        _, (g, u, hq) = mlp.local(x)
+        y = mlp(x)
+        torch.cuda.synchronize()
+        # this rank's down-projection input: bit-exact against the oracle fed with the GPU's
+        # fp16 gate / up shard (which must be the perm_i-reordered channels of this rank)
+        Ir, ko = mlp.Ir, mlp.ko
+        g0, _ = tp.k_shard_groups(I, world, rank)
+        rows = perm_i[g0 * 128:g0 * 128 + Ir]
+        ident = np.arange(Ir, dtype=np.int32)
+        a4, a8, asc = oracle.silu_mul_quantize_rows(g.cpu().numpy(), u.cpu().numpy(), ident, Ir, ko)
+        if a4.size:
+            np.testing.assert_array_equal(hq.q4.cpu().numpy(), a4)
+        if ko:
+            np.testing.assert_array_equal(hq.q8.cpu().numpy(), a8)
+        np.testing.assert_array_equal(hq.scales.cpu().numpy().view(np.uint32), asc.view(np.uint32))
+        # the gate shard is the reordered channels of the unsharded gate projection
+        full_g = oracle.quantized_linear(X, perm_h, Wg[rows], H)["c"]
+        assert np.all(np.abs(g.float().cpu().numpy() - full_g) <= 2.0 ** -10 + 1e-3 * np.abs(full_g))
+        # oracle partial of this rank's down projection, summed over ranks like the GPU partials
+        w4, w8, wsc = oracle.quantize_rows(np.ascontiguousarray(Wd[:, rows]), ident, Ir, ko, 0.85, 1.0)
+        part = torch.from_numpy(oracle.output_rows(a4, a8, asc, w4, w8, wsc, M, H, Ir, ko,
+                                                   np.arange(M)))
+        dist.all_reduce(part)
+        if rank == 0:
+            q.put((y.cpu().numpy(), part.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_tp_paired_mlp(world):
+    """NEXT-4: Megatron-paired Llama MLP (gate/up column parallel without a gather, SwiGLU fused
+    into the down projection's quantizer, down row parallel, one all-reduce) on the real kernels,
+    world ranks sharing cuda:0."""
+    M, H, I = 48, 1024, 2048
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_mlp_worker, args=(r, world, port, M, H, I, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    y, ref = q.get(timeout=600)
+    for p in ps:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    err = np.abs(y.astype(np.float64) - ref)
+    assert np.all(err <= 2.0 ** -10 + 1e-3 * np.abs(ref)), np.max(err)
