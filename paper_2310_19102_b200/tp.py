@@ -109,6 +109,14 @@ class TensorParallelLinear:
         return self.combine(self.gemm(self.quantize(x)))
 
 
+def mlp_shard(perm_i, I: int, P: int, r: int, k_outlier: int = 128):
+    """(rows, I_r, k_outlier_r) of rank r in the paired MLP: the original intermediate channels
+    perm_i[i0:i1] whose gate / up rows the rank owns (in reordered order), which are also its
+    down-projection K-shard (identity perm inside the shard, INT8 group on the last rank)."""
+    g0, g1 = k_shard_groups(I, P, r)
+    return perm_i[g0 * GROUP:g1 * GROUP], (g1 - g0) * GROUP, (k_outlier if r == P - 1 else 0)
+
+
 class TensorParallelMLP:
     """NEXT-4: a Llama MLP  y = down(silu(gate(x)) * up(x))  on the W4A4 path, Megatron-paired
     over the default process group: gate / up are column parallel WITHOUT a gather, the SwiGLU is
@@ -135,11 +143,9 @@ class TensorParallelMLP:
         I, H = w_gate.shape
         if w_up.shape != (I, H) or w_down.shape != (H, I):
             raise ValueError("expected W_gate, W_up [I][H] and W_down [H][I]")
-        g0, g1 = k_shard_groups(I, self.P, self.r)
-        i0, i1 = g0 * GROUP, g1 * GROUP
-        rows = perm_i[i0:i1].long()                       # reordered channels of this rank
-        self.H, self.Ir = H, i1 - i0
-        self.ko = k_outlier if self.r == self.P - 1 else 0
+        rows, self.Ir, self.ko = mlp_shard(perm_i, I, self.P, self.r, k_outlier)
+        rows = rows.long()                                # reordered channels of this rank
+        self.H = H
         self.perm_h = perm_h
         self.ident = torch.arange(self.Ir, dtype=torch.int32, device=perm_i.device)
         self.clip_a, self.clip_int8 = clip_a, clip_int8
