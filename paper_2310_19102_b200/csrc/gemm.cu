@@ -146,9 +146,9 @@ __device__ __forceinline__ uint4 unpack_hi(uint4 v) {  // odd channels -> 16*q b
 __device__ __forceinline__ float biased(uint32_t r, uint32_t magic) {
   return __uint_as_float(and_xor(r, 0x007FFFFFu, magic));
 }
-// The same value as an integer multiply-add, R * 1 + 0x4B400000 (= the LOP3 result for
-// |R| < 2^22), which issues to the FMA pipe instead of the ALU pipe; `one` is an opaque 1 so
-// ptxas keeps the IMAD.  Used for part of the columns to balance the two pipes.
+// The same value as an integer add, R * 1 + 0x4B400000 (= the LOP3 result for |R| < 2^22).
+// ptxas emits it as VIADD, which does not issue to the ALU pipe the LOP3s (and the unpack warps)
+// load; used for half of the columns (measured best of 0, 1/4, 1/2, 3/4).
 __device__ __forceinline__ float biased_fma(uint32_t r, uint32_t one, uint32_t magic) {
   uint32_t d;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(r), "r"(one), "r"(magic));
