@@ -681,12 +681,22 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
               const int j = bi * 16 + jj;
               if (j < NCOL && j < ncol) {
                 uint32_t* rv = r[bi & 1] + jj;
+#ifndef ATOM_I2F_MASK
+#define ATOM_I2F_MASK 0x99   // quads jj = 0, 12 of every batch (A/B: NOTES.md)
+#endif
+                // Conversions spread over three pipes: half of the column quads by I2FP (quarter
+                // rate, but otherwise idle), a quarter by LOP3 (ALU), a quarter by VIADD.  The
+                // I2FP columns dequantize as g = RN(sw' * float(R)) -- the same single rounding
+                // as the magic path's fused multiply-add, so the result is bit-identical.
+                const bool i2f = !kDebug && kMode == 0 && !kPre &&
+                                 ((ATOM_I2F_MASK >> ((bi & 1) * 4 + jj / 4)) & 1) != 0;
                 if constexpr (!kPre) {
 #pragma unroll
                   for (int v = 0; v < 4; ++v)
-                    rv[v] = __float_as_uint(((kMode & 8192) == 0 && (jj & 4) != 0)
-                                                ? biased_fma(rv[v], one, magic)
-                                                : biased(rv[v], magic));
+                    rv[v] = i2f ? __float_as_uint(__int2float_rn(static_cast<int>(rv[v])))
+                                : __float_as_uint(((kMode & 8192) == 0 && (jj & 4) != 0)
+                                                      ? biased_fma(rv[v], one, magic)
+                                                      : biased(rv[v], magic));
                 }
                 if constexpr (kDebug) {
 #pragma unroll
@@ -703,10 +713,11 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                   acc[j] += __uint_as_float(rv[0] ^ rv[3]);
                   continue;
                 }
+                const float2 ncq = i2f ? make_float2(0.0f, 0.0f) : nc2;
                 const float2 g0 = __ffma2_rn(
-                    make_float2(__uint_as_float(rv[0]), __uint_as_float(rv[1])), sw2, nc2);
+                    make_float2(__uint_as_float(rv[0]), __uint_as_float(rv[1])), sw2, ncq);
                 const float2 g1 = __ffma2_rn(
-                    make_float2(__uint_as_float(rv[2]), __uint_as_float(rv[3])), sw2, nc2);
+                    make_float2(__uint_as_float(rv[2]), __uint_as_float(rv[3])), sw2, ncq);
                 const float2 a0 = __ffma2_rn(make_float2(s4.x, s4.y), g0,
                                              make_float2(acc[j], acc[j + 1]));
                 const float2 a1 = __ffma2_rn(make_float2(s4.z, s4.w), g1,
