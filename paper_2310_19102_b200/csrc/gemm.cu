@@ -682,12 +682,13 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
               if (j < NCOL && j < ncol) {
                 uint32_t* rv = r[bi & 1] + jj;
 #ifndef ATOM_I2F_MASK
-#define ATOM_I2F_MASK 0x99   // quads jj = 0, 12 of every batch (A/B: NOTES.md)
+#define ATOM_I2F_MASK 0xFF   // all column quads (A/B of the mixes: profiles/r01/NOTES.md)
 #endif
-                // Conversions spread over three pipes: half of the column quads by I2FP (quarter
-                // rate, but otherwise idle), a quarter by LOP3 (ALU), a quarter by VIADD.  The
-                // I2FP columns dequantize as g = RN(sw' * float(R)) -- the same single rounding
-                // as the magic path's fused multiply-add, so the result is bit-identical.
+                // int32 -> float by I2FP (measured faster than the LOP3 / VIADD magic-number
+                // conversions, alone or mixed, once the epilogue is dequant-bound); the I2FP
+                // columns dequantize as g = RN(sw' * float(R)) -- the same single rounding as
+                // the magic path's fused multiply-add, so either form gives identical bits.
+                // The debug-partials kernel keeps the magic path (it reads R back from it).
                 const bool i2f = !kDebug && kMode == 0 && !kPre &&
                                  ((ATOM_I2F_MASK >> ((bi & 1) * 4 + jj / 4)) & 1) != 0;
                 if constexpr (!kPre) {
