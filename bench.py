@@ -502,6 +502,48 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def _spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment: re-launch this script
+    as N ranks on this node (torch.distributed.run, one process per GPU, rendezvous on
+    127.0.0.1), exactly the launch the driver uses, and return the launcher's exit code."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, M, N, K, cfg_name, world, rank):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo on CPU): every rank derives its
+    shard, the shard table is all-gathered, rank 0 prints it as one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_19102_b200 import tp
+    if args.shard == "n":
+        lo, hi = tp.n_shard_rows(N, world, rank)
+    else:
+        g0, g1 = tp.k_shard_groups(K, world, rank)
+        lo, hi = g0 * 128, g1 * 128
+    mine = torch.tensor([rank, lo, hi], dtype=torch.int64)
+    table = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(table, mine)
+    else:
+        table = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "config": {"workload": cfg_name},
+                          "shard": args.shard,
+                          "ranks": [[int(v) for v in t.tolist()] for t in table]}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -518,19 +560,40 @@ def main():
                     help="launch the step's kernels directly instead of replaying CUDA graphs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only (gloo, no GPU work): prints the shard table")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     M, N, K, _ = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, M, N, K, args.config, world, rank)
         return
+    if args.dry_run:
+        import torch.distributed as dist
+        if world > 1:
+            dist.init_process_group("gloo")
+        try:
+            run_dry(args, M, N, K, args.config, world, rank)
+        finally:
+            if world > 1:
+                dist.destroy_process_group()
+        return
     if world > 1:
         import torch
         import torch.distributed as dist
+        # communicator setup (ring / NVLS) is logged per rank beside the bench output
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH,NVLS")
+        os.environ.setdefault("NCCL_DEBUG_FILE", str(ROOT / "gpurun_out" / "nccl.%h.%p.log"))
+        (ROOT / "gpurun_out").mkdir(exist_ok=True)
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
