@@ -1,0 +1,257 @@
+// probe_epi.cu -- round-2 epilogue design probe (development tool, not product).
+// 8 epilogue warps drain a 128 x 256 fp32 partial per "group" from TMEM and apply the (A)-layout
+// dequant  h = P*alpha + beta (per-thread scalars), acc += s_col * h (per-column vector), while a
+// kind::f8f6f4 128x256x128 MMA stream runs into the other half of TMEM.  Variants differ only in
+// where the per-column vector comes from and in the TMEM load shape:
+//   V0  column scales held in registers (no load: the upper bound)
+//   V1  32x32b.x16 loads one batch ahead; scales by LDS.128, one batch ahead
+//   V2  32x32b.x16; the 32 scales of a 32-column block by 8 LDS.128 before that block's loads
+//   V3  16x256b.x4 loads (two in flight); the thread's 32 column scales of the group by 16
+//       LDS.64 at the group start, before any TMEM load of the group
+//   V4  32x32b.x32 loads one batch ahead; scales by LDS.128, one batch ahead
+//   V5  32x32b.x16; scales by LDG.128 (L1) one batch ahead
+//   V6  32x32b.x16; scales by LDC from a __constant__ array (register-indexed), one batch ahead
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2310_19102_b200/csrc -o tools/probe_epi tools/probe_epi.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+using namespace atom;
+
+__host__ __device__ constexpr uint32_t idesc_f8(uint32_t m, uint32_t n) {
+  return (1u << 4) | ((n >> 3) << 17) | ((m >> 4) << 24);   // D f32, A = B = E4M3, K-major
+}
+__device__ __forceinline__ void umma_f8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+#define R8(b) "=r"(r[b + 0]), "=r"(r[b + 1]), "=r"(r[b + 2]), "=r"(r[b + 3]), "=r"(r[b + 4]), \
+              "=r"(r[b + 5]), "=r"(r[b + 6]), "=r"(r[b + 7])
+__device__ __forceinline__ void ld32x32b_x32(uint32_t t, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+               "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31},"
+               " [%32];"
+               : R8(0), R8(8), R8(16), R8(24) : "r"(t) : "memory");
+}
+
+__constant__ float c_scales[512];
+
+__device__ __forceinline__ float2 f2(uint32_t a, uint32_t b) {
+  return make_float2(__uint_as_float(a), __uint_as_float(b));
+}
+
+template <int V>
+__global__ void __launch_bounds__(384, 1) epi(int groups, int mma_groups, const float* gsc,
+                                              long long* out, float* sink) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ __align__(16) float ssc[4][256];
+  for (int i = threadIdx.x * 16; i < (128 + 256) * 128; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(base + i) = make_uint4(0x38383838u, 0x40404040u, 0xB8B8B8B8u, 0);
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) (&ssc[0][0])[i] = 1.0f + i * 1e-3f;
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  if (warp < 4) {
+    setmaxnreg_dec<56>();
+    if (warp == 0 && lane == 0 && mma_groups > 0) {
+      constexpr uint32_t id = idesc_f8(128, 256);
+      const uint32_t a = smem_u32(base), b = smem_u32(base + 128 * 128);
+      long long t0 = clock64();
+      for (int g = 0; g < mma_groups; ++g)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_f8(tbase + 256, umma_desc_sw128(a + 32 * k), umma_desc_sw128(b + 32 * k), id, k > 0);
+      umma_commit(&bar);
+      mbar_wait(&bar, 0);
+      out[1] = clock64() - t0;
+    }
+  } else {
+    setmaxnreg_inc<224>();
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const uint32_t tq = tbase + (static_cast<uint32_t>(q * 32) << 16) + half * 128;
+    float acc[128];
+#pragma unroll
+    for (int i = 0; i < 128; ++i) acc[i] = 0.0f;
+    const float al = 0.5f + lane * 1e-3f, be = 0.25f - lane * 1e-3f;
+    const float2 al2 = make_float2(al, al), be2 = make_float2(be, be);
+    float sreg[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sreg[i] = 1.0f + i * 0.01f + lane * 1e-4f;
+    long long c0 = clock64();
+    for (int g = 0; g < groups; ++g) {
+      const float* ss = &ssc[g & 3][half * 128];
+      const float* gs = gsc + (g & 63) * 256 + half * 128;
+      const int cbase = (g & 1) * 256 + half * 128;
+      if constexpr (V == 0 || V == 1 || V == 5 || V == 6) {
+        uint32_t r[2][16];
+        float4 sn[4], sc[4];
+        auto lds = [&](int bi, float4* d) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if constexpr (V == 1) d[j] = *reinterpret_cast<const float4*>(ss + bi * 16 + 4 * j);
+            else if constexpr (V == 5) d[j] = __ldg(reinterpret_cast<const float4*>(gs + bi * 16 + 4 * j));
+            else if constexpr (V == 6) {
+              const int o = cbase + bi * 16 + 4 * j;
+              d[j] = make_float4(c_scales[o], c_scales[o + 1], c_scales[o + 2], c_scales[o + 3]);
+            }
+          }
+        };
+        tmem_ld16p(tq, r[0]);
+        if constexpr (V != 0) lds(0, sn);
+#pragma unroll
+        for (int bi = 0; bi < 8; ++bi) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sc[j] = sn[j];
+          if (bi + 1 < 8) {
+            tmem_ld16p(tq + 16 * (bi + 1), r[(bi + 1) & 1]);
+            if constexpr (V != 0) lds(bi + 1, sn);
+          } else {
+            tmem_ld_wait();
+          }
+          const uint32_t* rv = r[bi & 1];
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            const int c = bi * 16 + j;
+            float2 s2;
+            if constexpr (V == 0) s2 = make_float2(sreg[j], sreg[j + 1]);
+            else {
+              const float4 s4 = sc[j / 4];
+              s2 = (j & 2) ? make_float2(s4.z, s4.w) : make_float2(s4.x, s4.y);
+            }
+            const float2 h = __ffma2_rn(f2(rv[j], rv[j + 1]), al2, be2);
+            const float2 a = __ffma2_rn(s2, h, make_float2(acc[c], acc[c + 1]));
+            acc[c] = a.x; acc[c + 1] = a.y;
+          }
+        }
+      } else if constexpr (V == 2) {
+#pragma unroll
+        for (int blk = 0; blk < 4; ++blk) {
+          float4 s[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) s[j] = *reinterpret_cast<const float4*>(ss + blk * 32 + 4 * j);
+          uint32_t r[2][16];
+          tmem_ld16p(tq + blk * 32, r[0]);
+          tmem_ld16p(tq + blk * 32 + 16, r[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const int c = blk * 32 + j;
+            const float4 s4 = s[j / 4];
+            const float2 s2 = (j & 2) ? make_float2(s4.z, s4.w) : make_float2(s4.x, s4.y);
+            const uint32_t* rv = r[j / 16];
+            const float2 h = __ffma2_rn(f2(rv[j & 15], rv[(j & 15) + 1]), al2, be2);
+            const float2 a = __ffma2_rn(s2, h, make_float2(acc[c], acc[c + 1]));
+            acc[c] = a.x; acc[c + 1] = a.y;
+          }
+        }
+      } else if constexpr (V == 3) {
+        // thread's columns: 8k + 2(lane%4) + {0,1}, k < 16; rows: lane/4 + {0, 8, 16, 24}
+        float2 s[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          s[k] = *reinterpret_cast<const float2*>(ss + 8 * k + 2 * (lane & 3));
+        // 8 loads: (lane half hh, 32-column block cb), each 16 regs = 4 chunks x 4
+        uint32_t r[2][16];
+        auto ld = [&](int i, uint32_t* d) {
+          const int hh = i & 1, cb = i >> 1;
+          tmem_ld_16x256b<4>(tq + (static_cast<uint32_t>(16 * hh) << 16) + 32 * cb, d);
+        };
+        ld(0, r[0]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i + 1 < 8) ld(i + 1, r[(i + 1) & 1]);
+          else tmem_ld_wait();
+          const int hh = i & 1, cb = i >> 1;
+          const uint32_t* rv = r[i & 1];
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const int k = cb * 4 + ch;                 // 8-column chunk
+            const int a0 = (hh * 2) * 32 + 2 * k;      // acc slot: row (hh*2 + {0,1}), col pair k
+            const float2 h0 = __ffma2_rn(f2(rv[4 * ch], rv[4 * ch + 1]), al2, be2);
+            const float2 h1 = __ffma2_rn(f2(rv[4 * ch + 2], rv[4 * ch + 3]), al2, be2);
+            const float2 x0 = __ffma2_rn(s[k], h0, make_float2(acc[a0], acc[a0 + 1]));
+            const float2 x1 = __ffma2_rn(s[k], h1, make_float2(acc[a0 + 32], acc[a0 + 33]));
+            acc[a0] = x0.x; acc[a0 + 1] = x0.y; acc[a0 + 32] = x1.x; acc[a0 + 33] = x1.y;
+          }
+        }
+      } else if constexpr (V == 4) {
+        uint32_t r[2][32];
+        float4 sn[8], sc[8];
+        auto lds = [&](int bi, float4* d) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) d[j] = *reinterpret_cast<const float4*>(ss + bi * 32 + 4 * j);
+        };
+        ld32x32b_x32(tq, r[0]);
+        lds(0, sn);
+#pragma unroll
+        for (int bi = 0; bi < 4; ++bi) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sc[j] = sn[j];
+          if (bi + 1 < 4) { ld32x32b_x32(tq + 32 * (bi + 1), r[(bi + 1) & 1]); lds(bi + 1, sn); }
+          else tmem_ld_wait();
+          const uint32_t* rv = r[bi & 1];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const int c = bi * 32 + j;
+            const float4 s4 = sc[j / 4];
+            const float2 s2 = (j & 2) ? make_float2(s4.z, s4.w) : make_float2(s4.x, s4.y);
+            const float2 h = __ffma2_rn(f2(rv[j], rv[j + 1]), al2, be2);
+            const float2 a = __ffma2_rn(s2, h, make_float2(acc[c], acc[c + 1]));
+            acc[c] = a.x; acc[c + 1] = a.y;
+          }
+        }
+      }
+    }
+    long long c1 = clock64();
+    if (lane == 0) out[2 + warp - 4] = c1 - c0;
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 128; ++i) s += acc[i];
+    if (s == 1.2345f) sink[threadIdx.x] = s;
+  }
+  tc_fence_before(); __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tbase, 512); }
+}
+
+int main() {
+  long long* d;
+  float *sink, *gsc;
+  cudaMalloc(&d, 64 * sizeof(long long));
+  cudaMalloc(&sink, 4096 * sizeof(float));
+  cudaMalloc(&gsc, 64 * 256 * sizeof(float));
+  float hs[512];
+  for (int i = 0; i < 512; ++i) hs[i] = 1.0f + i * 1e-3f;
+  cudaMemcpyToSymbol(c_scales, hs, sizeof(hs));
+  cudaMemset(gsc, 0, 64 * 256 * sizeof(float));
+  long long h[64];
+  const int G = 400, smem = (128 + 256) * 128 + 1024;
+#define RUN(V)                                                                                     \
+  do {                                                                                             \
+    cudaFuncSetAttribute(epi<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
+    for (int withmma = 0; withmma < 2; ++withmma) {                                                \
+      cudaMemset(d, 0, sizeof(h));                                                                 \
+      epi<V><<<1, 384, smem>>>(G, withmma ? 4 * G : 0, gsc, d, sink);                              \
+      cudaError_t e = cudaGetLastError();                                                          \
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();                                           \
+      if (e != cudaSuccess) { printf("V%d ERROR %s\n", V, cudaGetErrorString(e)); return 1; }      \
+      cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);                                         \
+      long long mx = 0;                                                                            \
+      for (int w = 0; w < 8; ++w) mx = h[2 + w] > mx ? h[2 + w] : mx;                              \
+      printf("V%d mma=%d: %7.1f clk per 128x256 group", V, withmma, (double)mx / G);               \
+      if (withmma) printf("   (MMA stream %.1f clk/group)", (double)h[1] / (4 * G));              \
+      printf("\n");                                                                                \
+    }                                                                                              \
+  } while (0)
+  RUN(0); RUN(1); RUN(2); RUN(3); RUN(4); RUN(5); RUN(6);
+  printf("rc=0\n");
+  return 0;
+}
