@@ -62,8 +62,9 @@ def algorithmic_bytes(M, N, K, c_bytes=2):
 
 
 def quant_bytes(M, K):
-    per_row = (K - K_OUT) // 2 + K_OUT + (K // 128) * 4
-    return M * K * 2 + K * 4 + M * per_row
+    """a1 as timed: read X fp16 + perm, write the GEMM operand form (one byte per code) and the
+    per-group code sums and scales (include/atom.h a_f8, a_csum, scales)."""
+    return M * K * 2 + K * 4 + M * K + M * (K // 128) * 8
 
 
 # ------------------------------------------------------------------------------------------------

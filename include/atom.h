@@ -23,7 +23,8 @@
  *     the hot path) surface at the caller's next synchronization.  atom_validate_perm() checks a
  *     perm on the device for tests.
  *   - All base pointers must be 16-byte aligned.  Calls are reentrant; the only global state is
- *     a per-device attribute cache.
+ *     per-device attribute caches and the driver's tensor-map encoder entry point, each
+ *     initialised once, thread-safely (std::call_once / function-local statics).
  *   - Group size is fixed at g = 128 ("group size of 128"); k_outlier is 0 or 128
  *     ("128 channels ... keep them in INT8"); K counts the outlier channels (P:256 fn).
  *
@@ -33,19 +34,24 @@
  *   q8      int8  [rows][k_outlier]          symmetric INT8 codes of the outlier block
  *   scales  fp32  [K/128][rows]              group-major; row t < G4 = (K-k_o)/128 is INT4 group
  *           t, the last row is the outlier scale when k_outlier == 128 (one per token / channel)
- *   x8      int8  [rows][K]                  the same codes, one per byte, in the K order the
- *           GEMM's tensor-core operand uses (activations only; written by atom_reorder_quantize
- *           when requested, read by atom_w4a4_gemm).  Group t occupies bytes [128t, 128t+128) of
- *           a row.  INT4 group (t < G4): reordered channel 128t + 32c + 8i + 2b + h (c, i, b < 4,
- *           h < 2) sits at byte 128t + 32c + 16h + 4i + b, i.e. within every 32-channel chunk
- *           the even channels come first, then the odd ones -- the order in which the GEMM
- *           expands a packed weight nibble pair (low nibble = even channel) to two bytes.  The
- *           permutation is the same for both operands, so every group dot product is unchanged
- *           (P:254 Step 1 sums over the group).  INT8 outlier group: natural order (= q8).
- *           Why: tcgen05 has no 4-bit integer MMA kind, so INT4 must be expanded to int8 on the
- *           SM; doing it for the activations in the HBM-bound quantize kernel (+1 byte/element
- *           written) instead of once per output tile inside the GEMM removes 2/3 of the GEMM's
- *           shared-memory unpack traffic.
+ *   a_f8    uint8 [rows][K]  GEMM operand form of the activations (written by the quantize
+ *           calls when requested, read by atom_w4a4_gemm_f8): one byte per code.  INT4 group t
+ *           (t < G4) occupies bytes [128t, 128t+128) of a row, each code as the E4M3 byte of
+ *           q * 2^-9 (sign-magnitude: q for q >= 0, 0x80 | -q for q < 0; bytes 0x00..0x0F of
+ *           E4M3 are exactly k * 2^-9), reordered channel 128t + 32c + 8i + 2b + h (c, i, b < 4,
+ *           h < 2) at byte 128t + 32c + 16h + 4i + b -- within every 32-channel chunk the even
+ *           channels first, then the odd ones, the order in which the GEMM expands a packed
+ *           weight nibble pair (low nibble = even channel).  The permutation is the same for both
+ *           operands, so every group dot product is unchanged (P:254 Step 1 sums over the
+ *           group).  INT8 outlier group: the int8 codes in natural order (= q8).
+ *   a_csum  int32 [K/128][rows]  sum of the codes of each INT4 group (0 for the outlier group).
+ *           Why this form: tcgen05 has no 4-bit integer MMA kind and converting int32 partials to
+ *           float runs at a quarter of the FP32 rate, so INT4 groups run on kind::f8f6f4 with
+ *           integer-valued E4M3 operands (fp32 accumulator = exact integer partial).  The
+ *           weights are expanded on the SM from the canonical packed nibbles as offset-binary
+ *           bytes (nibble ^ 8, one LOP3 per 4 codes); the offset adds 8 * a_csum to each partial,
+ *           which the GEMM removes in the per-row dequant constant.  The activations are
+ *           expanded once in the quantize kernel instead of once per output tile.
  *   Quantizer: s = 2*max|x|*c/(2^n - 1), evaluated as alpha = fl(fl(2c)/(2^n-1)),
  *   s = fl(amax*alpha) (s = FLT_MIN for an all-zero group), q = clamp(rint_even(fl(x*fl(1/s))),
  *   -2^(n-1), 2^(n-1)-1).
@@ -60,7 +66,7 @@
 extern "C" {
 #endif
 
-#define ATOM_ABI_VERSION 2
+#define ATOM_ABI_VERSION 3
 #define ATOM_GROUP 128
 
 typedef enum {
@@ -88,19 +94,21 @@ typedef enum { ATOM_F16 = 0, ATOM_F32 = 1 } atom_dtype_t;
  *   k_outlier  0 or 128
  *   clip_int4  clipping factor of the INT4 groups, in (0,1]; the paper's 0.9 for activations
  *   clip_int8  clipping factor of the INT8 outlier block, in (0,1]; 1.0
- *   q4, q8, x8, scales  outputs as described above.  scales is required.  q4 (when
- *              K > k_outlier), q8 (when k_outlier == 128) and x8 are each optional (NULL = not
- *              written), but q4 must be NULL when K == k_outlier, q8 must be NULL when
- *              k_outlier == 0, and at least one code output must be given.  The GEMM reads x8;
- *              q4/q8 are the canonical packed storage format (bit-exact with the oracle).
+ *   q4, q8, a_f8, a_csum, scales  outputs as described above.  scales is required.  q4 (when
+ *              K > k_outlier), q8 (when k_outlier == 128) and the pair (a_f8, a_csum) are each
+ *              optional (NULL = not written; a_f8 and a_csum are given together or not at all),
+ *              but q4 must be NULL when K == k_outlier, q8 must be NULL when k_outlier == 0, and
+ *              at least one code output must be given.  q4/q8 are the canonical packed storage
+ *              format (read by atom_w4a4_gemm); a_f8/a_csum the operand form (read by
+ *              atom_w4a4_gemm_f8).  All bit-exact with the oracle.
  *              ldx % 8 == 0 (16-byte rows).
  *   M == 0 is a no-op.
  */
 atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8,
-                                    uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
-                                    void* stream);
+                                    uint8_t* q4, int8_t* q8, uint8_t* a_f8, int32_t* a_csum,
+                                    float* scales, void* stream);
 
 /*
  * NEXT-1: RMSNorm fused with a1 -- the "prior operator" the paper fuses reordering and
@@ -116,8 +124,8 @@ atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_
                                             const void* gamma_f16, float eps,
                                             const int32_t* perm, int64_t K, int32_t k_outlier,
                                             float clip_int4, float clip_int8,
-                                            uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
-                                            void* stream);
+                                            uint8_t* q4, int8_t* q8, uint8_t* a_f8,
+                                            int32_t* a_csum, float* scales, void* stream);
 
 /*
  * NEXT-4 piece: the SwiGLU of a Llama MLP fused with a1 for the down projection (the "prior
@@ -131,8 +139,8 @@ atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_
 atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* up_f16, int64_t M,
                                              int64_t ldx, const int32_t* perm, int64_t K,
                                              int32_t k_outlier, float clip_int4, float clip_int8,
-                                             uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
-                                             void* stream);
+                                             uint8_t* q4, int8_t* q8, uint8_t* a_f8,
+                                             int32_t* a_csum, float* scales, void* stream);
 
 /*
  * a0: offline weight reorder + quantize (Fig 4 P:237 "The weight matrix (W) is statically
@@ -148,38 +156,59 @@ atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
 
 /*
  * a2-a5: fused mixed-precision group GEMM (P:254 Steps 1-3, Fig 6, outliers P:230):
- *     P_t[m][n] = sum_{j in group t} qa[m][j] * qw[n][j]            exact int32 (tensor cores)
+ *     P_t[m][n] = sum_{j in group t} qa[m][j] * qw[n][j]            exact integer (tensor cores)
  *     C[m][n]   = sum_t a_scales[t][m] * w_scales[t][n] * P_t[m][n]  fp32 accumulation
  *   written to c[m*ldc + n] as fp16 (c_dtype = ATOM_F16) or as the fp32 partial sum (ATOM_F32,
  *   for K-sharded tensor parallelism where partials are all-reduced in fp32).
- *   a_x8/a_scales       activations from atom_reorder_quantize (M rows; the x8 operand form)
+ *   a_q4/a_q8/a_scales  activations in the canonical packed format (M rows), as written by
+ *                       atom_reorder_quantize; expanded on the device into the
+ *                       operand form (a_f8, a_csum) in the workspace, then multiplied
  *   w_q4/w_q8/w_scales  weights from atom_quantize_weights (N rows), same perm and K
- *   M >= 0 (M == 0 is a no-op), N % 128 == 0, K % 128 == 0, k_outlier in {0,128},
+ *   M >= 0 (M == 0 is a no-op), N % 128 == 0, K % 128 == 0, k_outlier in {0,128}; a_q4 / w_q4
+ *   are required iff K > k_outlier, a_q8 / w_q8 iff k_outlier == 128.
  *   ldc >= N, ldc % 8 == 0 (an N-shard can write its column block into a wider buffer).
  *   debug_partials  NULL, or int32 [K/128][M][N]: every exact group partial P_t (test-only).
  *   workspace       device buffer of at least atom_w4a4_gemm_workspace_size(M, N, K, k_outlier)
- *                   bytes, 16-byte aligned (may be NULL when that size is 0).  The (tile,
- *                   K-group) work is divided evenly over one persistent CTA per SM ("stream-K"),
- *                   so an output tile may be computed in K segments by consecutive CTAs; the
- *                   segments publish fp32 partials and per-tile arrival counters there and the
- *                   CTA holding the tile's last segment sums them in a fixed order
- *                   (deterministic).  The first atom_w4a4_gemm_counter_bytes() bytes hold
- *                   arrival counters: they MUST be zero before the first use, and every completed
- *                   call leaves them zero again (self-cleaning), so no per-call memset is
- *                   launched and one buffer can serve every shape on the device; the rest is
- *                   scratch.  Must not be shared by calls that may run concurrently, and the
- *                   counters must be re-zeroed if a call was aborted.
+ *                   bytes, 16-byte aligned.  The (tile, K-group) work is divided evenly over one
+ *                   persistent CTA per SM ("stream-K"), so an output tile may be computed in K
+ *                   segments by consecutive CTAs; the segments publish fp32 partials and
+ *                   per-tile arrival counters there and the CTA holding the tile's last segment
+ *                   sums them in a fixed order (deterministic).  The first
+ *                   atom_w4a4_gemm_counter_bytes() bytes hold arrival counters: they MUST be zero
+ *                   before the first use, and every completed call leaves them zero again
+ *                   (self-cleaning), so no per-call memset is launched and one buffer can serve
+ *                   every shape on the device; the rest is scratch.  Must not be shared by calls
+ *                   that may run concurrently, and the counters must be re-zeroed if a call was
+ *                   aborted.
  */
-atom_status_t atom_w4a4_gemm(const int8_t* a_x8, const float* a_scales,
+atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
                              const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
                              int64_t M, int64_t N, int64_t K, int32_t k_outlier,
                              void* c, int64_t ldc, atom_dtype_t c_dtype,
                              int32_t* debug_partials, void* workspace, size_t workspace_bytes,
                              void* stream);
 
+/*
+ * The same GEMM on the activation operand form (a_f8, a_csum) that atom_reorder_quantize writes
+ * in the same pass as the scales: the hot path (quantize -> GEMM) then writes and reads only
+ * what the GEMM consumes.  Same arguments, results (bit for bit) and errors as atom_w4a4_gemm;
+ * a_f8 and a_csum are required.  Workspace: atom_w4a4_gemm_f8_workspace_size bytes (may be 0;
+ * any atom_w4a4_gemm workspace also serves).
+ */
+atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const int32_t* a_csum, const float* a_scales,
+                                const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
+                                int64_t M, int64_t N, int64_t K, int32_t k_outlier,
+                                void* c, int64_t ldc, atom_dtype_t c_dtype,
+                                int32_t* debug_partials, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
 /* Bytes of device workspace atom_w4a4_gemm needs for this shape on the CURRENT device (0 when
- * no output tile is split between CTAs, or when the current device is not an sm_100 GPU). */
+ * the current device is not an sm_100 GPU). */
 size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier);
+
+/* Bytes of device workspace atom_w4a4_gemm_f8 needs (0 when no output tile is split between
+ * CTAs, or when the current device is not an sm_100 GPU). */
+size_t atom_w4a4_gemm_f8_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier);
 
 /* Size of the leading counter region of every GEMM workspace on the CURRENT device (the part
  * that must be zero before first use; 0 when the device is not an sm_100 GPU). */

@@ -29,8 +29,9 @@ ATOM_F16, ATOM_F32 = 0, 1
 # every symbol include/atom.h declares
 ABI_SYMBOLS = ("atom_reorder_quantize", "atom_rmsnorm_reorder_quantize",
                "atom_silu_mul_reorder_quantize", "atom_quantize_weights",
-               "atom_w4a4_gemm",
-               "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_counter_bytes",
+               "atom_w4a4_gemm", "atom_w4a4_gemm_f8",
+               "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_f8_workspace_size",
+               "atom_w4a4_gemm_counter_bytes",
                "atom_validate_perm", "atom_status_string",
                "atom_abi_version", "atom_last_launch_count")
 
@@ -55,18 +56,22 @@ def _lib():
         L = ctypes.CDLL(str(LIB_PATH))
         P, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
         q_args = [P, i64, i64, P, i64, i32, f32, f32, P, P, P, P]
-        L.atom_reorder_quantize.argtypes = q_args[:10] + [P] + q_args[10:]
+        L.atom_reorder_quantize.argtypes = q_args[:10] + [P, P] + q_args[10:]
         L.atom_quantize_weights.argtypes = q_args
         L.atom_rmsnorm_reorder_quantize.argtypes = [P, i64, i64, P, f32] + q_args[3:10] + \
-            [P] + q_args[10:]
+            [P, P] + q_args[10:]
         L.atom_rmsnorm_reorder_quantize.restype = ctypes.c_int
         L.atom_silu_mul_reorder_quantize.argtypes = [P, P, i64, i64] + q_args[3:10] + \
-            [P] + q_args[10:]
+            [P, P] + q_args[10:]
         L.atom_silu_mul_reorder_quantize.restype = ctypes.c_int
-        L.atom_w4a4_gemm.argtypes = [P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int,
-                                     P, P, ctypes.c_size_t, P]
-        L.atom_w4a4_gemm_workspace_size.argtypes = [i64, i64, i64, i32]
-        L.atom_w4a4_gemm_workspace_size.restype = ctypes.c_size_t
+        g_args = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int, P, P,
+                  ctypes.c_size_t, P]
+        L.atom_w4a4_gemm.argtypes = g_args
+        L.atom_w4a4_gemm_f8.argtypes = g_args
+        L.atom_w4a4_gemm_f8.restype = ctypes.c_int
+        for f in (L.atom_w4a4_gemm_workspace_size, L.atom_w4a4_gemm_f8_workspace_size):
+            f.argtypes = [i64, i64, i64, i32]
+            f.restype = ctypes.c_size_t
         L.atom_w4a4_gemm_counter_bytes.restype = ctypes.c_size_t
         L.atom_validate_perm.argtypes = [P, i64, i64, P, P, P]
         L.atom_status_string.argtypes = [ctypes.c_int]
@@ -112,21 +117,45 @@ def _check(st: int, what: str):
 class Quantized:
     """Quantized operand: q4 uint8 [rows][(K-k_o)/2] packed INT4, q8 int8 [rows][k_o] (or None),
     scales fp32 [K/128][rows] (group-major), with the reordered K and k_outlier.  Activations
-    also carry x8 int8 [rows][K]: the same codes one per byte in the GEMM operand order
-    (include/atom.h), which is what atom_w4a4_gemm reads."""
+    may also carry the GEMM operand form (include/atom.h): f8 uint8 [rows][K] (E4M3 codes) and
+    csum int32 [K/128][rows] (group code sums), which atom_w4a4_gemm_f8 reads."""
     q4: object
     q8: object
     scales: object
     K: int
     k_outlier: int
-    x8: object = None
+    f8: object = None
+    csum: object = None
 
     @property
     def rows(self) -> int:
         return int(self.scales.shape[1])
 
 
-def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream, x8=False,
+def _check_quantized(out, rows, K, k_outlier, dev, operand):
+    """Shapes / dtypes of a caller-supplied Quantized (the C ABI sees bare pointers)."""
+    import torch
+    G = K // GROUP
+
+    def want(t, shape, dtype, name):
+        if t is None:
+            return
+        if tuple(t.shape) != shape or t.dtype != dtype or not t.is_contiguous() \
+                or t.device != dev:
+            raise ValueError(f"out.{name}: expected contiguous {dtype} {shape} on {dev}")
+    if out.K != K or out.k_outlier != k_outlier:
+        raise ValueError("out was allocated for another K / k_outlier")
+    want(out.q4, (rows, (K - k_outlier) // 2), torch.uint8, "q4")
+    want(out.q8, (rows, k_outlier), torch.int8, "q8")
+    want(out.scales, (G, rows), torch.float32, "scales")
+    if operand:
+        want(out.f8, (rows, K), torch.uint8, "f8")
+        want(out.csum, (G, rows), torch.int32, "csum")
+    if out.scales is None:
+        raise ValueError("out.scales is required")
+
+
+def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream, operand=False,
               packed=True, norm=None, up=None):
     import torch
     if x.dtype != torch.float16 or x.dim() != 2 or not x.is_cuda:
@@ -137,6 +166,8 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
         raise TypeError("perm must be a contiguous CUDA int32 tensor")
     rows, ld = x.shape[0], x.stride(0)
     K = int(perm.numel()) if K is None else int(K)
+    if K > perm.numel():
+        raise ValueError(f"K = {K} exceeds perm.numel() = {perm.numel()}")
     if out is None:
         dev = x.device
         q4 = torch.empty((rows, (K - k_outlier) // 2), dtype=torch.uint8, device=dev) \
@@ -144,11 +175,14 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
         q8 = torch.empty((rows, k_outlier), dtype=torch.int8, device=dev) \
             if k_outlier and packed else None
         sc = torch.empty((K // GROUP, rows), dtype=torch.float32, device=dev)
-        xx = torch.empty((rows, K), dtype=torch.int8, device=dev) if x8 else None
-        out = Quantized(q4, q8, sc, K, k_outlier, xx)
+        f8 = torch.empty((rows, K), dtype=torch.uint8, device=dev) if operand else None
+        cs = torch.empty((K // GROUP, rows), dtype=torch.int32, device=dev) if operand else None
+        out = Quantized(q4, q8, sc, K, k_outlier, f8, cs)
+    else:
+        _check_quantized(out, rows, K, k_outlier, x.device, operand)
     codes = (_ptr(out.q4), _ptr(out.q8))
     if fn_name != "atom_quantize_weights":
-        codes = codes + (_ptr(out.x8),)
+        codes = codes + (_ptr(out.f8), _ptr(out.csum))
     head = (_ptr(x), rows, ld)
     if up is not None:                        # the up projection of the fused SwiGLU
         if up.dtype != torch.float16 or not up.is_cuda or up.shape != x.shape \
@@ -172,31 +206,33 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
 
 def reorder_quantize(x, perm, K: Optional[int] = None, k_outlier: int = 128,
                      clip_int4: float = 0.9, clip_int8: float = 1.0, out: Quantized = None,
-                     stream=None, packed: bool = True) -> Quantized:
+                     stream=None, packed: bool = True, operand: bool = True) -> Quantized:
     """a1: reorder + dynamically quantize activations x fp16 [M][ldx] (clip 0.9).
 
-    Writes the GEMM operand form x8 and, unless ``packed=False``, the canonical packed q4/q8."""
+    Writes the canonical packed q4/q8 unless ``packed=False`` and the GEMM operand form
+    (f8, csum) unless ``operand=False``."""
     return _quantize("atom_reorder_quantize", x, perm, K, k_outlier, clip_int4, clip_int8, out,
-                     stream, x8=True, packed=packed)
+                     stream, operand=operand, packed=packed)
 
 
 def rmsnorm_reorder_quantize(x, gamma, perm, eps: float = 1e-6, K: Optional[int] = None,
                              k_outlier: int = 128, clip_int4: float = 0.9, clip_int8: float = 1.0,
-                             out: Quantized = None, stream=None, packed: bool = True) -> Quantized:
+                             out: Quantized = None, stream=None, packed: bool = True,
+                             operand: bool = True) -> Quantized:
     """NEXT-1: fp16 RMSNorm of x [M][hidden] (weight gamma fp16 [hidden]) fused with the reorder
     + dynamic quantize of a1 -- the paper's fusion into the prior operator."""
     return _quantize("atom_rmsnorm_reorder_quantize", x, perm, K, k_outlier, clip_int4,
-                     clip_int8, out, stream, x8=True, packed=packed, norm=(gamma, eps))
+                     clip_int8, out, stream, operand=operand, packed=packed, norm=(gamma, eps))
 
 
 def silu_mul_reorder_quantize(gate, up, perm, K: Optional[int] = None, k_outlier: int = 128,
                               clip_int4: float = 0.9, clip_int8: float = 1.0,
-                              out: Quantized = None, stream=None,
-                              packed: bool = True) -> Quantized:
+                              out: Quantized = None, stream=None, packed: bool = True,
+                              operand: bool = True) -> Quantized:
     """NEXT-4 piece: SwiGLU h = silu(gate) * up of a Llama MLP (fp16 [M][I] gate / up projection
     outputs) fused with the reorder + dynamic quantize of the down projection's input."""
     return _quantize("atom_silu_mul_reorder_quantize", gate, perm, K, k_outlier, clip_int4,
-                     clip_int8, out, stream, x8=True, packed=packed, up=up)
+                     clip_int8, out, stream, operand=operand, packed=packed, up=up)
 
 
 def quantize_weights(w, perm, K: Optional[int] = None, k_outlier: int = 128,
@@ -208,6 +244,7 @@ def quantize_weights(w, perm, K: Optional[int] = None, k_outlier: int = 128,
 
 
 def workspace_size(M: int, N: int, K: int, k_outlier: int = 128) -> int:
+    """Workspace bytes of atom_w4a4_gemm (canonical inputs); also serves atom_w4a4_gemm_f8."""
     return int(_lib().atom_w4a4_gemm_workspace_size(M, N, K, k_outlier))
 
 
@@ -221,7 +258,8 @@ _WORKSPACES = {}
 
 def gemm_workspace(M: int, N: int, K: int, k_outlier: int = 128, stream=None):
     """A zero-filled GEMM workspace for this shape, cached per (device, stream): the GEMM leaves
-    it zero-filled after every completed call (include/atom.h), so it is cleared only once."""
+    its counter region zero after every completed call (include/atom.h), so it is cleared only
+    when first allocated."""
     import torch
     n = workspace_size(M, N, K, k_outlier)
     if n == 0:
@@ -237,9 +275,11 @@ def gemm_workspace(M: int, N: int, K: int, k_outlier: int = 128, stream=None):
 
 
 def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partials=None,
-              workspace=None, stream=None):
+              workspace=None, stream=None, canonical: bool = False):
     """a2-a5: C[m][n] = sum_t s_a[t][m] s_w[t][n] P_t[m][n] (fp32 accumulate), fp16 or fp32 out.
 
+    Reads the activation operand form (a.f8, a.csum) through atom_w4a4_gemm_f8 when present,
+    else (or with ``canonical=True``) the packed a.q4 / a.q8 through atom_w4a4_gemm.
     ``out`` may be a wider [M][ldc] view (ldc >= N) to write an N-shard in place.
     ``debug_partials``: optional int32 [K/128][M][N] CUDA tensor receiving every exact partial.
     """
@@ -247,21 +287,39 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
     if a.K != w.K or a.k_outlier != w.k_outlier:
         raise ValueError("activation and weight quantization disagree on K / k_outlier")
     M, N = a.rows, w.rows
+    dev = a.scales.device
     if out is None:
         dt = torch.float16 if out_dtype is None else out_dtype
-        out = torch.empty((M, N), dtype=dt, device=a.scales.device)
-    if out.dtype not in (torch.float16, torch.float32) or out.stride(1) != 1:
-        raise TypeError("out must be fp16/fp32 with contiguous rows")
+        out = torch.empty((M, N), dtype=dt, device=dev)
+    if out.dtype not in (torch.float16, torch.float32) or out.dim() != 2 or out.stride(1) != 1:
+        raise TypeError("out must be a 2-D fp16/fp32 tensor with contiguous rows")
+    if out.shape[0] < M or out.shape[1] < N or out.device != dev:
+        raise ValueError(f"out must be at least [{M}][{N}] on {dev}, got {tuple(out.shape)} "
+                         f"on {out.device}")
+    if debug_partials is not None and (
+            tuple(debug_partials.shape) != (a.K // GROUP, M, N) or
+            debug_partials.dtype != torch.int32 or not debug_partials.is_contiguous() or
+            debug_partials.device != dev):
+        raise ValueError("debug_partials must be a contiguous int32 [K/128][M][N] tensor")
     c_dtype = ATOM_F16 if out.dtype == torch.float16 else ATOM_F32
-    if a.x8 is None:
-        raise ValueError("activations lack the x8 operand form (use reorder_quantize)")
+    use_f8 = a.f8 is not None and not canonical
+    if not use_f8 and (a.q4 is None) != (a.K == a.k_outlier):
+        raise ValueError("activations lack the packed codes (quantize with packed=True)")
     if workspace is None:
         workspace = gemm_workspace(M, N, a.K, a.k_outlier, stream)
-    st = _lib().atom_w4a4_gemm(_ptr(a.x8), _ptr(a.scales), _ptr(w.q4), _ptr(w.q8),
-                               _ptr(w.scales), M, N, a.K, a.k_outlier, _ptr(out), out.stride(0),
-                               c_dtype, _ptr(debug_partials), _ptr(workspace),
-                               0 if workspace is None else workspace.numel(), _stream(stream))
-    _check(st, "atom_w4a4_gemm")
+    wsz = 0 if workspace is None else workspace.numel()
+    if use_f8:
+        st = _lib().atom_w4a4_gemm_f8(_ptr(a.f8), _ptr(a.csum), _ptr(a.scales), _ptr(w.q4),
+                                      _ptr(w.q8), _ptr(w.scales), M, N, a.K, a.k_outlier,
+                                      _ptr(out), out.stride(0), c_dtype, _ptr(debug_partials),
+                                      _ptr(workspace), wsz, _stream(stream))
+        _check(st, "atom_w4a4_gemm_f8")
+    else:
+        st = _lib().atom_w4a4_gemm(_ptr(a.q4), _ptr(a.q8), _ptr(a.scales), _ptr(w.q4),
+                                   _ptr(w.q8), _ptr(w.scales), M, N, a.K, a.k_outlier,
+                                   _ptr(out), out.stride(0), c_dtype, _ptr(debug_partials),
+                                   _ptr(workspace), wsz, _stream(stream))
+        _check(st, "atom_w4a4_gemm")
     return out
 
 

@@ -52,8 +52,8 @@ bool clip_ok(float c) { return c > 0.0f && c <= 1.0f; }
 
 atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
                                int64_t K, int32_t k_o, float clip4, float clip8,
-                               const uint8_t* q4, const int8_t* q8, const int8_t* x8,
-                               const float* scales, bool packed_required) {
+                               const uint8_t* q4, const int8_t* q8, const uint8_t* af8,
+                               const int32_t* csum, const float* scales, bool packed_required) {
   if (rows < 0) return ATOM_ERR_SHAPE;
   if (!(k_o == 0 || k_o == ATOM_GROUP)) return ATOM_ERR_ARG;
   if (K <= 0 || K % ATOM_GROUP != 0 || K < k_o) return ATOM_ERR_SHAPE;
@@ -67,99 +67,53 @@ atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const in
   if ((K == k_o && q4 != nullptr) || (k_o == 0 && q8 != nullptr)) return ATOM_ERR_NULL;
   if (packed_required) {
     if ((K > k_o) != (q4 != nullptr) || (k_o > 0) != (q8 != nullptr)) return ATOM_ERR_NULL;
-  } else if (!q4 && !q8 && !x8) {
+  } else if (!q4 && !q8 && !af8) {
     return ATOM_ERR_NULL;
   }
+  if ((af8 == nullptr) != (csum == nullptr)) return ATOM_ERR_NULL;   // the operand form is a pair
   if (!aligned16(x) || !aligned16(perm) || !aligned16(scales) || (q4 && !aligned16(q4)) ||
-      (q8 && !aligned16(q8)) || (x8 && !aligned16(x8)))
+      (q8 && !aligned16(q8)) || (af8 && !aligned16(af8)) || (csum && !aligned16(csum)))
     return ATOM_ERR_ALIGN;
   return ATOM_OK;
 }
 
 atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
                               int64_t K, int32_t k_o, float clip4, float clip8, uint8_t* q4,
-                              int8_t* q8, int8_t* x8, float* scales, bool packed_required,
+                              int8_t* q8, uint8_t* af8, int32_t* csum, float* scales,
+                              bool packed_required,
                               void* stream, const void* gamma = nullptr, float eps = 0.0f,
                               const void* up = nullptr) {
   g_last_launches = 0;
-  atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, x8, scales,
-                                      packed_required);
+  atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, af8, csum,
+                                      scales, packed_required);
   if (st != ATOM_OK || rows == 0) return st;
   DeviceInfo dev;
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   cudaError_t e = atom::launch_reorder_quantize(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8,
-                                                x8, scales, static_cast<cudaStream_t>(stream),
-                                                dev.num_sms, gamma, eps, up);
+                                                af8, csum, scales,
+                                                static_cast<cudaStream_t>(stream), dev.num_sms,
+                                                gamma, eps, up);
   if (e != cudaSuccess) return ATOM_ERR_CUDA;
   g_last_launches = 1;
   return ATOM_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
-                                    const int32_t* perm, int64_t K, int32_t k_outlier,
-                                    float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
-                                    int8_t* x8, float* scales, void* stream) {
-  return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, x8,
-                         scales, false, stream);
+size_t counter_region(int num_sms) {
+  return ((static_cast<size_t>(num_sms) * sizeof(int) + 255) / 256) * 256;
 }
 
-atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
-                                            const void* gamma_f16, float eps,
-                                            const int32_t* perm, int64_t K, int32_t k_outlier,
-                                            float clip_int4, float clip_int8, uint8_t* q4,
-                                            int8_t* q8, int8_t* x8, float* scales, void* stream) {
-  g_last_launches = 0;
-  if (!(eps >= 0.0f)) return ATOM_ERR_ARG;
-  if (M > 0 && !gamma_f16) return ATOM_ERR_NULL;
-  if (gamma_f16 && !aligned16(gamma_f16)) return ATOM_ERR_ALIGN;
-  return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, x8,
-                         scales, false, stream, gamma_f16, eps);
+// The GEMM's own workspace part (counters + split-tile slots), rounded so the canonical entry's
+// operand area that follows it starts 256-byte aligned; at least the counter region, so one
+// buffer serves both entries.
+size_t gemm_part_bytes(const atom::GemmPlan& pl, int num_sms) {
+  const size_t b = pl.workspace_bytes > 0 ? pl.workspace_bytes : counter_region(num_sms);
+  return ((b + 255) / 256) * 256;
 }
 
-atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* up_f16, int64_t M,
-                                             int64_t ldx, const int32_t* perm, int64_t K,
-                                             int32_t k_outlier, float clip_int4, float clip_int8,
-                                             uint8_t* q4, int8_t* q8, int8_t* x8, float* scales,
-                                             void* stream) {
-  g_last_launches = 0;
-  if (M > 0 && !up_f16) return ATOM_ERR_NULL;
-  if (up_f16 && !aligned16(up_f16)) return ATOM_ERR_ALIGN;
-  return quantize_common(gate_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, x8,
-                         scales, false, stream, nullptr, 0.0f, up_f16);
-}
-
-atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
-                                    const int32_t* perm, int64_t K, int32_t k_outlier,
-                                    float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
-                                    float* scales, void* stream) {
-  return quantize_common(w_f16, N, ldw, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, nullptr,
-                         scales, true, stream);
-}
-
-size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
-  (void)k_outlier;
-  if (M <= 0 || N <= 0 || N % 128 != 0 || K <= 0 || K % ATOM_GROUP != 0) return 0;
-  DeviceInfo dev;
-  if (current_device(&dev) != ATOM_OK) return 0;   // no sm_100 device: the GEMM cannot run
-  return atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
-}
-
-size_t atom_w4a4_gemm_counter_bytes(void) {
-  DeviceInfo dev;
-  if (current_device(&dev) != ATOM_OK) return 0;
-  return ((static_cast<size_t>(dev.num_sms) * sizeof(int) + 255) / 256) * 256;
-}
-
-atom_status_t atom_w4a4_gemm(const int8_t* a_x8, const float* a_scales,
-                             const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
-                             int64_t M, int64_t N, int64_t K, int32_t k_outlier, void* c,
-                             int64_t ldc, atom_dtype_t c_dtype, int32_t* debug_partials,
-                             void* workspace, size_t workspace_bytes, void* stream) {
-  g_last_launches = 0;
+atom_status_t check_gemm_args(const float* a_scales, const uint8_t* w_q4, const int8_t* w_q8,
+                              const float* w_scales, int64_t M, int64_t N, int64_t K,
+                              int32_t k_outlier, const void* c, int64_t ldc, atom_dtype_t c_dtype,
+                              const int32_t* debug_partials) {
   if (M < 0 || N <= 0 || N % 128 != 0) return ATOM_ERR_SHAPE;
   if (!(k_outlier == 0 || k_outlier == ATOM_GROUP)) return ATOM_ERR_ARG;
   if (K <= 0 || K % ATOM_GROUP != 0 || K < k_outlier) return ATOM_ERR_SHAPE;
@@ -167,22 +121,25 @@ atom_status_t atom_w4a4_gemm(const int8_t* a_x8, const float* a_scales,
   if (ldc < N || ldc % 8 != 0) return ATOM_ERR_SHAPE;
   if (!(c_dtype == ATOM_F16 || c_dtype == ATOM_F32)) return ATOM_ERR_ARG;
   if (M == 0) return ATOM_OK;
-  if (!a_x8 || !a_scales || !w_scales || !c) return ATOM_ERR_NULL;
+  if (!a_scales || !w_scales || !c) return ATOM_ERR_NULL;
   const bool has4 = K > k_outlier, has8 = k_outlier > 0;
   if (has4 != (w_q4 != nullptr)) return ATOM_ERR_NULL;
   if (has8 != (w_q8 != nullptr)) return ATOM_ERR_NULL;
-  if (!aligned16(a_scales) || !aligned16(w_scales) || !aligned16(c) || !aligned16(a_x8) ||
-      (w_q4 && !aligned16(w_q4)) ||
-      (w_q8 && !aligned16(w_q8)) || (debug_partials && !aligned16(debug_partials)))
+  if (!aligned16(a_scales) || !aligned16(w_scales) || !aligned16(c) ||
+      (w_q4 && !aligned16(w_q4)) || (w_q8 && !aligned16(w_q8)) ||
+      (debug_partials && !aligned16(debug_partials)))
     return ATOM_ERR_ALIGN;
-  DeviceInfo dev;
-  atom_status_t st = current_device(&dev);
-  if (st != ATOM_OK) return st;
-  const size_t ws = atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
-  if (ws > 0 && (workspace == nullptr || workspace_bytes < ws || !aligned16(workspace)))
-    return ATOM_ERR_WORKSPACE;
+  return ATOM_OK;
+}
+
+cudaError_t run_gemm(const uint8_t* af8, const int32_t* csum, const float* a_scales,
+                     const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales, int64_t M,
+                     int64_t N, int64_t K, int32_t k_outlier, void* c, int64_t ldc,
+                     atom_dtype_t c_dtype, int32_t* debug_partials, void* workspace,
+                     size_t workspace_bytes, void* stream, const DeviceInfo& dev, int* launches) {
   atom::GemmArgs a;
-  a.a_x8 = a_x8;
+  a.a_f8 = af8;
+  a.a_csum = csum;
   a.a_scales = a_scales;
   a.w_q4 = w_q4;
   a.w_q8 = w_q8;
@@ -195,12 +152,134 @@ atom_status_t atom_w4a4_gemm(const int8_t* a_x8, const float* a_scales,
   a.ldc = ldc;
   a.c_f32 = c_dtype == ATOM_F32;
   a.debug_partials = debug_partials;
+  return atom::launch_w4a4_gemm(a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
+                                dev.num_sms, launches);
+}
+
+}  // namespace
+
+extern "C" {
+
+atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
+                                    uint8_t* a_f8, int32_t* a_csum, float* scales, void* stream) {
+  return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, a_f8,
+                         a_csum, scales, false, stream);
+}
+
+atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
+                                            const void* gamma_f16, float eps,
+                                            const int32_t* perm, int64_t K, int32_t k_outlier,
+                                            float clip_int4, float clip_int8, uint8_t* q4,
+                                            int8_t* q8, uint8_t* a_f8, int32_t* a_csum,
+                                            float* scales, void* stream) {
+  g_last_launches = 0;
+  if (!(eps >= 0.0f)) return ATOM_ERR_ARG;
+  if (M > 0 && !gamma_f16) return ATOM_ERR_NULL;
+  if (gamma_f16 && !aligned16(gamma_f16)) return ATOM_ERR_ALIGN;
+  return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, a_f8,
+                         a_csum, scales, false, stream, gamma_f16, eps);
+}
+
+atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* up_f16, int64_t M,
+                                             int64_t ldx, const int32_t* perm, int64_t K,
+                                             int32_t k_outlier, float clip_int4, float clip_int8,
+                                             uint8_t* q4, int8_t* q8, uint8_t* a_f8,
+                                             int32_t* a_csum, float* scales, void* stream) {
+  g_last_launches = 0;
+  if (M > 0 && !up_f16) return ATOM_ERR_NULL;
+  if (up_f16 && !aligned16(up_f16)) return ATOM_ERR_ALIGN;
+  return quantize_common(gate_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, a_f8,
+                         a_csum, scales, false, stream, nullptr, 0.0f, up_f16);
+}
+
+atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
+                                    const int32_t* perm, int64_t K, int32_t k_outlier,
+                                    float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
+                                    float* scales, void* stream) {
+  return quantize_common(w_f16, N, ldw, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, nullptr,
+                         nullptr, scales, true, stream);
+}
+
+size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
+  (void)k_outlier;
+  if (M <= 0 || N <= 0 || N % 128 != 0 || K <= 0 || K % ATOM_GROUP != 0) return 0;
+  DeviceInfo dev;
+  if (current_device(&dev) != ATOM_OK) return 0;   // no sm_100 device: the GEMM cannot run
+  const atom::GemmPlan pl = atom::plan_w4a4_gemm(M, N, K, dev.num_sms);
+  return gemm_part_bytes(pl, dev.num_sms) + atom::expand_bytes(M, K);
+}
+
+size_t atom_w4a4_gemm_f8_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
+  (void)k_outlier;
+  if (M <= 0 || N <= 0 || N % 128 != 0 || K <= 0 || K % ATOM_GROUP != 0) return 0;
+  DeviceInfo dev;
+  if (current_device(&dev) != ATOM_OK) return 0;
+  return atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
+}
+
+size_t atom_w4a4_gemm_counter_bytes(void) {
+  DeviceInfo dev;
+  if (current_device(&dev) != ATOM_OK) return 0;
+  return counter_region(dev.num_sms);
+}
+
+atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const int32_t* a_csum, const float* a_scales,
+                                const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
+                                int64_t M, int64_t N, int64_t K, int32_t k_outlier, void* c,
+                                int64_t ldc, atom_dtype_t c_dtype, int32_t* debug_partials,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  atom_status_t st = check_gemm_args(a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc,
+                                     c_dtype, debug_partials);
+  if (st != ATOM_OK || M == 0) return st;
+  if (!a_f8 || !a_csum) return ATOM_ERR_NULL;
+  if (!aligned16(a_f8) || !aligned16(a_csum)) return ATOM_ERR_ALIGN;
+  DeviceInfo dev;
+  if ((st = current_device(&dev)) != ATOM_OK) return st;
+  const size_t ws = atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
+  if (ws > 0 && (workspace == nullptr || workspace_bytes < ws || !aligned16(workspace)))
+    return ATOM_ERR_WORKSPACE;
   int launches = 0;
-  cudaError_t e = atom::launch_w4a4_gemm(a, workspace, workspace_bytes,
-                                         static_cast<cudaStream_t>(stream), dev.num_sms,
-                                         &launches);
-  if (e != cudaSuccess) return ATOM_ERR_CUDA;
+  if (run_gemm(a_f8, a_csum, a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+               debug_partials, workspace, workspace_bytes, stream, dev, &launches) != cudaSuccess)
+    return ATOM_ERR_CUDA;
   g_last_launches = launches;
+  return ATOM_OK;
+}
+
+atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const float* a_scales,
+                             const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
+                             int64_t M, int64_t N, int64_t K, int32_t k_outlier, void* c,
+                             int64_t ldc, atom_dtype_t c_dtype, int32_t* debug_partials,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  atom_status_t st = check_gemm_args(a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc,
+                                     c_dtype, debug_partials);
+  if (st != ATOM_OK || M == 0) return st;
+  if ((K > k_outlier) != (a_q4 != nullptr) || (k_outlier > 0) != (a_q8 != nullptr))
+    return ATOM_ERR_NULL;
+  if ((a_q4 && !aligned16(a_q4)) || (a_q8 && !aligned16(a_q8))) return ATOM_ERR_ALIGN;
+  DeviceInfo dev;
+  if ((st = current_device(&dev)) != ATOM_OK) return st;
+  const atom::GemmPlan pl = atom::plan_w4a4_gemm(M, N, K, dev.num_sms);
+  const size_t part = gemm_part_bytes(pl, dev.num_sms);
+  const size_t need = part + atom::expand_bytes(M, K);
+  if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
+    return ATOM_ERR_WORKSPACE;
+  // the operand form lives after the GEMM's own part of the workspace
+  uint8_t* af8 = static_cast<uint8_t*>(workspace) + part;
+  int32_t* csum = reinterpret_cast<int32_t*>(af8 + ((static_cast<size_t>(M) * K + 255) / 256) * 256);
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (atom::launch_expand_activations(a_q4, a_q8, M, K, k_outlier, af8, csum, s, dev.num_sms) !=
+      cudaSuccess)
+    return ATOM_ERR_CUDA;
+  int launches = 0;
+  if (run_gemm(af8, csum, a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+               debug_partials, workspace, part, stream, dev, &launches) != cudaSuccess)
+    return ATOM_ERR_CUDA;
+  g_last_launches = launches + 1;
   return ATOM_OK;
 }
 

@@ -2,7 +2,6 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
-#include <cstdlib>
 #include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -12,11 +11,10 @@ namespace atom {
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
 // previous kernel of the stream is finishing; every kernel of this library calls griddep_wait()
 // before touching global memory another kernel may write, so the semantics are those of a plain
-// launch.  ATOM_NO_PDL=1 (development A/B) launches without the attribute.
+// launch.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t stream, Args&&... args) {
-  static const bool off = std::getenv("ATOM_NO_PDL") != nullptr;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -26,14 +24,15 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cfg.attrs = attr;
-  cfg.numAttrs = off ? 0 : 1;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    int8_t* x8, float* scales, cudaStream_t stream, int num_sms,
+                                    uint8_t* af8, int32_t* csum, float* scales,
+                                    cudaStream_t stream, int num_sms,
                                     const void* gamma = nullptr, float eps = 0.0f,
                                     const void* up = nullptr);
 
@@ -41,7 +40,8 @@ cudaError_t launch_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, in
                                  int32_t* ok, cudaStream_t stream);
 
 struct GemmArgs {
-  const int8_t* a_x8;
+  const uint8_t* a_f8;      // activation operand form (include/atom.h "a_f8")
+  const int32_t* a_csum;    // [K/128][M] group code sums
   const float* a_scales;
   const uint8_t* w_q4;
   const int8_t* w_q8;
@@ -55,7 +55,6 @@ struct GemmArgs {
 };
 
 struct GemmPlan {
-  int bt = 256;                 // token tile
   int grid = 0;                 // persistent CTAs (<= SMs)
   int dp_waves = 0;             // whole-tile round-robin waves
   int64_t sk_units = 0;         // (tile, group) units divided evenly after the waves
@@ -66,7 +65,14 @@ struct GemmPlan {
 
 GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms);
 
-// Returns the number of kernel launches (incl. memsets) issued through *launches.
+// Bytes of workspace the canonical entry needs for a_f8 + a_csum (after the GEMM's own part).
+size_t expand_bytes(int64_t M, int64_t K);
+
+cudaError_t launch_expand_activations(const uint8_t* q4, const int8_t* q8, int64_t M, int64_t K,
+                                      int32_t k_outlier, uint8_t* af8, int32_t* csum,
+                                      cudaStream_t stream, int num_sms);
+
+// Returns the number of kernel launches issued through *launches.
 cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,
                              cudaStream_t stream, int num_sms, int* launches);
 

@@ -11,7 +11,8 @@
 // reads shared memory.  One half-warp per 128-channel group: each lane owns 8 reordered
 // channels (two 128-bit perm loads), the group |max| is a 4-step shuffle reduction, codes are
 // packed in registers and written as 64 contiguous bytes (INT4) or 128 bytes (INT8), plus the
-// GEMM operand form x8 (one byte per code, include/atom.h).
+// GEMM operand form a_f8 (one E4M3 byte per code) and the group code sums a_csum
+// (include/atom.h).
 // Numerics are pinned to the oracle's binary32 steps: __fdiv_rn / __fmul_rn / __frcp_rn are
 // IEEE round-to-nearest and never contracted; cvt.rni gives round-half-to-even.
 #include <cfloat>
@@ -52,7 +53,8 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                         const int32_t* __restrict__ perm, int32_t G, int32_t G4,
                         int32_t groups_per_cta, float clip4, float clip8,
                         uint8_t* __restrict__ q4, int8_t* __restrict__ q8,
-                        int8_t* __restrict__ x8, int64_t K, float* __restrict__ scales,
+                        uint8_t* __restrict__ af8, int32_t* __restrict__ csum, int64_t K,
+                        float* __restrict__ scales,
                         const __half* __restrict__ gamma, float eps,
                         const __half* __restrict__ up) {
   constexpr bool kNorm = kPre == 1;
@@ -178,26 +180,40 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                                     0x5410);
     const uint32_t od = __byte_perm(__byte_perm(f[1], f[3], 0x0040), __byte_perm(f[5], f[7], 0x0040),
                                     0x5410);
+    // group code sum (the GEMM's offset-binary correction, include/atom.h "a_csum")
+    int qs = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) qs += static_cast<int>(f[k] - 0x4B400000u);
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, off);
     if (valid) {
-      int8_t* xg = x8 ? x8 + row * K + t * 128 : nullptr;
+      uint8_t* ag = af8 ? af8 + row * K + t * 128 : nullptr;
       if (is_int4) {
         // packed byte j = (q_2j & 0xF) | (q_2j+1 << 4)   (low nibble = even channel)
         if (q4)
           reinterpret_cast<uint32_t*>(q4 + row * row4 + t * 64)[hl] =
               (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
-        if (xg) {
-          // GEMM operand order (atom.h "x8"): channel 32c + 8i + 2b + h of the group sits at
-          // byte 32c + 16h + 4i + b -- the order in which the GEMM unpacks weight nibbles.
+        if (ag) {
+          // GEMM operand: E4M3 sign-magnitude byte of q (value q * 2^-9); channel 32c + 8i +
+          // 2b + h of the group sits at byte 32c + 16h + 4i + b (include/atom.h "a_f8")
+          auto sm4 = [](uint32_t w) {   // 4 two's-complement nibbles (low bits of each byte)
+            const uint32_t n = w & 0x0F0F0F0Fu;
+            const uint32_t neg = (n >> 3) & 0x01010101u;
+            return (((n ^ (neg * 0x0Fu)) + neg) & 0x0F0F0F0Fu) | (neg << 7);
+          };
           const int p = 32 * (hl >> 2) + 4 * (hl & 3);
-          *reinterpret_cast<uint32_t*>(xg + p) = ev;
-          *reinterpret_cast<uint32_t*>(xg + p + 16) = od;
+          *reinterpret_cast<uint32_t*>(ag + p) = sm4(ev);
+          *reinterpret_cast<uint32_t*>(ag + p + 16) = sm4(od);
         }
       } else {
         const uint32_t w0 = __byte_perm(ev, od, 0x5140), w1 = __byte_perm(ev, od, 0x7362);
         if (q8) reinterpret_cast<uint2*>(q8 + row * 128)[hl] = make_uint2(w0, w1);
-        if (xg) reinterpret_cast<uint2*>(xg)[hl] = make_uint2(w0, w1);
+        if (ag) reinterpret_cast<uint2*>(ag)[hl] = make_uint2(w0, w1);
       }
-      if (hl == 0) scales[static_cast<int64_t>(t) * rows + row] = s;
+      if (hl == 0) {
+        scales[static_cast<int64_t>(t) * rows + row] = s;
+        if (csum) csum[static_cast<int64_t>(t) * rows + row] = is_int4 ? qs : 0;
+      }
     }
   }
 }
@@ -205,8 +221,9 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    int8_t* x8, float* scales, cudaStream_t stream, int num_sms,
-                                    const void* gamma, float eps, const void* up) {
+                                    uint8_t* af8, int32_t* csum, float* scales,
+                                    cudaStream_t stream, int num_sms, const void* gamma,
+                                    float eps, const void* up) {
   const int G = static_cast<int>(K / 128);
   const int G4 = static_cast<int>((K - k_outlier) / 128);
   // Enough CTAs to cover the SMs ~4 times; each extra split re-stages the row (from L2).
@@ -225,7 +242,7 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
   }
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
   return launch_pdl(kern, grid, dim3(kQuantThreads), smem, stream, static_cast<const __half*>(x),
-                    rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, x8, K, scales,
+                    rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, af8, csum, K, scales,
                     static_cast<const __half*>(gamma), eps, static_cast<const __half*>(up));
 }
 

@@ -73,9 +73,10 @@ class TensorParallelLinear:
         self.torch = torch
 
     def quantize(self, x, out=None):
+        """a1 on the hot path: writes only what the GEMM reads (the operand form + scales)."""
         return self.atom.reorder_quantize(x, self.perm, K=self.K, k_outlier=self.ko,
                                           clip_int4=self.clip_a, clip_int8=self.clip_int8,
-                                          out=out)
+                                          out=out, packed=False)
 
     def gemm(self, a, out=None):
         dt = self.torch.float16 if self.shard == "n" else self.torch.float32

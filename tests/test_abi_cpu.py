@@ -26,7 +26,8 @@ def declared_symbols():
 
 def test_header_declares_the_three_calls():
     syms = declared_symbols()
-    for s in ("atom_reorder_quantize", "atom_quantize_weights", "atom_w4a4_gemm"):
+    for s in ("atom_reorder_quantize", "atom_quantize_weights", "atom_w4a4_gemm",
+              "atom_w4a4_gemm_f8"):
         assert s in syms
 
 
@@ -45,13 +46,14 @@ def test_sm100a_only_cubin():
                          text=True).stdout
     assert "sm_100a" in out and "sm_90" not in out
     sass = subprocess.run(["cuobjdump", "-sass", str(so)], capture_output=True, text=True).stdout
-    assert "UTCIMMA" in sass       # tcgen05.mma kind::i8
+    assert "UTCIMMA" in sass       # tcgen05.mma kind::i8 (INT8 outlier group)
+    assert "UTCQMMA" in sass       # tcgen05.mma kind::f8f6f4 (INT4 groups as E4M3)
     assert "UTMALDG" in sass       # TMA tile loads
     assert "LDTM" in sass          # tcgen05.ld
 
 
 def test_version_and_status_strings(lib):
-    assert lib.atom_abi_version() == 2
+    assert lib.atom_abi_version() == 3
     for s in range(8):
         assert lib.atom_status_string(s).startswith(b"ATOM_")
 
@@ -59,43 +61,45 @@ def test_version_and_status_strings(lib):
 def test_host_validation_without_device(lib):
     f = ctypes.c_float
     # shape / argument errors are detected before any device query
-    assert lib.atom_reorder_quantize(None, -1, 256, None, 256, 128, f(0.9), f(1.0), None, None,
-                                     None, None, None) == 2
-    assert lib.atom_reorder_quantize(None, 4, 256, None, 200, 128, f(0.9), f(1.0), None, None,
-                                     None, None, None) == 2
-    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 64, f(0.9), f(1.0), None, None,
-                                     None, None, None) == 4
-    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(1.5), f(1.0), None, None,
-                                     None, None, None) == 4
-    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(0.9), f(1.0), None, None,
-                                     None, None, None) == 1
+    z5 = (None,) * 5
+    assert lib.atom_reorder_quantize(None, -1, 256, None, 256, 128, f(0.9), f(1.0), *z5,
+                                     None) == 2
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 200, 128, f(0.9), f(1.0), *z5,
+                                     None) == 2
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 64, f(0.9), f(1.0), *z5,
+                                     None) == 4
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(1.5), f(1.0), *z5,
+                                     None) == 4
+    assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(0.9), f(1.0), *z5,
+                                     None) == 1
     assert lib.atom_quantize_weights(None, 4, 250, None, 256, 128, f(0.85), f(1.0), None, None,
                                      None, None) == 2
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, 4, 100, 256, 128, None, 128, 0,
-                              None, None, 0, None) == 2
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, 4, 128, 256, 128, None, 128, 3,
-                              None, None, 0, None) == 4
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, 4, 128, 256, 128, None, 128, 0,
-                              None, None, 0, None) == 1
+    z6 = (None,) * 6
+    for gemm in (lib.atom_w4a4_gemm, lib.atom_w4a4_gemm_f8):
+        assert gemm(*z6, 4, 100, 256, 128, None, 128, 0, None, None, 0, None) == 2
+        assert gemm(*z6, 4, 128, 256, 128, None, 128, 3, None, None, 0, None) == 4
+        assert gemm(*z6, 4, 128, 256, 128, None, 128, 0, None, None, 0, None) == 1
+        assert gemm(*z6, 4, 128, 256, 128, None, 100, 0, None, None, 0, None) == 2   # ldc < N
+        # M == 0 is a no-op that succeeds without a device
+        assert gemm(*z6, 0, 128, 256, 128, None, 128, 0, None, None, 0, None) == 0
     assert lib.atom_w4a4_gemm_workspace_size(1024, 28672, 8192, 128) == 0
-    # M == 0 is a no-op that succeeds without a device
-    assert lib.atom_w4a4_gemm(None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
-                              None, None, 0, None) == 0
+    assert lib.atom_w4a4_gemm_f8_workspace_size(1024, 28672, 8192, 128) == 0
     assert lib.atom_last_launch_count() == 0
     # fused RMSNorm variant: eps < 0 is an argument error, M == 0 a no-op
     assert lib.atom_rmsnorm_reorder_quantize(None, 4, 256, None, f(-1.0), None, 256, 128, f(0.9),
-                                             f(1.0), None, None, None, None, None) == 4
+                                             f(1.0), *z6) == 4
     assert lib.atom_rmsnorm_reorder_quantize(None, 0, 256, None, f(1e-6), None, 256, 128, f(0.9),
-                                             f(1.0), None, None, None, None, None) == 0
+                                             f(1.0), *z6) == 0
 
 
 def test_silu_mul_quantize_host_validation(lib):
     f = ctypes.c_float
     # missing up projection: a NULL error; M == 0: a no-op; both decided on the host
+    z6 = (None,) * 6
     assert lib.atom_silu_mul_reorder_quantize(None, None, 4, 256, None, 256, 128, f(0.9), f(1.0),
-                                              None, None, None, None, None) == 1
+                                              *z6) == 1
     assert lib.atom_silu_mul_reorder_quantize(None, None, 0, 256, None, 256, 128, f(0.9), f(1.0),
-                                              None, None, None, None, None) == 0
+                                              *z6) == 0
     assert lib.atom_last_launch_count() == 0
 
 

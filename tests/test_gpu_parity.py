@@ -51,26 +51,36 @@ def quant_both(atom, x, perm, K, k_o, clip4, weights=False):
     return q, (o4, o8, osc)
 
 
-def x8_from_packed(o4, o8):
-    """The x8 operand form (include/atom.h) rebuilt from the oracle's packed codes: within each
-    32-channel chunk of an INT4 group, byte 16h + 4i + b holds channel 8i + 2b + h; the INT8
-    outlier group is copied as is.  Independent of the kernels (plain index arithmetic)."""
+def codes_from_packed(o4):
+    """Signed INT4 codes [rows][K - k_o] from packed two's-complement nibbles (low = even)."""
+    lo = (o4 & 0xF).astype(np.int16)
+    hi = (o4 >> 4).astype(np.int16)
+    codes = np.empty((o4.shape[0], o4.shape[1] * 2), dtype=np.int16)
+    codes[:, 0::2], codes[:, 1::2] = lo, hi
+    return np.where(codes >= 8, codes - 16, codes)
+
+
+def f8_from_packed(o4, o8):
+    """The GEMM operand form (include/atom.h "a_f8", "a_csum") rebuilt from the oracle's packed
+    codes with plain index arithmetic, independent of the kernels: INT4 code q as the E4M3 byte
+    of q * 2^-9 (q, or 0x80 | -q when negative); within each 32-channel chunk byte 16h + 4i + b
+    holds channel 8i + 2b + h; the INT8 outlier group copied as is.  csum = per-group code sums
+    of the INT4 groups ([K/128][rows], 0 for the outlier group)."""
     rows = o4.shape[0] if o4.size else o8.shape[0]
-    parts = []
+    parts, sums = [], []
     if o4.size:
-        lo = (o4 & 0xF).astype(np.int16)
-        hi = (o4 >> 4).astype(np.int16)
-        codes = np.empty((rows, o4.shape[1] * 2), dtype=np.int16)
-        codes[:, 0::2], codes[:, 1::2] = lo, hi
-        codes = np.where(codes >= 8, codes - 16, codes).astype(np.int8)
+        codes = codes_from_packed(o4)
         p = np.arange(codes.shape[1])
         c, r = (p % 128) // 32, p % 32
         h, i, b = r // 16, (r % 16) // 4, r % 4
         src = (p // 128) * 128 + 32 * c + 8 * i + 2 * b + h
-        parts.append(codes[:, src])
+        q = codes[:, src]
+        parts.append(np.where(q < 0, 0x80 | (-q), q).astype(np.uint8))
+        sums.append(codes.reshape(rows, -1, 128).sum(axis=2).T)
     if o8 is not None:
-        parts.append(o8)
-    return np.concatenate(parts, axis=1)
+        parts.append(o8.view(np.uint8))
+        sums.append(np.zeros((1, rows), np.int64))
+    return np.concatenate(parts, axis=1), np.concatenate(sums, axis=0).astype(np.int32)
 
 
 def assert_quant_equal(q, ref):
@@ -79,8 +89,10 @@ def assert_quant_equal(q, ref):
         np.testing.assert_array_equal(host(q.q4), o4)
     if o8 is not None and q.q8 is not None:
         np.testing.assert_array_equal(host(q.q8), o8)
-    if q.x8 is not None:
-        np.testing.assert_array_equal(host(q.x8), x8_from_packed(o4, o8))
+    if q.f8 is not None:
+        f8, cs = f8_from_packed(o4, o8)
+        np.testing.assert_array_equal(host(q.f8), f8)
+        np.testing.assert_array_equal(host(q.csum), cs)
     got = host(q.scales)
     np.testing.assert_array_equal(got.view(np.uint32), osc.view(np.uint32))
 
@@ -236,14 +248,14 @@ def test_llama_mlp_w4a4_chain(atom):
 # ----------------------------------------------------------------------------------------------
 # a2-a5: GEMM -- exact partials (debug mode) and tolerance outputs
 # ----------------------------------------------------------------------------------------------
-def run_gemm(atom, X, W, perm, K, k_o, debug=False, out_dtype=None):
+def run_gemm(atom, X, W, perm, K, k_o, debug=False, out_dtype=None, canonical=False):
     import torch
     pd = dev(perm)
     wq = atom.quantize_weights(dev(W), pd, K=K, k_outlier=k_o)
     aq = atom.reorder_quantize(dev(X), pd, K=K, k_outlier=k_o)
     dbg = torch.full((K // 128, X.shape[0], W.shape[0]), -7, dtype=torch.int32,
                      device="cuda") if debug else None
-    c = atom.w4a4_gemm(aq, wq, debug_partials=dbg, out_dtype=out_dtype)
+    c = atom.w4a4_gemm(aq, wq, debug_partials=dbg, out_dtype=out_dtype, canonical=canonical)
     torch.cuda.synchronize()
     return aq, wq, c, dbg
 
@@ -261,12 +273,36 @@ def run_gemm(atom, X, W, perm, K, k_o, debug=False, out_dtype=None):
     (1024, 3200, 1152, 128), # data-parallel waves + stream-K tail, ragged K split points
     (40, 11008, 640, 0),     # BT = 64, many n-tiles, pure INT4, tail segments
 ])
-def test_gemm_partials_bitexact(atom, M, N, K, k_o):
+@pytest.mark.parametrize("canonical", [False, True])
+def test_gemm_partials_bitexact(atom, M, N, K, k_o, canonical):
     X, W, perm = synth.problem(M, N, K, seed=M * 7 + N, k_outlier=k_o)
-    aq, wq, c, dbg = run_gemm(atom, X, W, perm, K, k_o, debug=True)
+    aq, wq, c, dbg = run_gemm(atom, X, W, perm, K, k_o, debug=True, canonical=canonical)
     ref = oracle.quantized_linear(X, perm, W, K, k_o)
     np.testing.assert_array_equal(host(dbg), ref["partials"])
     assert_close_tol(host(c.float()), ref["c"], "C")
+    # the production kernel (no debug stores) gives the same output bits
+    c2 = atom.w4a4_gemm(aq, wq, canonical=canonical)
+    assert __import__("torch").equal(c, c2)
+
+
+def test_gemm_canonical_equals_operand_form(atom):
+    """atom_w4a4_gemm on the packed codes (expanded on the device) and atom_w4a4_gemm_f8 on the
+    quantizer's operand form give identical bits; so does the oracle's packed activation bytes
+    fed straight into the canonical entry."""
+    import torch
+    M, N, K = 200, 1024, 2048
+    X, W, perm = synth.problem(M, N, K, seed=17)
+    pd = dev(perm)
+    wq = atom.quantize_weights(dev(W), pd)
+    aq = atom.reorder_quantize(dev(X), pd)
+    c_f8 = atom.w4a4_gemm(aq, wq)
+    c_can = atom.w4a4_gemm(aq, wq, canonical=True)
+    a4, a8, asc = oracle.quantize_rows(X, perm, K, 128, 0.9, 1.0)
+    ora = atom.Quantized(dev(a4), dev(a8), dev(asc), K, 128)
+    c_ora = atom.w4a4_gemm(ora, wq)
+    torch.cuda.synchronize()
+    assert torch.equal(c_f8, c_can) and torch.equal(c_f8, c_ora)
+    assert_close_tol(host(c_f8.float()), oracle.quantized_linear(X, perm, W, K)["c"], "C")
 
 
 @pytest.mark.parametrize("M", [1, 8, 16, 31, 64, 127, 128, 129, 256, 513])
@@ -278,14 +314,16 @@ def test_gemm_output_config1_family(atom, M):
     assert_close_tol(host(c.float()), ref["c"], f"M={M}")
 
 
-def test_gemm_unit_scale_exact_integer(atom):
-    """P3 on the GPU: clip 1 and integer-valued groups -> C is the exact integer GEMM."""
+@pytest.mark.parametrize("M", [16, 40, 100, 300, 1024])
+def test_gemm_unit_scale_exact_integer(atom, M):
+    """P3 on the GPU, production kernel (no debug stores), fp32 output: clip 1 and integer-valued
+    groups -> C is the exact integer GEMM (every split / tile path must be exact)."""
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).parent))
     from test_oracle_pins import scatter, unit_scale_block
-    rng = np.random.default_rng(1)
-    M, N, K = 40, 256, 1024
+    rng = np.random.default_rng(M)
+    N, K = 768, 1024
     perm = rng.permutation(K).astype(np.int32)
     av, ac = unit_scale_block(rng, M, K, 128)
     wv, wc = unit_scale_block(rng, N, K, 128)
@@ -549,14 +587,15 @@ def test_error_codes_launch_nothing(atom):
         (3, (x.data_ptr() + 2, 4, 256, perm.data_ptr(), 256, 128, f(0.9), f(1.0))),  # misaligned
     ]
     for want, args in cases:
-        st = L.atom_reorder_quantize(*args, q4.data_ptr(), q8.data_ptr(), None, sc.data_ptr(),
-                                     None)
+        st = L.atom_reorder_quantize(*args, q4.data_ptr(), q8.data_ptr(), None, None,
+                                     sc.data_ptr(), None)
         assert st == want, (want, st)
         assert atom.last_launch_count() == 0
     torch.cuda.synchronize()
     assert torch.all(q4 == 0xAB) and torch.all(q8 == 5) and torch.all(sc == 3.0)
     # GEMM: N % 128, ldc < N, bad dtype
-    args = [q8.data_ptr(), sc.data_ptr(), q4.data_ptr(), q8.data_ptr(), sc.data_ptr()]
+    args = [q4.data_ptr(), q8.data_ptr(), sc.data_ptr(), q4.data_ptr(), q8.data_ptr(),
+            sc.data_ptr()]
     out = torch.zeros((4, 256), dtype=torch.float16, device="cuda")
     assert L.atom_w4a4_gemm(*args, 4, 200, 256, 128, out.data_ptr(), 256, 0, None, None, 0,
                             None) == 2
@@ -573,7 +612,9 @@ def test_error_codes_launch_nothing(atom):
 def test_empty_m_is_noop(atom):
     import torch
     L = atom.load()
-    assert L.atom_reorder_quantize(None, 0, 256, None, 256, 128, 0.9, 1.0, None, None, None,
-                                   None, None) == 0
-    assert L.atom_w4a4_gemm(None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
-                            None, None, 0, None) == 0
+    f = __import__("ctypes").c_float
+    assert L.atom_reorder_quantize(None, 0, 256, None, 256, 128, f(0.9), f(1.0), None, None,
+                                   None, None, None, None) == 0
+    for gemm in (L.atom_w4a4_gemm, L.atom_w4a4_gemm_f8):
+        assert gemm(None, None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
+                    None, None, 0, None) == 0
