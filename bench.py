@@ -62,9 +62,9 @@ def algorithmic_bytes(M, N, K, c_bytes=2):
 
 
 def quant_bytes(M, K):
-    """a1 as timed: read X fp16 + perm, write the GEMM operand form (one byte per code) and the
-    per-group code sums and scales (include/atom.h a_f8, a_csum, scales)."""
-    return M * K * 2 + K * 4 + M * K + M * (K // 128) * 8
+    """a1 as timed: read X fp16 + perm, write the GEMM operand form (one byte per code, and the
+    per-row (alpha, beta) pairs) and the scales (include/atom.h a_f8, a_ab, scales)."""
+    return M * K * 2 + K * 4 + M * K + M * (K // 128) * 12
 
 
 # ------------------------------------------------------------------------------------------------

@@ -44,14 +44,20 @@
  *           weight nibble pair (low nibble = even channel).  The permutation is the same for both
  *           operands, so every group dot product is unchanged (P:254 Step 1 sums over the
  *           group).  INT8 outlier group: the int8 codes in natural order (= q8).
- *   a_csum  int32 [K/128][rows]  sum of the codes of each INT4 group (0 for the outlier group).
+ *   a_ab    fp32 [K/128][Mp][2], Mp = rows rounded up to 128: per token and group the dequant
+ *           constants (alpha, beta) = (s * 2^18, RN(-8 ca * s)) for an INT4 group (ca = sum of
+ *           its 128 codes, s its scale) and (s, 0) for the outlier group.  Row order within
+ *           every 32 rows: token 32b + r at position 32b + 4 (r % 8) + r / 8 (so a GEMM thread
+ *           finds its 4 tokens r, r + 8, r + 16, r + 24 in 32 contiguous bytes); rows past
+ *           `rows` are padding (never read for stored outputs).
  *           Why this form: tcgen05 has no 4-bit integer MMA kind and converting int32 partials to
  *           float runs at a quarter of the FP32 rate, so INT4 groups run on kind::f8f6f4 with
  *           integer-valued E4M3 operands (fp32 accumulator = exact integer partial).  The
  *           weights are expanded on the SM from the canonical packed nibbles as offset-binary
- *           bytes (nibble ^ 8, one LOP3 per 4 codes); the offset adds 8 * a_csum to each partial,
- *           which the GEMM removes in the per-row dequant constant.  The activations are
- *           expanded once in the quantize kernel instead of once per output tile.
+ *           bytes (nibble ^ 8, one LOP3 per 4 codes), which adds 8 * ca to each partial; the
+ *           GEMM removes it with h = alpha * P' + beta (P' = 2^-18 (P + 8 ca), the fp32
+ *           accumulator), i.e. h = s * P up to one rounding.  The activations are expanded once
+ *           in the quantize kernel instead of once per output tile.
  *   Quantizer: s = 2*max|x|*c/(2^n - 1), evaluated as alpha = fl(fl(2c)/(2^n-1)),
  *   s = fl(amax*alpha) (s = FLT_MIN for an all-zero group), q = clamp(rint_even(fl(x*fl(1/s))),
  *   -2^(n-1), 2^(n-1)-1).
@@ -94,12 +100,12 @@ typedef enum { ATOM_F16 = 0, ATOM_F32 = 1 } atom_dtype_t;
  *   k_outlier  0 or 128
  *   clip_int4  clipping factor of the INT4 groups, in (0,1]; the paper's 0.9 for activations
  *   clip_int8  clipping factor of the INT8 outlier block, in (0,1]; 1.0
- *   q4, q8, a_f8, a_csum, scales  outputs as described above.  scales is required.  q4 (when
- *              K > k_outlier), q8 (when k_outlier == 128) and the pair (a_f8, a_csum) are each
- *              optional (NULL = not written; a_f8 and a_csum are given together or not at all),
+ *   q4, q8, a_f8, a_ab, scales  outputs as described above.  scales is required.  q4 (when
+ *              K > k_outlier), q8 (when k_outlier == 128) and the pair (a_f8, a_ab) are each
+ *              optional (NULL = not written; a_f8 and a_ab are given together or not at all),
  *              but q4 must be NULL when K == k_outlier, q8 must be NULL when k_outlier == 0, and
  *              at least one code output must be given.  q4/q8 are the canonical packed storage
- *              format (read by atom_w4a4_gemm); a_f8/a_csum the operand form (read by
+ *              format (read by atom_w4a4_gemm); a_f8/a_ab the operand form (read by
  *              atom_w4a4_gemm_f8).  All bit-exact with the oracle.
  *              ldx % 8 == 0 (16-byte rows).
  *   M == 0 is a no-op.
@@ -107,7 +113,7 @@ typedef enum { ATOM_F16 = 0, ATOM_F32 = 1 } atom_dtype_t;
 atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8,
-                                    uint8_t* q4, int8_t* q8, uint8_t* a_f8, int32_t* a_csum,
+                                    uint8_t* q4, int8_t* q8, uint8_t* a_f8, float* a_ab,
                                     float* scales, void* stream);
 
 /*
@@ -125,7 +131,7 @@ atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_
                                             const int32_t* perm, int64_t K, int32_t k_outlier,
                                             float clip_int4, float clip_int8,
                                             uint8_t* q4, int8_t* q8, uint8_t* a_f8,
-                                            int32_t* a_csum, float* scales, void* stream);
+                                            float* a_ab, float* scales, void* stream);
 
 /*
  * NEXT-4 piece: the SwiGLU of a Llama MLP fused with a1 for the down projection (the "prior
@@ -140,7 +146,7 @@ atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* u
                                              int64_t ldx, const int32_t* perm, int64_t K,
                                              int32_t k_outlier, float clip_int4, float clip_int8,
                                              uint8_t* q4, int8_t* q8, uint8_t* a_f8,
-                                             int32_t* a_csum, float* scales, void* stream);
+                                             float* a_ab, float* scales, void* stream);
 
 /*
  * a0: offline weight reorder + quantize (Fig 4 P:237 "The weight matrix (W) is statically
@@ -162,7 +168,7 @@ atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
  *   for K-sharded tensor parallelism where partials are all-reduced in fp32).
  *   a_q4/a_q8/a_scales  activations in the canonical packed format (M rows), as written by
  *                       atom_reorder_quantize; expanded on the device into the
- *                       operand form (a_f8, a_csum) in the workspace, then multiplied
+ *                       operand form (a_f8, a_ab) in the workspace, then multiplied
  *   w_q4/w_q8/w_scales  weights from atom_quantize_weights (N rows), same perm and K
  *   M >= 0 (M == 0 is a no-op), N % 128 == 0, K % 128 == 0, k_outlier in {0,128}; a_q4 / w_q4
  *   are required iff K > k_outlier, a_q8 / w_q8 iff k_outlier == 128.
@@ -189,13 +195,13 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
                              void* stream);
 
 /*
- * The same GEMM on the activation operand form (a_f8, a_csum) that atom_reorder_quantize writes
+ * The same GEMM on the activation operand form (a_f8, a_ab) that atom_reorder_quantize writes
  * in the same pass as the scales: the hot path (quantize -> GEMM) then writes and reads only
- * what the GEMM consumes.  Same arguments, results (bit for bit) and errors as atom_w4a4_gemm;
- * a_f8 and a_csum are required.  Workspace: atom_w4a4_gemm_f8_workspace_size bytes (may be 0;
- * any atom_w4a4_gemm workspace also serves).
+ * what the GEMM consumes.  Same results (bit for bit) and errors as atom_w4a4_gemm; a_f8 and
+ * a_ab are required (the activation scales are inside a_ab).  Workspace:
+ * atom_w4a4_gemm_f8_workspace_size bytes (may be 0; any atom_w4a4_gemm workspace also serves).
  */
-atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const int32_t* a_csum, const float* a_scales,
+atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const float* a_ab,
                                 const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
                                 int64_t M, int64_t N, int64_t K, int32_t k_outlier,
                                 void* c, int64_t ldc, atom_dtype_t c_dtype,

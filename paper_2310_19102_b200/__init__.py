@@ -64,10 +64,9 @@ def _lib():
         L.atom_silu_mul_reorder_quantize.argtypes = [P, P, i64, i64] + q_args[3:10] + \
             [P, P] + q_args[10:]
         L.atom_silu_mul_reorder_quantize.restype = ctypes.c_int
-        g_args = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, ctypes.c_int, P, P,
-                  ctypes.c_size_t, P]
-        L.atom_w4a4_gemm.argtypes = g_args
-        L.atom_w4a4_gemm_f8.argtypes = g_args
+        g_tail = [i64, i64, i64, i32, P, i64, ctypes.c_int, P, P, ctypes.c_size_t, P]
+        L.atom_w4a4_gemm.argtypes = [P] * 6 + g_tail
+        L.atom_w4a4_gemm_f8.argtypes = [P] * 5 + g_tail
         L.atom_w4a4_gemm_f8.restype = ctypes.c_int
         for f in (L.atom_w4a4_gemm_workspace_size, L.atom_w4a4_gemm_f8_workspace_size):
             f.argtypes = [i64, i64, i64, i32]
@@ -118,18 +117,24 @@ class Quantized:
     """Quantized operand: q4 uint8 [rows][(K-k_o)/2] packed INT4, q8 int8 [rows][k_o] (or None),
     scales fp32 [K/128][rows] (group-major), with the reordered K and k_outlier.  Activations
     may also carry the GEMM operand form (include/atom.h): f8 uint8 [rows][K] (E4M3 codes) and
-    csum int32 [K/128][rows] (group code sums), which atom_w4a4_gemm_f8 reads."""
+    ab fp32 [K/128][Mp][2] (per-row dequant constants, Mp = rows rounded up to 128), which
+    atom_w4a4_gemm_f8 reads."""
     q4: object
     q8: object
     scales: object
     K: int
     k_outlier: int
     f8: object = None
-    csum: object = None
+    ab: object = None
 
     @property
     def rows(self) -> int:
         return int(self.scales.shape[1])
+
+
+def ab_rows(rows: int) -> int:
+    """Rows of the a_ab operand per group: rows rounded up to the GEMM's 128-token tile."""
+    return (rows + 127) // 128 * 128
 
 
 def _check_quantized(out, rows, K, k_outlier, dev, operand):
@@ -150,7 +155,7 @@ def _check_quantized(out, rows, K, k_outlier, dev, operand):
     want(out.scales, (G, rows), torch.float32, "scales")
     if operand:
         want(out.f8, (rows, K), torch.uint8, "f8")
-        want(out.csum, (G, rows), torch.int32, "csum")
+        want(out.ab, (G, ab_rows(rows), 2), torch.float32, "ab")
     if out.scales is None:
         raise ValueError("out.scales is required")
 
@@ -176,13 +181,14 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
             if k_outlier and packed else None
         sc = torch.empty((K // GROUP, rows), dtype=torch.float32, device=dev)
         f8 = torch.empty((rows, K), dtype=torch.uint8, device=dev) if operand else None
-        cs = torch.empty((K // GROUP, rows), dtype=torch.int32, device=dev) if operand else None
-        out = Quantized(q4, q8, sc, K, k_outlier, f8, cs)
+        ab = torch.empty((K // GROUP, ab_rows(rows), 2), dtype=torch.float32, device=dev) \
+            if operand else None
+        out = Quantized(q4, q8, sc, K, k_outlier, f8, ab)
     else:
         _check_quantized(out, rows, K, k_outlier, x.device, operand)
     codes = (_ptr(out.q4), _ptr(out.q8))
     if fn_name != "atom_quantize_weights":
-        codes = codes + (_ptr(out.f8), _ptr(out.csum))
+        codes = codes + (_ptr(out.f8), _ptr(out.ab))
     head = (_ptr(x), rows, ld)
     if up is not None:                        # the up projection of the fused SwiGLU
         if up.dtype != torch.float16 or not up.is_cuda or up.shape != x.shape \
@@ -210,7 +216,7 @@ def reorder_quantize(x, perm, K: Optional[int] = None, k_outlier: int = 128,
     """a1: reorder + dynamically quantize activations x fp16 [M][ldx] (clip 0.9).
 
     Writes the canonical packed q4/q8 unless ``packed=False`` and the GEMM operand form
-    (f8, csum) unless ``operand=False``."""
+    (f8, ab) unless ``operand=False``."""
     return _quantize("atom_reorder_quantize", x, perm, K, k_outlier, clip_int4, clip_int8, out,
                      stream, operand=operand, packed=packed)
 
@@ -278,7 +284,7 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
               workspace=None, stream=None, canonical: bool = False):
     """a2-a5: C[m][n] = sum_t s_a[t][m] s_w[t][n] P_t[m][n] (fp32 accumulate), fp16 or fp32 out.
 
-    Reads the activation operand form (a.f8, a.csum) through atom_w4a4_gemm_f8 when present,
+    Reads the activation operand form (a.f8, a.ab) through atom_w4a4_gemm_f8 when present,
     else (or with ``canonical=True``) the packed a.q4 / a.q8 through atom_w4a4_gemm.
     ``out`` may be a wider [M][ldc] view (ldc >= N) to write an N-shard in place.
     ``debug_partials``: optional int32 [K/128][M][N] CUDA tensor receiving every exact partial.
@@ -309,7 +315,7 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
         workspace = gemm_workspace(M, N, a.K, a.k_outlier, stream)
     wsz = 0 if workspace is None else workspace.numel()
     if use_f8:
-        st = _lib().atom_w4a4_gemm_f8(_ptr(a.f8), _ptr(a.csum), _ptr(a.scales), _ptr(w.q4),
+        st = _lib().atom_w4a4_gemm_f8(_ptr(a.f8), _ptr(a.ab), _ptr(w.q4),
                                       _ptr(w.q8), _ptr(w.scales), M, N, a.K, a.k_outlier,
                                       _ptr(out), out.stride(0), c_dtype, _ptr(debug_partials),
                                       _ptr(workspace), wsz, _stream(stream))

@@ -22,8 +22,17 @@ FLAGS = [
 ]
 
 
+STAMP = LIB.with_name("libatom.so.flags")
+
+
+def _extra() -> list:
+    return os.environ.get("ATOM_NVCC_EXTRA", "").split()   # development variants (A/B runs)
+
+
 def _stale() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not STAMP.exists():
+        return True
+    if STAMP.read_text() != " ".join(FLAGS + _extra()):     # built with other flags
         return True
     mt = LIB.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + \
@@ -35,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     tmp = LIB.with_name(f"libatom.so.tmp{os.getpid()}")
-    extra = os.environ.get("ATOM_NVCC_EXTRA", "").split()   # development variants (A/B runs)
+    extra = _extra()
     cmd = [NVCC, *FLAGS, *extra, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / "build.log"
@@ -46,6 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(tmp, LIB)
+    STAMP.write_text(" ".join(FLAGS + extra))
     return LIB
 
 

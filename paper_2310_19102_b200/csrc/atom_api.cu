@@ -53,7 +53,7 @@ bool clip_ok(float c) { return c > 0.0f && c <= 1.0f; }
 atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
                                int64_t K, int32_t k_o, float clip4, float clip8,
                                const uint8_t* q4, const int8_t* q8, const uint8_t* af8,
-                               const int32_t* csum, const float* scales, bool packed_required) {
+                               const float* ab, const float* scales, bool packed_required) {
   if (rows < 0) return ATOM_ERR_SHAPE;
   if (!(k_o == 0 || k_o == ATOM_GROUP)) return ATOM_ERR_ARG;
   if (K <= 0 || K % ATOM_GROUP != 0 || K < k_o) return ATOM_ERR_SHAPE;
@@ -70,27 +70,27 @@ atom_status_t check_quant_args(const void* x, int64_t rows, int64_t ld, const in
   } else if (!q4 && !q8 && !af8) {
     return ATOM_ERR_NULL;
   }
-  if ((af8 == nullptr) != (csum == nullptr)) return ATOM_ERR_NULL;   // the operand form is a pair
+  if ((af8 == nullptr) != (ab == nullptr)) return ATOM_ERR_NULL;   // the operand form is a pair
   if (!aligned16(x) || !aligned16(perm) || !aligned16(scales) || (q4 && !aligned16(q4)) ||
-      (q8 && !aligned16(q8)) || (af8 && !aligned16(af8)) || (csum && !aligned16(csum)))
+      (q8 && !aligned16(q8)) || (af8 && !aligned16(af8)) || (ab && !aligned16(ab)))
     return ATOM_ERR_ALIGN;
   return ATOM_OK;
 }
 
 atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int32_t* perm,
                               int64_t K, int32_t k_o, float clip4, float clip8, uint8_t* q4,
-                              int8_t* q8, uint8_t* af8, int32_t* csum, float* scales,
+                              int8_t* q8, uint8_t* af8, float* ab, float* scales,
                               bool packed_required,
                               void* stream, const void* gamma = nullptr, float eps = 0.0f,
                               const void* up = nullptr) {
   g_last_launches = 0;
-  atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, af8, csum,
+  atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, af8, ab,
                                       scales, packed_required);
   if (st != ATOM_OK || rows == 0) return st;
   DeviceInfo dev;
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   cudaError_t e = atom::launch_reorder_quantize(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8,
-                                                af8, csum, scales,
+                                                af8, ab, scales,
                                                 static_cast<cudaStream_t>(stream), dev.num_sms,
                                                 gamma, eps, up);
   if (e != cudaSuccess) return ATOM_ERR_CUDA;
@@ -110,10 +110,9 @@ size_t gemm_part_bytes(const atom::GemmPlan& pl, int num_sms) {
   return ((b + 255) / 256) * 256;
 }
 
-atom_status_t check_gemm_args(const float* a_scales, const uint8_t* w_q4, const int8_t* w_q8,
-                              const float* w_scales, int64_t M, int64_t N, int64_t K,
-                              int32_t k_outlier, const void* c, int64_t ldc, atom_dtype_t c_dtype,
-                              const int32_t* debug_partials) {
+atom_status_t check_gemm_args(const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
+                              int64_t M, int64_t N, int64_t K, int32_t k_outlier, const void* c,
+                              int64_t ldc, atom_dtype_t c_dtype, const int32_t* debug_partials) {
   if (M < 0 || N <= 0 || N % 128 != 0) return ATOM_ERR_SHAPE;
   if (!(k_outlier == 0 || k_outlier == ATOM_GROUP)) return ATOM_ERR_ARG;
   if (K <= 0 || K % ATOM_GROUP != 0 || K < k_outlier) return ATOM_ERR_SHAPE;
@@ -121,26 +120,24 @@ atom_status_t check_gemm_args(const float* a_scales, const uint8_t* w_q4, const 
   if (ldc < N || ldc % 8 != 0) return ATOM_ERR_SHAPE;
   if (!(c_dtype == ATOM_F16 || c_dtype == ATOM_F32)) return ATOM_ERR_ARG;
   if (M == 0) return ATOM_OK;
-  if (!a_scales || !w_scales || !c) return ATOM_ERR_NULL;
+  if (!w_scales || !c) return ATOM_ERR_NULL;
   const bool has4 = K > k_outlier, has8 = k_outlier > 0;
   if (has4 != (w_q4 != nullptr)) return ATOM_ERR_NULL;
   if (has8 != (w_q8 != nullptr)) return ATOM_ERR_NULL;
-  if (!aligned16(a_scales) || !aligned16(w_scales) || !aligned16(c) ||
+  if (!aligned16(w_scales) || !aligned16(c) ||
       (w_q4 && !aligned16(w_q4)) || (w_q8 && !aligned16(w_q8)) ||
       (debug_partials && !aligned16(debug_partials)))
     return ATOM_ERR_ALIGN;
   return ATOM_OK;
 }
 
-cudaError_t run_gemm(const uint8_t* af8, const int32_t* csum, const float* a_scales,
-                     const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales, int64_t M,
+cudaError_t run_gemm(const uint8_t* af8, const float* ab, const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales, int64_t M,
                      int64_t N, int64_t K, int32_t k_outlier, void* c, int64_t ldc,
                      atom_dtype_t c_dtype, int32_t* debug_partials, void* workspace,
                      size_t workspace_bytes, void* stream, const DeviceInfo& dev, int* launches) {
   atom::GemmArgs a;
   a.a_f8 = af8;
-  a.a_csum = csum;
-  a.a_scales = a_scales;
+  a.a_ab = ab;
   a.w_q4 = w_q4;
   a.w_q8 = w_q8;
   a.w_scales = w_scales;
@@ -163,35 +160,35 @@ extern "C" {
 atom_status_t atom_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
-                                    uint8_t* a_f8, int32_t* a_csum, float* scales, void* stream) {
+                                    uint8_t* a_f8, float* a_ab, float* scales, void* stream) {
   return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, a_f8,
-                         a_csum, scales, false, stream);
+                         a_ab, scales, false, stream);
 }
 
 atom_status_t atom_rmsnorm_reorder_quantize(const void* x_f16, int64_t M, int64_t ldx,
                                             const void* gamma_f16, float eps,
                                             const int32_t* perm, int64_t K, int32_t k_outlier,
                                             float clip_int4, float clip_int8, uint8_t* q4,
-                                            int8_t* q8, uint8_t* a_f8, int32_t* a_csum,
+                                            int8_t* q8, uint8_t* a_f8, float* a_ab,
                                             float* scales, void* stream) {
   g_last_launches = 0;
   if (!(eps >= 0.0f)) return ATOM_ERR_ARG;
   if (M > 0 && !gamma_f16) return ATOM_ERR_NULL;
   if (gamma_f16 && !aligned16(gamma_f16)) return ATOM_ERR_ALIGN;
   return quantize_common(x_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, a_f8,
-                         a_csum, scales, false, stream, gamma_f16, eps);
+                         a_ab, scales, false, stream, gamma_f16, eps);
 }
 
 atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* up_f16, int64_t M,
                                              int64_t ldx, const int32_t* perm, int64_t K,
                                              int32_t k_outlier, float clip_int4, float clip_int8,
                                              uint8_t* q4, int8_t* q8, uint8_t* a_f8,
-                                             int32_t* a_csum, float* scales, void* stream) {
+                                             float* a_ab, float* scales, void* stream) {
   g_last_launches = 0;
   if (M > 0 && !up_f16) return ATOM_ERR_NULL;
   if (up_f16 && !aligned16(up_f16)) return ATOM_ERR_ALIGN;
   return quantize_common(gate_f16, M, ldx, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, a_f8,
-                         a_csum, scales, false, stream, nullptr, 0.0f, up_f16);
+                         a_ab, scales, false, stream, nullptr, 0.0f, up_f16);
 }
 
 atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
@@ -225,24 +222,24 @@ size_t atom_w4a4_gemm_counter_bytes(void) {
   return counter_region(dev.num_sms);
 }
 
-atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const int32_t* a_csum, const float* a_scales,
-                                const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
-                                int64_t M, int64_t N, int64_t K, int32_t k_outlier, void* c,
-                                int64_t ldc, atom_dtype_t c_dtype, int32_t* debug_partials,
-                                void* workspace, size_t workspace_bytes, void* stream) {
+atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const float* a_ab, const uint8_t* w_q4,
+                                const int8_t* w_q8, const float* w_scales, int64_t M, int64_t N,
+                                int64_t K, int32_t k_outlier, void* c, int64_t ldc,
+                                atom_dtype_t c_dtype, int32_t* debug_partials, void* workspace,
+                                size_t workspace_bytes, void* stream) {
   g_last_launches = 0;
-  atom_status_t st = check_gemm_args(a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc,
-                                     c_dtype, debug_partials);
+  atom_status_t st = check_gemm_args(w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+                                     debug_partials);
   if (st != ATOM_OK || M == 0) return st;
-  if (!a_f8 || !a_csum) return ATOM_ERR_NULL;
-  if (!aligned16(a_f8) || !aligned16(a_csum)) return ATOM_ERR_ALIGN;
+  if (!a_f8 || !a_ab) return ATOM_ERR_NULL;
+  if (!aligned16(a_f8) || !aligned16(a_ab)) return ATOM_ERR_ALIGN;
   DeviceInfo dev;
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   const size_t ws = atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
   if (ws > 0 && (workspace == nullptr || workspace_bytes < ws || !aligned16(workspace)))
     return ATOM_ERR_WORKSPACE;
   int launches = 0;
-  if (run_gemm(a_f8, a_csum, a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+  if (run_gemm(a_f8, a_ab, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
                debug_partials, workspace, workspace_bytes, stream, dev, &launches) != cudaSuccess)
     return ATOM_ERR_CUDA;
   g_last_launches = launches;
@@ -255,12 +252,14 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
                              int64_t ldc, atom_dtype_t c_dtype, int32_t* debug_partials,
                              void* workspace, size_t workspace_bytes, void* stream) {
   g_last_launches = 0;
-  atom_status_t st = check_gemm_args(a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc,
-                                     c_dtype, debug_partials);
+  atom_status_t st = check_gemm_args(w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+                                     debug_partials);
   if (st != ATOM_OK || M == 0) return st;
+  if (!a_scales) return ATOM_ERR_NULL;
   if ((K > k_outlier) != (a_q4 != nullptr) || (k_outlier > 0) != (a_q8 != nullptr))
     return ATOM_ERR_NULL;
-  if ((a_q4 && !aligned16(a_q4)) || (a_q8 && !aligned16(a_q8))) return ATOM_ERR_ALIGN;
+  if ((a_q4 && !aligned16(a_q4)) || (a_q8 && !aligned16(a_q8)) || !aligned16(a_scales))
+    return ATOM_ERR_ALIGN;
   DeviceInfo dev;
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   const atom::GemmPlan pl = atom::plan_w4a4_gemm(M, N, K, dev.num_sms);
@@ -270,13 +269,13 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
     return ATOM_ERR_WORKSPACE;
   // the operand form lives after the GEMM's own part of the workspace
   uint8_t* af8 = static_cast<uint8_t*>(workspace) + part;
-  int32_t* csum = reinterpret_cast<int32_t*>(af8 + ((static_cast<size_t>(M) * K + 255) / 256) * 256);
+  float* ab = reinterpret_cast<float*>(af8 + ((static_cast<size_t>(M) * K + 255) / 256) * 256);
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (atom::launch_expand_activations(a_q4, a_q8, M, K, k_outlier, af8, csum, s, dev.num_sms) !=
-      cudaSuccess)
+  if (atom::launch_expand_activations(a_q4, a_q8, a_scales, M, K, k_outlier, af8, ab, s,
+                                      dev.num_sms) != cudaSuccess)
     return ATOM_ERR_CUDA;
   int launches = 0;
-  if (run_gemm(af8, csum, a_scales, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+  if (run_gemm(af8, ab, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
                debug_partials, workspace, part, stream, dev, &launches) != cudaSuccess)
     return ATOM_ERR_CUDA;
   g_last_launches = launches + 1;

@@ -18,7 +18,9 @@
 //                    codes (low nibbles) / SHF + LOP3 (high nibbles)
 //     The fp32 accumulator then holds P' = 2^-18 (P_t + 8 ca), exactly (|P_t + 8 ca| < 2^15), where
 //     P_t is the exact integer group partial and ca = sum of the group's activation codes of the
-//     token (a_csum, also written by the quantize kernel).
+//     token.  The quantize kernel also writes, per token and group, alpha = s_a * 2^18 and
+//     beta = RN(-8 ca * s_a) (include/atom.h "a_ab"), in a row order that gives each epilogue
+//     thread its 4 rows in two 16-byte loads.
 //   * INT8 outlier group: kind::i8 on the canonical int8 codes, int32 accumulator (one kind
 //     switch per tile).
 //   * Epilogue (8 warps, 16x256b TMEM loads: a thread holds 4 token rows x 32 channel columns of
@@ -33,6 +35,7 @@
 //     last segment adds them in a fixed order (deterministic).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 #include <cuda.h>
@@ -56,14 +59,34 @@ constexpr int kNumUnpackWarps = 4;
 constexpr int kEpiWarp0 = 8;
 constexpr int kNumEpiWarps = 8;
 constexpr int kEpiThreads = kNumEpiWarps * 32;
-constexpr int kRegsProd = 24, kRegsUnpack = 56, kRegsHigh = 216;   // 128*(24+56) + 256*216 = 65536
+constexpr int kRegsProd = 32, kRegsUnpack = 56, kRegsHigh = 208;   // 128*(32+56) + 256*208 <= 65536
 constexpr int kTileM = 128;     // tokens per tile (MMA M, TMEM lanes)
 constexpr int kTileN = 256;     // output channels per tile (MMA N, TMEM columns)
+#ifndef ATOM_RW
+#define ATOM_RW 2
+#endif
+#ifndef ATOM_KS
+#define ATOM_KS 4
+#endif
+#ifndef ATOM_LDX
+#define ATOM_LDX 2
+#endif
 constexpr int kRS = 4;          // activation slots (= go / mdone ring)
-constexpr int kRW = 2;          // expanded weight slots
+constexpr int kRW = ATOM_RW;    // expanded weight slots
 constexpr int kRT = 2;          // TMEM accumulator buffers (kTileN columns each)
-constexpr int kKS = 4;          // packed INT4 weight stages (one group: kTileN x 64 B)
-constexpr int kLdX = 2;         // 8-column chunks per 16x256b TMEM load
+constexpr int kKS = ATOM_KS;    // packed INT4 weight stages (one group: kTileN x 64 B)
+constexpr int kLdX = ATOM_LDX;  // 8-column chunks per 16x256b TMEM load
+// development timing probes (results wrong by design; only with -DATOM_PROBE_MODE=n):
+// bit 0 = the weight expansion moves no data; bit 1 = the epilogue skips its arithmetic;
+// bit 2 = the epilogue also skips its TMEM loads; bit 3 = the epilogue keeps the first group's
+// scales (no per-group scale loads)
+#ifndef ATOM_PROBE_MODE
+#define ATOM_PROBE_MODE 0
+#endif
+#ifndef ATOM_LD_AHEAD
+#define ATOM_LD_AHEAD 1
+#endif
+constexpr int kLdAhead = ATOM_LD_AHEAD;   // TMEM loads in flight ahead of the one being used
 constexpr uint32_t kTmemCols = kRT * kTileN;
 // split-tile partial of one CTA: [epi warps][32 float4][32 lanes]
 constexpr size_t kSlotFloats = static_cast<size_t>(kNumEpiWarps) * 128 * 32;
@@ -71,25 +94,43 @@ static_assert(kTmemCols <= 512, "TMEM holds at most 512 columns");
 static_assert(kRS >= kRT && kRS >= kRW, "ring sizes");
 
 struct GemmParams {
-  const float* a_scales;     // [G][M]
-  const int32_t* a_csum;     // [G][M] sum of the group's activation codes (INT4 groups)
+  const float* a_ab;         // [G][Mp][2] per-row dequant constants (include/atom.h "a_ab")
   const float* w_scales;     // [G][N]
   void* c;
   int64_t ldc;
   int32_t* debug;
   int M, N, G, G4, c_f32;
+  int Mp;                    // rows of a_ab per group (M rounded up to 128)
   int m_tiles;
   int dp_waves;              // whole tiles per CTA dealt round-robin
   int64_t sk_base;           // first stream-K unit (= dp_waves * grid * G)
   int64_t sk_units;          // stream-K (tile, group) units
   float* partials;           // [gridDim.x][kSlotFloats] split-tile partials
   int* counters;             // [gridDim.x] arrivals per reducing CTA (zero between launches)
+#ifdef ATOM_DEV_PROBES
+  long long* trace;          // development timeline probe: [kTraceEv][kTraceN] clock64 of CTA 0
+#endif
 };
+
+#ifdef ATOM_DEV_PROBES
+// Development-only timeline probe (never in the shipped library): clock64 of event ev for group
+// g of CTA 0.  Built with ATOM_NVCC_EXTRA=-DATOM_DEV_PROBES, enabled by ATOM_GEMM_TRACE=1.
+constexpr int kTraceN = 512, kTraceEv = 25;
+#define TRACE(ev, g)                                                                      \
+  do {                                                                                    \
+    if (p.trace != nullptr && blockIdx.x == 0 && (g) < kTraceN)                           \
+      p.trace[(ev) * kTraceN + (g)] = clock64();                                          \
+  } while (0)
+#else
+#define TRACE(ev, g) \
+  do {               \
+  } while (0)
+#endif
 
 struct __align__(1024) GemmSmem {
   uint8_t a[kRS][kTileM * 128];          // activation group, E4M3 / int8, SW128 K-major (TMA)
   uint8_t w[kRW][kTileN * 128];          // expanded weight group, SW128 K-major
-  uint8_t stage[kKS][kTileN * 64];       // packed INT4 weight group (TMA, no swizzle)
+  uint8_t stage[kKS][kTileN * 64];       // packed weight group (TMA, no swizzle)
   uint64_t full[kKS], empty[kKS];
   // go[u]: group g (slot u = g % kRS) may be issued -- its weights are expanded (4 arrivals),
   // its activations landed (1 arrival + tx bytes) and its TMEM buffer was drained (8 epilogue
@@ -180,6 +221,17 @@ __device__ __forceinline__ Item get_item(const GemmParams& p, const Sched& s, in
   return it;
 }
 
+// Waits of the roles off the MMA <-> epilogue critical loop (producer, activation loader,
+// weight expansion): hardware-suspended try_wait, so they do not take issue slots from the
+// epilogue warps of their SM sub-partition.
+__device__ __forceinline__ void wait_off(uint64_t* bar, uint32_t parity) {
+#if defined(ATOM_SPIN_OFF)
+  mbar_wait_test(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 // ring position: slot index + phase parity, advanced one step at a time (no division)
 template <int N>
 struct Ring {
@@ -196,6 +248,9 @@ __device__ __forceinline__ float2 ldg_f2(const float* p) {
   float2 v;
   asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
   return v;
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 __device__ __forceinline__ float2 u2f2(uint32_t a, uint32_t b) {
   return make_float2(__uint_as_float(a), __uint_as_float(b));
@@ -241,90 +296,129 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   // setmaxnreg sits at the top of each warpgroup's branch, so ptxas allocates every role's code
   // with its own register budget
   if (warp < kUnpackWarp0) {
-  setmaxnreg_dec<kRegsProd>();
-  if (warp == 0) {
-    // ===================== producer: packed INT4 weight groups (TMA) =====================
-    if (lane == 0) {
-      Ring<kKS> st;
-      const uint64_t pol_w = l2_policy_evict_first();
-      if (n_items > 0) {   // PDL: warm L2 with the first weight groups while the previous kernel ends
-        const Item w = get_item(p, sch, 0);
-        for (int t = w.t0, s = 0; t < w.t1 && t < G4 && s < kKS; ++t, ++s)
-          tma_prefetch_2d(&tm_wq4, t * 64, w.n0);
-      }
-      griddep_wait();
-      for (int k = 0; k < n_items; ++k) {
-        const Item w = get_item(p, sch, k);
-        const int te = w.t1 < G4 ? w.t1 : G4;
-        for (int t = w.t0; t < te; ++t, st.next()) {
-          mbar_wait(&sm.empty[st.i], st.ph ^ 1);
-          mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
-          // read by the m-tiles of this n-tile at about the same time, then dead
-          tma_load_2d_hint(sm.stage[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
+    setmaxnreg_dec<kRegsProd>();
+    if (warp == 0) {
+      // ===================== producer: packed weight groups (TMA) =====================
+      // INT4 group: one stage [256 rows][64 B]; INT8 group: two stages (bytes 0-63, 64-127).
+      if (lane == 0) {
+        Ring<kKS> st;
+        const uint64_t pol_w = l2_policy_evict_first();
+        if (n_items > 0) {   // PDL: warm L2 with the first weight groups while the previous ends
+          const Item w = get_item(p, sch, 0);
+          for (int t = w.t0, s = 0; t < w.t1 && t < G4 && s < kKS; ++t, ++s)
+            tma_prefetch_2d(&tm_wq4, t * 64, w.n0);
         }
-      }
-    }
-  } else if (warp == kALoaderWarp) {
-    // ===================== activation-tile loader (single thread) =====================
-    // Slot u is free exactly when the MMAs of the group that used it complete.
-    if (lane == 0) {
-      Ring<kRS> u;
-      const uint64_t pol_a = l2_policy_evict_last();
-      griddep_wait();                    // the activation tiles come from the previous kernel
-      for (int k = 0; k < n_items; ++k) {
-        const Item w = get_item(p, sch, k);
-        for (int t = w.t0; t < w.t1; ++t, u.next()) {
-          mbar_wait_test(&sm.mdone[u.i], u.ph ^ 1);
-          mbar_arrive_expect_tx(&sm.go[u.i], kTileM * 128);
-          // re-read by every n-tile: keep in L2
-          tma_load_2d_hint(sm.a[u.i], &tm_af8, &sm.go[u.i], t * 128, w.m0, pol_a);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ===================== MMA issuer (single thread) =====================
-    // Every instruction this thread executes between dispatches idles the tensor pipe for as
-    // long (tcgen05.mma issue returns only as the previous dispatch drains), so the loop is one
-    // barrier probe, 4 dispatches and one commit per group.
-    if (lane == 0) {
-      constexpr uint32_t id4 = umma_idesc_e4m3(kTileM, kTileN);
-      constexpr uint32_t id8 = umma_idesc_i8(kTileM, kTileN);
-      const uint64_t da0 = umma_desc_sw128(smem_u32(sm.a[0]));
-      const uint64_t db0 = umma_desc_sw128(smem_u32(sm.w[0]));
-      Ring<kRS> u;
-      Ring<kRW> uw;
-      Ring<kRT> b;
-      for (int k = 0; k < n_items; ++k) {
-        const Item w = get_item(p, sch, k);
-        for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), b.next()) {
-          mbar_wait_test(&sm.go[u.i], u.ph);
-          tc_fence_after();
-          const uint32_t d = tmem + b.i * kTileN;
-          // descriptor start address field counts 16-byte units: slot, K step kk (32 bytes)
-          const uint64_t da = da0 + u.i * (kTileM * 128 / 16);
-          const uint64_t db = db0 + uw.i * (kTileN * 128 / 16);
-          if (t < G4) {
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) umma_e4m3(d, da + 2 * kk, db + 2 * kk, id4, kk > 0);
-          } else {
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) umma_i8(d, da + 2 * kk, db + 2 * kk, id8, kk > 0);
+        griddep_wait();
+        int gp = 0;
+        for (int k = 0; k < n_items; ++k) {
+          const Item w = get_item(p, sch, k);
+          for (int t = w.t0; t < w.t1; ++t, ++gp) {
+            const int nst = t < G4 ? 1 : 2;
+            for (int h = 0; h < nst; ++h, st.next()) {
+              mbar_wait(&sm.empty[st.i], st.ph ^ 1);
+              TRACE(0, gp);
+              mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
+              // read by the m-tiles of this n-tile at about the same time, then dead
+              if (t < G4)
+                tma_load_2d_hint(sm.stage[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
+              else
+                tma_load_2d_hint(sm.stage[st.i], &tm_wq8, &sm.full[st.i], h * 64, w.n0, pol_w);
+            }
           }
-          umma_commit(&sm.mdone[u.i]);
+        }
+      }
+    } else if (warp == kALoaderWarp) {
+      // ===================== activation-tile loader (single thread) =====================
+      // Slot u is free exactly when the MMAs of the group that used it complete.  The group's
+      // scales (weight scales of the tile's channels, activation scales and code sums of its
+      // tokens) are prefetched into L2 at the same time, kRS groups ahead of the epilogue that
+      // reads them with plain loads.
+      if (lane == 0) {
+        Ring<kRS> u;
+        const uint64_t pol_a = l2_policy_evict_last();
+        griddep_wait();                  // activations and scales come from the previous kernel
+        int ga = 0;
+        for (int k = 0; k < n_items; ++k) {
+          const Item w = get_item(p, sch, k);
+          const uint32_t sw_bytes = static_cast<uint32_t>(min(kTileN, p.N - w.n0)) * 4;
+          for (int t = w.t0; t < w.t1; ++t, u.next(), ++ga) {
+            wait_off(&sm.mdone[u.i], u.ph ^ 1);
+            TRACE(1, ga);
+            mbar_arrive_expect_tx(&sm.go[u.i], kTileM * 128);
+            // re-read by every n-tile: keep in L2
+            tma_load_2d_hint(sm.a[u.i], &tm_af8, &sm.go[u.i], t * 128, w.m0, pol_a);
+            prefetch_l2_bulk(p.w_scales + static_cast<int64_t>(t) * p.N + w.n0, sw_bytes);
+            prefetch_l2_bulk(p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + w.m0), kTileM * 8);
+          }
+        }
+      }
+#ifdef ATOM_DEV_PROBES
+    } else if (warp == 3) {
+      // development probe: observe every group's MMA completion (event 8)
+      if (lane == 0 && p.trace != nullptr && blockIdx.x == 0) {
+        Ring<kRS> u;
+        int go_ = 0;
+        for (int k = 0; k < n_items; ++k) {
+          const Item w = get_item(p, sch, k);
+          for (int t = w.t0; t < w.t1; ++t, u.next(), ++go_) {
+            mbar_wait_spin(&sm.mdone[u.i], u.ph);
+            TRACE(8, go_);
+          }
+        }
+      }
+#endif
+    } else if (warp == 1) {
+      // ===================== MMA issuer (single thread) =====================
+      // Every instruction this thread executes between dispatches idles the tensor pipe for as
+      // long (tcgen05.mma issue returns only as the previous dispatch drains), so the loop is
+      // one barrier probe, 4 dispatches and one commit per group.
+      if (lane == 0) {
+        constexpr uint32_t id4 = umma_idesc_e4m3(kTileM, kTileN);
+        constexpr uint32_t id8 = umma_idesc_i8(kTileM, kTileN);
+        const uint64_t da0 = umma_desc_sw128(smem_u32(sm.a[0]));
+        const uint64_t db0 = umma_desc_sw128(smem_u32(sm.w[0]));
+        Ring<kRS> u;
+        Ring<kRW> uw;
+        Ring<kRT> b;
+        int gm = 0;
+        for (int k = 0; k < n_items; ++k) {
+          const Item w = get_item(p, sch, k);
+          for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), b.next(), ++gm) {
+            mbar_wait_test(&sm.go[u.i], u.ph);
+            TRACE(3, gm);
+            tc_fence_after();
+            const uint32_t d = tmem + b.i * kTileN;
+            // descriptor start address field counts 16-byte units: slot, K step kk (32 bytes)
+            const uint64_t da = da0 + u.i * (kTileM * 128 / 16);
+            const uint64_t db = db0 + uw.i * (kTileN * 128 / 16);
+            if (t < G4) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) umma_e4m3(d, da + 2 * kk, db + 2 * kk, id4, kk > 0);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) umma_i8(d, da + 2 * kk, db + 2 * kk, id8, kk > 0);
+            }
+            umma_commit(&sm.mdone[u.i]);
+          }
         }
       }
     }
-  }
   } else if (warp < kEpiWarp0) {
     setmaxnreg_dec<kRegsUnpack>();
-    // ===================== weight expansion: packed INT4 -> E4M3 offset-binary, SW128 =====
-    // 128 threads: thread ut owns packed 16-byte chunk c = ut & 3 of rows r0 + 32k, k < 8
-    // (r0 = ut >> 2; all its rows share one swizzle phase).  The INT8 group is TMA'd straight
-    // into the operand slot (its rows are 128 bytes, one SW128 row).
+    // ===================== weight expansion -> E4M3 offset-binary / int8, SW128 =============
+    // 128 threads: thread ut owns 16-byte chunk c = ut & 3 of the 64-byte stage rows
+    // r0 + 32k, k < 8 (r0 = ut >> 2).  Weight row r of the tile goes to operand row
+    // j(r) = 128 (r / 128) + 8 ((r % 32) / 2) + 2 ((r / 32) % 4) + r % 2, so that TMEM column j
+    // holds output channel r and a 16x256b-loading epilogue thread (columns 8k + 2 (lane % 4)
+    // + {0,1}) owns 32 consecutive output channels (contiguous scales and stores).  The
+    // swizzle phase of row j is (2 k + r0 % 2) & 7 (k < 4): the two rows a quarter-warp writes have
+    // phases of opposite parity, so the stores are bank-conflict-free.
     const int ut = threadIdx.x - kUnpackWarp0 * 32;
     const uint32_t r0 = static_cast<uint32_t>(ut) >> 2, c = static_cast<uint32_t>(ut) & 3u;
-    const uint32_t r7 = r0 & 7u;
-    const uint32_t olo = ((2 * c) ^ r7) << 4, ohi = ((2 * c + 1) ^ r7) << 4;
+#ifndef ATOM_PERM
+#define ATOM_PERM 0
+#endif
+    const uint32_t jb = ATOM_PERM ? 8 * (r0 >> 1) + (r0 & 1) : r0;   // operand row of k = 0
     uint32_t m0f = 0x0F0F0F0Fu, x08 = 0x08080808u;
     asm volatile("" : "+r"(m0f), "+r"(x08));   // keep the LOP3 constants in registers
     Ring<kKS> st;
@@ -337,46 +431,62 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       const Item w = get_item(p, sch, k);
       for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), ++gu) {
         if (gu >= kRW) {                 // MMAs of group g - kRW finished with this slot
-          mbar_wait_test(&sm.mdone[lag.i], lag.ph);
+          wait_off(&sm.mdone[lag.i], lag.ph);
           lag.next();
         }
+        if (ut == 0) TRACE(2, gu);
+        uint8_t* dst = sm.w[uw.i];
         if (t < G4) {
-          mbar_wait_test(&sm.full[st.i], st.ph);
+          wait_off(&sm.full[st.i], st.ph);
           const uint8_t* src = sm.stage[st.i] + r0 * 64 + c * 16;
-          uint8_t* dst = sm.w[uw.i] + r0 * 128;
+          // all 8 shared-memory loads first: their latency grows several-fold while the tensor
+          // core streams operands, so it is paid once per group
+          uint4 v[8];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint4 v[4];
+          for (int j = 0; j < 8; ++j)
+            if constexpr ((ATOM_PROBE_MODE & 1) == 0)
+              v[j] = *reinterpret_cast<const uint4*>(src + j * 32 * 64);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              v[j] = *reinterpret_cast<const uint4*>(src + (4 * h + j) * 32 * 64);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint8_t* d = dst + (4 * h + j) * 32 * 128;
-              *reinterpret_cast<uint4*>(d + olo) =
-                  make_uint4(lop_and_xor(v[j].x, m0f, x08), lop_and_xor(v[j].y, m0f, x08),
-                             lop_and_xor(v[j].z, m0f, x08), lop_and_xor(v[j].w, m0f, x08));
-              *reinterpret_cast<uint4*>(d + ohi) =
-                  make_uint4(lop_and_xor(v[j].x >> 4, m0f, x08),
-                             lop_and_xor(v[j].y >> 4, m0f, x08),
-                             lop_and_xor(v[j].z >> 4, m0f, x08),
-                             lop_and_xor(v[j].w >> 4, m0f, x08));
-            }
+          for (int j = 0; j < 8; ++j) {
+            if constexpr ((ATOM_PROBE_MODE & 1) != 0) break;
+            const uint32_t row = ATOM_PERM ? 128 * (j >> 2) + jb + 2 * (j & 3) : jb + 32 * j;
+            const uint32_t ph = ATOM_PERM ? (2 * (j & 3) + (r0 & 1)) & 7 : r0 & 7;
+            uint8_t* d = dst + row * 128;
+            *reinterpret_cast<uint4*>(d + (((2 * c) ^ ph) << 4)) =
+                make_uint4(lop_and_xor(v[j].x, m0f, x08), lop_and_xor(v[j].y, m0f, x08),
+                           lop_and_xor(v[j].z, m0f, x08), lop_and_xor(v[j].w, m0f, x08));
+            *reinterpret_cast<uint4*>(d + (((2 * c + 1) ^ ph) << 4)) =
+                make_uint4(lop_and_xor(v[j].x >> 4, m0f, x08), lop_and_xor(v[j].y >> 4, m0f, x08),
+                           lop_and_xor(v[j].z >> 4, m0f, x08), lop_and_xor(v[j].w >> 4, m0f, x08));
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[st.i]);
           st.next();
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.go[u.i]);
-        } else if (lane == 0) {
-          if (warp == kUnpackWarp0) {
-            mbar_arrive_expect_tx(&sm.go[u.i], kTileN * 128);
-            tma_load_2d(sm.w[uw.i], &tm_wq8, &sm.go[u.i], 0, w.n0);
-          } else {
-            mbar_arrive(&sm.go[u.i]);
+        } else {
+          // INT8 outlier group: bytes 0-63 of each row in one stage, 64-127 in the next; copied
+          // with the same row permutation
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            wait_off(&sm.full[st.i], st.ph);
+            const uint8_t* src = sm.stage[st.i] + r0 * 64 + c * 16;
+            uint4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = *reinterpret_cast<const uint4*>(src + j * 32 * 64);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t row = ATOM_PERM ? 128 * (j >> 2) + jb + 2 * (j & 3) : jb + 32 * j;
+              const uint32_t ph = ATOM_PERM ? (2 * (j & 3) + (r0 & 1)) & 7 : r0 & 7;
+              *reinterpret_cast<uint4*>(dst + row * 128 + (((4 * h + c) ^ ph) << 4)) = v[j];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[st.i]);
+            st.next();
           }
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (ut == 0) TRACE(4, gu);
+        if (lane == 0) mbar_arrive(&sm.go[u.i]);
       }
     }
   } else {
@@ -387,61 +497,59 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     const int half = e >> 2;             // column half
     const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * 128;
     const int rl = q * 32 + (lane >> 2);           // + 8 ri: the thread's 4 tile rows
-    const int cl = half * 128 + 2 * (lane & 3);    // + 8 k: the thread's 16 column pairs
-    griddep_wait();                      // scales come from the previous kernel
+    // + 2k (+1): its 16 channel pairs (ATOM_PERM: 32 consecutive channels)
+    const int cl = half * 128 + (ATOM_PERM ? 32 : 2) * (lane & 3);
+    constexpr int kPairStride = ATOM_PERM ? 2 : 8;   // channel distance of consecutive pairs
+    griddep_wait();
     if (lane == 0)                       // the first kRT groups find their TMEM buffers free
       for (int b = 0; b < kRT; ++b) mbar_arrive(&sm.go[b % kRS]);
 
-    // scales of the group being drained: 16 column-pair weight scales and per-row alpha / beta,
-    // refilled one group ahead (the column scales block by block as they fall free)
+    // scales of the group being drained: 16 channel-pair weight scales and per-row alpha /
+    // beta, loaded (LDG: unaffected by the tensor core's shared-memory traffic, unlike LDS)
+    // one group ahead, the weight scales block by block as their registers fall free.  The
+    // right half of a partial n-tile (N % 256 == 128) reads the left half's scales (its
+    // outputs are never stored); rows past M are clamped (separate, rarely taken path).
+    const int cl_ld = cl - ((half == 1 && (p.N & 255) != 0) ? 128 : 0);
     float2 sw[16];
     float al[4], be[4];
-    int cs_dbg[4];
-    auto load_sw = [&](int t, int n0, int k0, int nk) {
-      const float* ws = p.w_scales + static_cast<int64_t>(t) * p.N;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (k < k0 || k >= k0 + nk) continue;
-        const int n = n0 + cl + 8 * k;
-        sw[k] = ldg_f2(ws + (n < p.N ? n : p.N - 2));
-      }
+    auto sw_base = [&](int t, int n0) {
+      return p.w_scales + static_cast<int64_t>(t) * p.N + n0 + ((n0 + kTileN <= p.N) ? cl : cl_ld);
     };
-    auto load_rows = [&](int t, int m0, float* sa, int* cs) {
+    auto load_sw = [&](const float* ws, int k0, int nk) {   // channel pairs k0 .. k0+nk (even)
 #pragma unroll
-      for (int ri = 0; ri < 4; ++ri) {
-        const int m = m0 + rl + 8 * ri;
-        const int64_t o = static_cast<int64_t>(t) * p.M + (m < p.M ? m : p.M - 1);
-        sa[ri] = __ldg(p.a_scales + o);
-        cs[ri] = t < G4 ? __ldg(p.a_csum + o) : 0;
-      }
-    };
-    auto make_ab = [&](int t, const float* sa, const int* cs) {
-#pragma unroll
-      for (int ri = 0; ri < 4; ++ri) {
-        if (t < G4) {
-          al[ri] = sa[ri] * 262144.0f;                              // s_a * 2^18, exact
-          be[ri] = __fmul_rn(static_cast<float>(-8 * cs[ri]), sa[ri]);
-        } else {
-          al[ri] = sa[ri];
-          be[ri] = 0.0f;
+      for (int k = 0; k < 16; k += 2)
+        if (k >= k0 && k < k0 + nk) {
+          if constexpr (ATOM_PERM) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(ws) + k / 2);
+            sw[k] = make_float2(v.x, v.y);
+            sw[k + 1] = make_float2(v.z, v.w);
+          } else {
+            sw[k] = ldg_f2(ws + 8 * k);
+            sw[k + 1] = ldg_f2(ws + 8 * k + 8);
+          }
         }
-        if constexpr (kDebug) cs_dbg[ri] = cs[ri];
-      }
+    };
+    // per-row alpha / beta of rows rl + 8 ri: two 16-byte loads (a_ab row order)
+    auto load_ab = [&](int t, int m0, float* a, float* bb) {
+      const float4* pa = reinterpret_cast<const float4*>(
+          p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + m0 + q * 32 + 4 * (lane >> 2)));
+      const float4 v0 = __ldg(pa), v1 = __ldg(pa + 1);
+      a[0] = v0.x; bb[0] = v0.y; a[1] = v0.z; bb[1] = v0.w;
+      a[2] = v1.x; bb[2] = v1.y; a[3] = v1.z; bb[3] = v1.w;
     };
     if (n_items > 0) {
       const Item w0 = get_item(p, sch, 0);
-      float sa[4];
-      int cs[4];
-      load_rows(w0.t0, w0.m0, sa, cs);
-      load_sw(w0.t0, w0.n0, 0, 16);
-      make_ab(w0.t0, sa, cs);
+      load_ab(w0.t0, w0.m0, al, be);
+      load_sw(sw_base(w0.t0, w0.n0), 0, 16);
     }
     Ring<kRS> u;
     Ring<kRT> b;
+    int ge = 0;
     for (int k = 0; k < n_items; ++k) {
       const Item w = get_item(p, sch, k);
-      // first group of the next item (the scales are prefetched across the item boundary)
-      int nt0 = -1, nn0 = 0, nm0 = 0;
+      // first group of the next item (after the last group, "next" is the last group itself:
+      // harmless reloads, no branches)
+      int nt0 = w.t1 - 1, nn0 = w.n0, nm0 = w.m0;
       if (k + 1 < n_items) {
         const Item wn = get_item(p, sch, k + 1);
         nt0 = wn.t0;
@@ -453,48 +561,62 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       for (int ri = 0; ri < 4; ++ri)
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[ri][j] = make_float2(0.0f, 0.0f);
-      for (int t = w.t0; t < w.t1; ++t, u.next(), b.next()) {
+      for (int t = w.t0; t < w.t1; ++t, u.next(), b.next(), ++ge) {
         const bool last = t + 1 >= w.t1;
-        const int xt = last ? nt0 : t + 1;     // next group (-1: none)
+        const int xt = last ? nt0 : t + 1;     // next group
         const int xn0 = last ? nn0 : w.n0, xm0 = last ? nm0 : w.m0;
-        float sa_n[4];
-        int cs_n[4];
-        if (xt >= 0) load_rows(xt, xm0, sa_n, cs_n);
+        const float* xws = sw_base(xt, xn0);
+        float al_n[4], be_n[4];
+        if constexpr ((ATOM_PROBE_MODE & 32) == 0) load_ab(xt, xm0, al_n, be_n);
         mbar_wait_test(&sm.mdone[u.i], u.ph);
+        if (e == 0 && lane == 0) TRACE(5, ge);
+        if (lane == 0) TRACE(17 + e, ge);
         tc_fence_after();
         const uint32_t taddr = tq + b.i * kTileN;
         const uint32_t go_next = u.i + kRT >= kRS ? u.i + kRT - kRS : u.i + kRT;
         // loads j = 2 cb + hh: 16 lanes (half hh of the quarter) x kLdX chunks (block cb),
-        // software-pipelined one load ahead
+        // software-pipelined kLdAhead loads ahead
         auto drain = [&](auto int4_tag) {
           constexpr bool kInt4 = decltype(int4_tag)::value;
           constexpr int NL = 2 * (16 / kLdX);
-          uint32_t r[2][4 * kLdX];
+          constexpr int NB = kLdAhead + 1;               // load buffers in flight
+          uint32_t r[NB][4 * kLdX];
           auto ld = [&](int j, uint32_t* dst) {
             const int hh = j & 1, cb = j >> 1;
-            tmem_ld_16x256b<kLdX>(
-                taddr + (static_cast<uint32_t>(16 * hh) << 16) + 8 * kLdX * cb, dst);
+            if constexpr ((ATOM_PROBE_MODE & 4) != 0) {
+#pragma unroll
+              for (int v = 0; v < 4 * kLdX; ++v) dst[v] = taddr + v + j;
+            } else {
+              tmem_ld_16x256b<kLdX>(
+                  taddr + (static_cast<uint32_t>(16 * hh) << 16) + 8 * kLdX * cb, dst);
+            }
           };
-          ld(0, r[0]);
+#pragma unroll
+          for (int j = 0; j < kLdAhead; ++j) ld(j, r[j]);
 #pragma unroll
           for (int j = 0; j < NL; ++j) {
-            uint32_t* rv = r[j & 1];
-            if (j + 1 < NL) {
-              ld(j + 1, r[(j + 1) & 1]);
-              // keep load j's registers live across the issue of load j + 1 (two buffers in
-              // flight; the LDTM destination registers are scoreboarded)
+            uint32_t* rv = r[j % NB];
+            if (j + kLdAhead < NL) {
+              ld(j + kLdAhead, r[(j + kLdAhead) % NB]);
+              // keep the registers of the loads in flight live across this issue (the LDTM
+              // destination registers are scoreboarded)
 #pragma unroll
-              for (int v = 0; v < 4 * kLdX; ++v) asm volatile("" : "+r"(rv[v]));
-            } else {                                   // all loads issued: release the buffer
+              for (int a = 0; a < kLdAhead; ++a)
+#pragma unroll
+                for (int v = 0; v < 4 * kLdX; ++v) asm volatile("" : "+r"(r[(j + a) % NB][v]));
+            }
+            if (j + kLdAhead == NL) {                  // all loads issued: release the buffer
               tmem_ld_wait();
               tc_fence_before();
               __syncwarp();
+              if (e == 0 && lane == 0) TRACE(6, ge);
+              if (lane == 0) TRACE(9 + e, ge);
               if (lane == 0) mbar_arrive(&sm.go[go_next]);
             }
             const int hh = j & 1, cb = j >> 1;
 #pragma unroll
             for (int ch = 0; ch < kLdX; ++ch) {
-              const int kc = cb * kLdX + ch;           // column-pair index of this chunk
+              const int kc = cb * kLdX + ch;           // channel-pair index of this chunk
 #pragma unroll
               for (int s = 0; s < 2; ++s) {            // tile row 2 hh + s
                 const int ri = 2 * hh + s;
@@ -506,12 +628,15 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                                    __int2float_rn(static_cast<int>(x1)));
                 if constexpr (kDebug) {
                   const int m = w.m0 + rl + 8 * ri;
-                  const int n = w.n0 + cl + 8 * kc;
+                  const int n = w.n0 + cl + kPairStride * kc;
                   if (m < p.M && n < p.N) {
                     int p0, p1;
                     if constexpr (kInt4) {   // P = P' * 2^18 - 8 ca, exact
-                      p0 = __float2int_rn(pv.x * 262144.0f) - 8 * cs_dbg[ri];
-                      p1 = __float2int_rn(pv.y * 262144.0f) - 8 * cs_dbg[ri];
+                      // ca = -beta / (8 s_a) rounded: beta = RN(-8 ca s_a) is within 2^-11 s_a
+                      const int ca = __double2int_rn(-static_cast<double>(be[ri]) * 32768.0 /
+                                                     static_cast<double>(al[ri]));
+                      p0 = __float2int_rn(pv.x * 262144.0f) - 8 * ca;
+                      p1 = __float2int_rn(pv.y * 262144.0f) - 8 * ca;
                     } else {
                       p0 = static_cast<int>(x0);
                       p1 = static_cast<int>(x1);
@@ -521,23 +646,35 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                     dp[1] = p1;
                   }
                 }
+                if constexpr ((ATOM_PROBE_MODE & 2) != 0) {
+                  acc[ri][kc].x += pv.x;
+                  continue;
+                }
                 const float2 h = __ffma2_rn(pv, make_float2(al[ri], al[ri]),
                                             make_float2(be[ri], be[ri]));
                 acc[ri][kc] = __ffma2_rn(sw[kc], h, acc[ri][kc]);
               }
             }
-            // block cb done for both lane halves: its column scales are free for the next group
-            if (hh == 1 && xt >= 0) load_sw(xt, xn0, cb * kLdX, kLdX);
+            // block cb done for both lane halves: its channel scales are free for the next group
+            if constexpr ((ATOM_PROBE_MODE & 16) == 0)
+              if (hh == 1) load_sw(xws, cb * kLdX, kLdX);
           }
         };
         if (t < G4) drain(std::true_type{});
         else drain(std::false_type{});
-        if (xt >= 0) make_ab(xt, sa_n, cs_n);
+#pragma unroll
+        for (int ri = 0; ri < 4; ++ri) {
+          if constexpr ((ATOM_PROBE_MODE & 32) == 0) {
+            al[ri] = al_n[ri];
+            be[ri] = be_n[ri];
+          }
+        }
+        if (e == 0 && lane == 0) TRACE(7, ge);
       }
 
       // ---- split tile: every segment but the tile's last publishes its fp32 partial; the CTA
       //      holding the last segment adds the others (in CTA order, deterministic) ----
-      // fragment i (float4) of this thread: row i / 8, column pairs 2 (i % 8), 2 (i % 8) + 1
+      // fragment i (float4) of this thread: row i / 8, channel pairs 2 (i % 8), 2 (i % 8) + 1
       if (w.t1 < p.G || w.t0 > 0) {
         auto frag = [&](float* slot, int i) {
           return reinterpret_cast<float4*>(slot) + (e * 32 + i) * 32 + lane;
@@ -578,22 +715,47 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         }
       }
 
-      // ---- tile output: row m0 + rl + 8 ri, columns n0 + cl + 8 k (+1) ----
+      // ---- tile output: rows m0 + rl + 8 ri, 32 consecutive channels n0 + cl .. +32 ----
       if (w.n0 + half * 128 >= p.N) continue;          // right half of a partial n-tile
 #pragma unroll
       for (int ri = 0; ri < 4; ++ri) {
         const int m = w.m0 + rl + 8 * ri;
         if (m >= p.M) continue;
-        if (!p.c_f32) {
-          __half2* crow = reinterpret_cast<__half2*>(static_cast<__half*>(p.c) +
-                                                     static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
-#pragma unroll
-          for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = __float22half2_rn(acc[ri][kc]);
-        } else {
-          float2* crow = reinterpret_cast<float2*>(static_cast<float*>(p.c) +
+        if constexpr (ATOM_PERM) {
+          if (!p.c_f32) {
+            uint4* crow = reinterpret_cast<uint4*>(static_cast<__half*>(p.c) +
                                                    static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
 #pragma unroll
-          for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = acc[ri][kc];
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              __half2 h0 = __float22half2_rn(acc[ri][4 * v]), h1 = __float22half2_rn(acc[ri][4 * v + 1]);
+              __half2 h2 = __float22half2_rn(acc[ri][4 * v + 2]), h3 = __float22half2_rn(acc[ri][4 * v + 3]);
+              o.x = *reinterpret_cast<uint32_t*>(&h0);
+              o.y = *reinterpret_cast<uint32_t*>(&h1);
+              o.z = *reinterpret_cast<uint32_t*>(&h2);
+              o.w = *reinterpret_cast<uint32_t*>(&h3);
+              crow[v] = o;
+            }
+          } else {
+            float4* crow = reinterpret_cast<float4*>(static_cast<float*>(p.c) +
+                                                     static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              crow[v] = make_float4(acc[ri][2 * v].x, acc[ri][2 * v].y, acc[ri][2 * v + 1].x,
+                                    acc[ri][2 * v + 1].y);
+          }
+        } else {
+          if (!p.c_f32) {
+            __half2* crow = reinterpret_cast<__half2*>(static_cast<__half*>(p.c) +
+                                                       static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
+#pragma unroll
+            for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = __float22half2_rn(acc[ri][kc]);
+          } else {
+            float2* crow = reinterpret_cast<float2*>(static_cast<float*>(p.c) +
+                                                     static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
+#pragma unroll
+            for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = acc[ri][kc];
+          }
         }
       }
     }
@@ -608,12 +770,14 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 }
 
 // ---------------------------------------------------------------------------------------------
-// activation operand expansion (canonical packed codes -> a_f8 + a_csum), for atom_w4a4_gemm
+// activation operand expansion (canonical packed codes + scales -> a_f8 + a_ab), for
+// atom_w4a4_gemm
 // ---------------------------------------------------------------------------------------------
 // One thread per 16-byte packed chunk (32 codes) of an INT4 group, 4 threads per group: the
 // two's-complement nibbles become E4M3 sign-magnitude bytes (value q * 2^-9) in the a_f8 order
 // (within each 32-channel chunk the even channels first, then the odd ones); the group's code
-// sum is reduced over the 4 threads.  INT8 outlier group: the codes are copied.
+// sum is reduced over the 4 threads and turned into (alpha, beta).  INT8 outlier group: the
+// codes are copied, (alpha, beta) = (s_a, 0).
 __device__ __forceinline__ uint32_t nib_to_sm(uint32_t n) {
   // n: 4 bytes, each a two's-complement nibble in its low 4 bits
   const uint32_t neg = (n >> 3) & 0x01010101u;            // 1 per negative byte
@@ -632,8 +796,8 @@ __device__ __forceinline__ int nib_sum(uint32_t n) {     // sum of 4 two's-compl
 
 __global__ void __launch_bounds__(256)
 expand_activations_kernel(const uint8_t* __restrict__ q4, const int8_t* __restrict__ q8,
-                          int64_t M, int G, int G4, uint8_t* __restrict__ af8,
-                          int32_t* __restrict__ csum) {
+                          const float* __restrict__ scales, int64_t M, int64_t Mp, int G, int G4,
+                          uint8_t* __restrict__ af8, float* __restrict__ ab) {
   griddep_wait();
   griddep_launch();
   const int64_t K = static_cast<int64_t>(G) * 128;
@@ -671,7 +835,15 @@ expand_activations_kernel(const uint8_t* __restrict__ q4, const int8_t* __restri
     // all 4 threads of a group are consecutive lanes of one warp (4 | 32)
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (c == 0) csum[static_cast<int64_t>(t) * M + m] = t < G4 ? s : 0;
+    if (c == 0) {
+      const float sa = scales[static_cast<int64_t>(t) * M + m];
+      const int64_t r = m & 31;
+      const int64_t pos = (m - r) + 4 * (r & 7) + (r >> 3);     // a_ab row order
+      float2 v;
+      if (t < G4) v = make_float2(sa * 262144.0f, __fmul_rn(static_cast<float>(-8 * s), sa));
+      else v = make_float2(sa, 0.0f);
+      reinterpret_cast<float2*>(ab)[static_cast<int64_t>(t) * Mp + pos] = v;
+    }
   }
 }
 
@@ -755,21 +927,22 @@ GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms) {
   return pl;
 }
 
+int64_t ab_rows(int64_t M) { return ((M + kTileM - 1) / kTileM) * kTileM; }
+
 size_t expand_bytes(int64_t M, int64_t K) {
   const size_t f8 = ((static_cast<size_t>(M) * K + 255) / 256) * 256;
-  const size_t cs = ((static_cast<size_t>(M) * (K / 128) * 4 + 255) / 256) * 256;
-  return f8 + cs;
+  return f8 + static_cast<size_t>(ab_rows(M)) * (K / 128) * 8;
 }
 
-cudaError_t launch_expand_activations(const uint8_t* q4, const int8_t* q8, int64_t M, int64_t K,
-                                      int32_t k_outlier, uint8_t* af8, int32_t* csum,
-                                      cudaStream_t stream, int num_sms) {
+cudaError_t launch_expand_activations(const uint8_t* q4, const int8_t* q8, const float* scales,
+                                      int64_t M, int64_t K, int32_t k_outlier, uint8_t* af8,
+                                      float* ab, cudaStream_t stream, int num_sms) {
   const int G = static_cast<int>(K / 128), G4 = static_cast<int>((K - k_outlier) / 128);
   const int64_t threads = M * G * 4;
   int64_t blocks = (threads + 255) / 256;
   if (blocks > 8LL * num_sms) blocks = 8LL * num_sms;
   return launch_pdl(expand_activations_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0,
-                    stream, q4, q8, M, G, G4, af8, csum);
+                    stream, q4, q8, scales, M, ab_rows(M), G, G4, af8, ab);
 }
 
 cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,
@@ -788,13 +961,13 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   const void* w8 = k_o ? static_cast<const void*>(a.w_q8) : static_cast<const void*>(a.w_q4);
   const uint64_t c4 = kp ? kp : 128, c8 = k_o ? 128 : kp;
   if (!make_map_u8(&m_wq4, w4, c4, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_map_u8(&m_wq8, w8, c8, N, 128, kTileN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map_u8(&m_wq8, w8, c8, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
       !make_map_u8(&m_af8, a.a_f8, K, M, 128, kTileM, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
 
   GemmParams p;
-  p.a_scales = a.a_scales;
-  p.a_csum = a.a_csum;
+  p.a_ab = a.a_ab;
+  p.Mp = static_cast<int>(ab_rows(a.M));
   p.w_scales = a.w_scales;
   p.c = a.c;
   p.ldc = a.ldc;
@@ -815,6 +988,14 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
     p.partials = reinterpret_cast<float*>(static_cast<char*>(workspace) + plan.counter_bytes);
   }
   const size_t smem = sizeof(GemmSmem) + 1024;
+#ifdef ATOM_DEV_PROBES
+  static long long* trace = nullptr;
+  static const bool want_trace = std::getenv("ATOM_GEMM_TRACE") != nullptr;
+  constexpr size_t kTraceBytes = static_cast<size_t>(kTraceEv) * kTraceN * sizeof(long long);
+  if (want_trace && trace == nullptr) cudaMalloc(&trace, kTraceBytes);
+  p.trace = want_trace ? trace : nullptr;
+  if (want_trace) cudaMemsetAsync(trace, 0, kTraceBytes, stream);
+#endif
   cudaError_t e;
   if (p.debug) {
     if ((e = set_smem_attr<true>(smem)) != cudaSuccess) return e;
@@ -827,6 +1008,28 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   }
   if (e != cudaSuccess) return e;
   ++*launches;
+#ifdef ATOM_DEV_PROBES
+  if (want_trace) {
+    static long long h[kTraceEv * kTraceN];
+    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "plan grid=%d dp_waves=%d sk_units=%lld\n", plan.grid, plan.dp_waves,
+                 static_cast<long long>(plan.sk_units));
+    std::fprintf(stderr, "g  W_tma A_tma unp_start unp_done mma_issue mma_done epi_start epi_release epi_end\n");
+    const long long t0 = h[3 * kTraceN];
+    for (int g = 0; g < kTraceN; ++g) {
+      if (h[3 * kTraceN + g] == 0) break;
+      if (g > 40 && g % 20 != 0) continue;
+      std::fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld |", g,
+                   h[g] - t0, h[kTraceN + g] - t0, h[2 * kTraceN + g] - t0,
+                   h[4 * kTraceN + g] - t0, h[3 * kTraceN + g] - t0, h[8 * kTraceN + g] - t0,
+                   h[5 * kTraceN + g] - t0, h[6 * kTraceN + g] - t0, h[7 * kTraceN + g] - t0);
+      for (int e = 0; e < 8; ++e)
+        std::fprintf(stderr, " %lld/%lld", h[(17 + e) * kTraceN + g] - t0,
+                     h[(9 + e) * kTraceN + g] - t0);
+      std::fprintf(stderr, "\n");
+    }
+  }
+#endif
   return cudaGetLastError();
 }
 

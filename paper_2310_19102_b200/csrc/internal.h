@@ -31,7 +31,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    uint8_t* af8, int32_t* csum, float* scales,
+                                    uint8_t* af8, float* ab, float* scales,
                                     cudaStream_t stream, int num_sms,
                                     const void* gamma = nullptr, float eps = 0.0f,
                                     const void* up = nullptr);
@@ -40,9 +40,8 @@ cudaError_t launch_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, in
                                  int32_t* ok, cudaStream_t stream);
 
 struct GemmArgs {
-  const uint8_t* a_f8;      // activation operand form (include/atom.h "a_f8")
-  const int32_t* a_csum;    // [K/128][M] group code sums
-  const float* a_scales;
+  const uint8_t* a_f8;      // activation operand form (include/atom.h "a_f8", "a_ab")
+  const float* a_ab;
   const uint8_t* w_q4;
   const int8_t* w_q8;
   const float* w_scales;
@@ -65,12 +64,15 @@ struct GemmPlan {
 
 GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms);
 
-// Bytes of workspace the canonical entry needs for a_f8 + a_csum (after the GEMM's own part).
+// Rows of a_ab per group: M rounded up to the 128-token tile.
+int64_t ab_rows(int64_t M);
+
+// Bytes of workspace the canonical entry needs for a_f8 + a_ab (after the GEMM's own part).
 size_t expand_bytes(int64_t M, int64_t K);
 
-cudaError_t launch_expand_activations(const uint8_t* q4, const int8_t* q8, int64_t M, int64_t K,
-                                      int32_t k_outlier, uint8_t* af8, int32_t* csum,
-                                      cudaStream_t stream, int num_sms);
+cudaError_t launch_expand_activations(const uint8_t* q4, const int8_t* q8, const float* scales,
+                                      int64_t M, int64_t K, int32_t k_outlier, uint8_t* af8,
+                                      float* ab, cudaStream_t stream, int num_sms);
 
 // Returns the number of kernel launches issued through *launches.
 cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,

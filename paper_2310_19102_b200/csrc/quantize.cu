@@ -11,7 +11,7 @@
 // reads shared memory.  One half-warp per 128-channel group: each lane owns 8 reordered
 // channels (two 128-bit perm loads), the group |max| is a 4-step shuffle reduction, codes are
 // packed in registers and written as 64 contiguous bytes (INT4) or 128 bytes (INT8), plus the
-// GEMM operand form a_f8 (one E4M3 byte per code) and the group code sums a_csum
+// GEMM operand form a_f8 (one E4M3 byte per code) and the per-row dequant constants a_ab
 // (include/atom.h).
 // Numerics are pinned to the oracle's binary32 steps: __fdiv_rn / __fmul_rn / __frcp_rn are
 // IEEE round-to-nearest and never contracted; cvt.rni gives round-half-to-even.
@@ -35,11 +35,6 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
   return r;
 }
 
-__device__ __forceinline__ int quant_code(float x, float inv, int lo, int hi) {
-  int q = __float2int_rn(__fmul_rn(x, inv));  // single RN multiply, then round-half-even
-  return min(max(q, lo), hi);
-}
-
 // kNorm (NEXT-1): the RMSNorm the paper fuses the quantizer into is applied to the
 // staged row first: r = RN32(1/sqrt(sum(x^2)/ldx + eps)) from a double sum of squares, and the
 // gathered value becomes y = fp16_rn(RN32(RN32(x*r) * gamma)) (oracle N1, reading G19).
@@ -53,8 +48,8 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                         const int32_t* __restrict__ perm, int32_t G, int32_t G4,
                         int32_t groups_per_cta, float clip4, float clip8,
                         uint8_t* __restrict__ q4, int8_t* __restrict__ q8,
-                        uint8_t* __restrict__ af8, int32_t* __restrict__ csum, int64_t K,
-                        float* __restrict__ scales,
+                        uint8_t* __restrict__ af8, float* __restrict__ ab, int64_t Mp,
+                        int64_t K, float* __restrict__ scales,
                         const __half* __restrict__ gamma, float eps,
                         const __half* __restrict__ up) {
   constexpr bool kNorm = kPre == 1;
@@ -180,7 +175,7 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                                     0x5410);
     const uint32_t od = __byte_perm(__byte_perm(f[1], f[3], 0x0040), __byte_perm(f[5], f[7], 0x0040),
                                     0x5410);
-    // group code sum (the GEMM's offset-binary correction, include/atom.h "a_csum")
+    // group code sum (the GEMM's offset-binary correction, include/atom.h "a_ab")
     int qs = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) qs += static_cast<int>(f[k] - 0x4B400000u);
@@ -212,7 +207,14 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
       }
       if (hl == 0) {
         scales[static_cast<int64_t>(t) * rows + row] = s;
-        if (csum) csum[static_cast<int64_t>(t) * rows + row] = is_int4 ? qs : 0;
+        if (ab) {   // (alpha, beta) of include/atom.h "a_ab", in its row order
+          const int64_t r = row & 31;
+          const int64_t pos = (row - r) + 4 * (r & 7) + (r >> 3);
+          const float2 v = is_int4 ? make_float2(s * 262144.0f,
+                                                 __fmul_rn(static_cast<float>(-8 * qs), s))
+                                   : make_float2(s, 0.0f);
+          reinterpret_cast<float2*>(ab)[static_cast<int64_t>(t) * Mp + pos] = v;
+        }
       }
     }
   }
@@ -221,7 +223,7 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    uint8_t* af8, int32_t* csum, float* scales,
+                                    uint8_t* af8, float* ab, float* scales,
                                     cudaStream_t stream, int num_sms, const void* gamma,
                                     float eps, const void* up) {
   const int G = static_cast<int>(K / 128);
@@ -242,7 +244,7 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
   }
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
   return launch_pdl(kern, grid, dim3(kQuantThreads), smem, stream, static_cast<const __half*>(x),
-                    rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, af8, csum, K, scales,
+                    rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, af8, ab, ab_rows(rows), K, scales,
                     static_cast<const __half*>(gamma), eps, static_cast<const __half*>(up));
 }
 

@@ -75,13 +75,13 @@ def test_host_validation_without_device(lib):
     assert lib.atom_quantize_weights(None, 4, 250, None, 256, 128, f(0.85), f(1.0), None, None,
                                      None, None) == 2
     z6 = (None,) * 6
-    for gemm in (lib.atom_w4a4_gemm, lib.atom_w4a4_gemm_f8):
-        assert gemm(*z6, 4, 100, 256, 128, None, 128, 0, None, None, 0, None) == 2
-        assert gemm(*z6, 4, 128, 256, 128, None, 128, 3, None, None, 0, None) == 4
-        assert gemm(*z6, 4, 128, 256, 128, None, 128, 0, None, None, 0, None) == 1
-        assert gemm(*z6, 4, 128, 256, 128, None, 100, 0, None, None, 0, None) == 2   # ldc < N
+    for gemm, zp in ((lib.atom_w4a4_gemm, z6), (lib.atom_w4a4_gemm_f8, z6[:5])):
+        assert gemm(*zp, 4, 100, 256, 128, None, 128, 0, None, None, 0, None) == 2
+        assert gemm(*zp, 4, 128, 256, 128, None, 128, 3, None, None, 0, None) == 4
+        assert gemm(*zp, 4, 128, 256, 128, None, 128, 0, None, None, 0, None) == 1
+        assert gemm(*zp, 4, 128, 256, 128, None, 100, 0, None, None, 0, None) == 2   # ldc < N
         # M == 0 is a no-op that succeeds without a device
-        assert gemm(*z6, 0, 128, 256, 128, None, 128, 0, None, None, 0, None) == 0
+        assert gemm(*zp, 0, 128, 256, 128, None, 128, 0, None, None, 0, None) == 0
     assert lib.atom_w4a4_gemm_workspace_size(1024, 28672, 8192, 128) == 0
     assert lib.atom_w4a4_gemm_f8_workspace_size(1024, 28672, 8192, 128) == 0
     assert lib.atom_last_launch_count() == 0

@@ -60,12 +60,13 @@ def codes_from_packed(o4):
     return np.where(codes >= 8, codes - 16, codes)
 
 
-def f8_from_packed(o4, o8):
-    """The GEMM operand form (include/atom.h "a_f8", "a_csum") rebuilt from the oracle's packed
-    codes with plain index arithmetic, independent of the kernels: INT4 code q as the E4M3 byte
-    of q * 2^-9 (q, or 0x80 | -q when negative); within each 32-channel chunk byte 16h + 4i + b
-    holds channel 8i + 2b + h; the INT8 outlier group copied as is.  csum = per-group code sums
-    of the INT4 groups ([K/128][rows], 0 for the outlier group)."""
+def f8_from_packed(o4, o8, osc):
+    """The GEMM operand form (include/atom.h "a_f8", "a_ab") rebuilt from the oracle's packed
+    codes and scales with plain index arithmetic, independent of the kernels: INT4 code q as the
+    E4M3 byte of q * 2^-9 (q, or 0x80 | -q when negative); within each 32-channel chunk byte
+    16h + 4i + b holds channel 8i + 2b + h; the INT8 outlier group copied as is.  a_ab: per
+    token and group (s * 2^18, fl32(fl32(-8 ca) * s)) for INT4 groups (ca = the group's code
+    sum), (s, 0) for the outlier group, token 32b + r at position 32b + 4 (r % 8) + r / 8."""
     rows = o4.shape[0] if o4.size else o8.shape[0]
     parts, sums = [], []
     if o4.size:
@@ -77,10 +78,21 @@ def f8_from_packed(o4, o8):
         q = codes[:, src]
         parts.append(np.where(q < 0, 0x80 | (-q), q).astype(np.uint8))
         sums.append(codes.reshape(rows, -1, 128).sum(axis=2).T)
+    G = osc.shape[0]
+    G4 = len(sums[0]) if sums else 0
     if o8 is not None:
         parts.append(o8.view(np.uint8))
-        sums.append(np.zeros((1, rows), np.int64))
-    return np.concatenate(parts, axis=1), np.concatenate(sums, axis=0).astype(np.int32)
+    ab = np.zeros((G, rows, 2), np.float32)
+    for t in range(G):
+        s = osc[t].astype(np.float32)
+        if t < G4:
+            ab[t, :, 0] = s * np.float32(262144.0)
+            ab[t, :, 1] = (-8 * sums[0][t]).astype(np.float32) * s   # float(-8 ca): +0 for ca = 0
+        else:
+            ab[t, :, 0] = s
+    pos = np.arange(rows)
+    pos = (pos - pos % 32) + 4 * (pos % 8) + (pos % 32) // 8
+    return np.concatenate(parts, axis=1), ab, pos
 
 
 def assert_quant_equal(q, ref):
@@ -90,9 +102,10 @@ def assert_quant_equal(q, ref):
     if o8 is not None and q.q8 is not None:
         np.testing.assert_array_equal(host(q.q8), o8)
     if q.f8 is not None:
-        f8, cs = f8_from_packed(o4, o8)
+        f8, ab, pos = f8_from_packed(o4, o8, osc)
         np.testing.assert_array_equal(host(q.f8), f8)
-        np.testing.assert_array_equal(host(q.csum), cs)
+        got_ab = host(q.ab)[:, pos, :]
+        np.testing.assert_array_equal(got_ab.view(np.uint32), ab.view(np.uint32))
     got = host(q.scales)
     np.testing.assert_array_equal(got.view(np.uint32), osc.view(np.uint32))
 
@@ -615,6 +628,7 @@ def test_empty_m_is_noop(atom):
     f = __import__("ctypes").c_float
     assert L.atom_reorder_quantize(None, 0, 256, None, 256, 128, f(0.9), f(1.0), None, None,
                                    None, None, None, None) == 0
-    for gemm in (L.atom_w4a4_gemm, L.atom_w4a4_gemm_f8):
-        assert gemm(None, None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
-                    None, None, 0, None) == 0
+    assert L.atom_w4a4_gemm(None, None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
+                            None, None, 0, None) == 0
+    assert L.atom_w4a4_gemm_f8(None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
+                               None, None, 0, None) == 0

@@ -86,6 +86,9 @@ __global__ void __launch_bounds__(384, 1) epi(int groups, int mma_groups, const 
     float sreg[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) sreg[i] = 1.0f + i * 0.01f + lane * 1e-4f;
+    float2 sw9[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sw9[i] = make_float2(1.0f + i * 0.01f, 1.0f - lane * 1e-4f);
     long long c0 = clock64();
     for (int g = 0; g < groups; ++g) {
       const float* ss = &ssc[g & 3][half * 128];
@@ -183,6 +186,52 @@ __global__ void __launch_bounds__(384, 1) epi(int groups, int mma_groups, const 
             acc[a0] = x0.x; acc[a0 + 1] = x0.y; acc[a0 + 32] = x1.x; acc[a0 + 33] = x1.y;
           }
         }
+      } else if constexpr (V == 7 || V == 8 || V == 9) {
+        // 16x256b loads of X chunks (V7, V9: x2; V8: x4), one ahead; column scales in 16 float2
+        // registers (V9: refilled per block from global memory for the "next group")
+        constexpr int X = (V == 8) ? 4 : 2;
+        constexpr int NL = 2 * (16 / X);
+        uint32_t r[2][4 * X];
+        auto ld = [&](int j, uint32_t* dst) {
+          const int hh = j & 1, cb = j >> 1;
+          if constexpr (X == 2) tmem_ld_16x256b<2>(tq + (static_cast<uint32_t>(16 * hh) << 16) + 16 * cb, dst);
+          else tmem_ld_16x256b<4>(tq + (static_cast<uint32_t>(16 * hh) << 16) + 32 * cb, dst);
+        };
+        ld(0, r[0]);
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+          uint32_t* rv = r[j & 1];
+          if (j + 1 < NL) {
+            ld(j + 1, r[(j + 1) & 1]);
+#pragma unroll
+            for (int v = 0; v < 4 * X; ++v) asm volatile("" : "+r"(rv[v]));
+          } else {
+            tmem_ld_wait();
+          }
+          const int hh = j & 1, cb = j >> 1;
+#pragma unroll
+          for (int ch = 0; ch < X; ++ch) {
+            const int kc = cb * X + ch;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const int ri = 2 * hh + s2;
+              const float2 h = __ffma2_rn(f2(rv[4 * ch + 2 * s2], rv[4 * ch + 2 * s2 + 1]), al2, be2);
+              const float2 a = __ffma2_rn(sw9[kc], h, make_float2(acc[ri * 32 + 2 * kc], acc[ri * 32 + 2 * kc + 1]));
+              acc[ri * 32 + 2 * kc] = a.x;
+              acc[ri * 32 + 2 * kc + 1] = a.y;
+            }
+          }
+          if constexpr (V == 9) {
+            if (hh == 1) {
+#pragma unroll
+              for (int ch = 0; ch < X; ++ch) {
+                const int kc = cb * X + ch;
+                const float* gp = gsc + ((g + 1) & 63) * 256 + half * 128 + 2 * (lane & 3) + 8 * kc;
+                asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(sw9[kc].x), "=f"(sw9[kc].y) : "l"(gp));
+              }
+            }
+          }
+        }
       } else if constexpr (V == 4) {
         uint32_t r[2][32];
         float4 sn[8], sc[8];
@@ -251,7 +300,7 @@ int main() {
       printf("\n");                                                                                \
     }                                                                                              \
   } while (0)
-  RUN(0); RUN(1); RUN(2); RUN(3); RUN(4); RUN(5); RUN(6);
+  RUN(0); RUN(3); RUN(7); RUN(8); RUN(9);
   printf("rc=0\n");
   return 0;
 }
