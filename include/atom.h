@@ -58,6 +58,12 @@
  *           GEMM removes it with h = alpha * P' + beta (P' = 2^-18 (P + 8 ca), the fp32
  *           accumulator), i.e. h = s * P up to one rounding.  The activations are expanded once
  *           in the quantize kernel instead of once per output tile.
+ *   w_sp    fp32 [K/128][N]  the weight scales in the GEMM's channel order (written by
+ *           atom_quantize_weights when requested, read by atom_w4a4_gemm_f8; N % 128 == 0):
+ *           within every 128 channels, channel 8k + 2c + b (k < 16, c < 4, b < 2) is stored at
+ *           32 (k / 4) + 8c + 2 (k % 4) + b, so the GEMM thread that owns channel pairs 2c + 8k
+ *           loads 4 of its pairs as 32 contiguous bytes and the 4 threads c = 0..3 one 128-byte
+ *           line (four 32-byte loads per group instead of sixteen 8-byte ones).
  *   Quantizer: s = 2*max|x|*c/(2^n - 1), evaluated as alpha = fl(fl(2c)/(2^n-1)),
  *   s = fl(amax*alpha) (s = FLT_MIN for an all-zero group), q = clamp(rint_even(fl(x*fl(1/s))),
  *   -2^(n-1), 2^(n-1)-1).
@@ -154,11 +160,14 @@ atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* u
  * and formats as atom_reorder_quantize with rows = output channels n of W [N][ldw] (nn.Linear
  * layout); the paper's clip is 0.85 for weights.  scales are fp32 [K/128][N].  q4 and
  * q8 are required (when K > k_outlier / k_outlier == 128): the weights stay packed in HBM.
+ * w_sp: NULL, or fp32 [K/128][N] receiving the same scales in the GEMM channel order (above);
+ * requires N % 128 == 0 (else ATOM_ERR_SHAPE).
  */
 atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8,
-                                    uint8_t* q4, int8_t* q8, float* scales, void* stream);
+                                    uint8_t* q4, int8_t* q8, float* scales, float* w_sp,
+                                    void* stream);
 
 /*
  * a2-a5: fused mixed-precision group GEMM (P:254 Steps 1-3, Fig 6, outliers P:230):
@@ -197,12 +206,13 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
 /*
  * The same GEMM on the activation operand form (a_f8, a_ab) that atom_reorder_quantize writes
  * in the same pass as the scales: the hot path (quantize -> GEMM) then writes and reads only
- * what the GEMM consumes.  Same results (bit for bit) and errors as atom_w4a4_gemm; a_f8 and
- * a_ab are required (the activation scales are inside a_ab).  Workspace:
+ * what the GEMM consumes; the weight scales come in the GEMM channel order w_sp that
+ * atom_quantize_weights writes offline.  Same results (bit for bit) and errors as
+ * atom_w4a4_gemm; a_f8 and a_ab are required (the activation scales are inside a_ab).  Workspace:
  * atom_w4a4_gemm_f8_workspace_size bytes (may be 0; any atom_w4a4_gemm workspace also serves).
  */
 atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const float* a_ab,
-                                const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales,
+                                const uint8_t* w_q4, const int8_t* w_q8, const float* w_sp,
                                 int64_t M, int64_t N, int64_t K, int32_t k_outlier,
                                 void* c, int64_t ldc, atom_dtype_t c_dtype,
                                 int32_t* debug_partials, void* workspace, size_t workspace_bytes,

@@ -57,7 +57,7 @@ def _lib():
         P, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
         q_args = [P, i64, i64, P, i64, i32, f32, f32, P, P, P, P]
         L.atom_reorder_quantize.argtypes = q_args[:10] + [P, P] + q_args[10:]
-        L.atom_quantize_weights.argtypes = q_args
+        L.atom_quantize_weights.argtypes = q_args[:11] + [P] + q_args[11:]
         L.atom_rmsnorm_reorder_quantize.argtypes = [P, i64, i64, P, f32] + q_args[3:10] + \
             [P, P] + q_args[10:]
         L.atom_rmsnorm_reorder_quantize.restype = ctypes.c_int
@@ -126,6 +126,7 @@ class Quantized:
     k_outlier: int
     f8: object = None
     ab: object = None
+    sp: object = None          # weights: scales in the GEMM channel order (include/atom.h "w_sp")
 
     @property
     def rows(self) -> int:
@@ -153,6 +154,7 @@ def _check_quantized(out, rows, K, k_outlier, dev, operand):
     want(out.q4, (rows, (K - k_outlier) // 2), torch.uint8, "q4")
     want(out.q8, (rows, k_outlier), torch.int8, "q8")
     want(out.scales, (G, rows), torch.float32, "scales")
+    want(out.sp, (G, rows), torch.float32, "sp")
     if operand:
         want(out.f8, (rows, K), torch.uint8, "f8")
         want(out.ab, (G, ab_rows(rows), 2), torch.float32, "ab")
@@ -173,6 +175,7 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
     K = int(perm.numel()) if K is None else int(K)
     if K > perm.numel():
         raise ValueError(f"K = {K} exceeds perm.numel() = {perm.numel()}")
+    prepared = fn_name == "atom_quantize_weights" and rows % GROUP == 0
     if out is None:
         dev = x.device
         q4 = torch.empty((rows, (K - k_outlier) // 2), dtype=torch.uint8, device=dev) \
@@ -183,12 +186,14 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
         f8 = torch.empty((rows, K), dtype=torch.uint8, device=dev) if operand else None
         ab = torch.empty((K // GROUP, ab_rows(rows), 2), dtype=torch.float32, device=dev) \
             if operand else None
-        out = Quantized(q4, q8, sc, K, k_outlier, f8, ab)
+        sp = torch.empty((K // GROUP, rows), dtype=torch.float32, device=dev) if prepared else None
+        out = Quantized(q4, q8, sc, K, k_outlier, f8, ab, sp)
     else:
         _check_quantized(out, rows, K, k_outlier, x.device, operand)
     codes = (_ptr(out.q4), _ptr(out.q8))
     if fn_name != "atom_quantize_weights":
         codes = codes + (_ptr(out.f8), _ptr(out.ab))
+    tail = (_ptr(out.sp),) if fn_name == "atom_quantize_weights" else ()
     head = (_ptr(x), rows, ld)
     if up is not None:                        # the up projection of the fused SwiGLU
         if up.dtype != torch.float16 or not up.is_cuda or up.shape != x.shape \
@@ -205,7 +210,7 @@ def _quantize(fn_name, x, perm, K, k_outlier, clip_int4, clip_int8, out, stream,
         head = head + (_ptr(gamma), ctypes.c_float(eps))
     st = getattr(_lib(), fn_name)(*head, _ptr(perm), K, k_outlier,
                                   ctypes.c_float(clip_int4), ctypes.c_float(clip_int8),
-                                  *codes, _ptr(out.scales), _stream(stream))
+                                  *codes, _ptr(out.scales), *tail, _stream(stream))
     _check(st, fn_name)
     return out
 
@@ -308,7 +313,7 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
             debug_partials.device != dev):
         raise ValueError("debug_partials must be a contiguous int32 [K/128][M][N] tensor")
     c_dtype = ATOM_F16 if out.dtype == torch.float16 else ATOM_F32
-    use_f8 = a.f8 is not None and not canonical
+    use_f8 = a.f8 is not None and w.sp is not None and not canonical
     if not use_f8 and (a.q4 is None) != (a.K == a.k_outlier):
         raise ValueError("activations lack the packed codes (quantize with packed=True)")
     if workspace is None:
@@ -316,7 +321,7 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
     wsz = 0 if workspace is None else workspace.numel()
     if use_f8:
         st = _lib().atom_w4a4_gemm_f8(_ptr(a.f8), _ptr(a.ab), _ptr(w.q4),
-                                      _ptr(w.q8), _ptr(w.scales), M, N, a.K, a.k_outlier,
+                                      _ptr(w.q8), _ptr(w.sp), M, N, a.K, a.k_outlier,
                                       _ptr(out), out.stride(0), c_dtype, _ptr(debug_partials),
                                       _ptr(workspace), wsz, _stream(stream))
         _check(st, "atom_w4a4_gemm_f8")

@@ -82,7 +82,7 @@ atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int
                               int8_t* q8, uint8_t* af8, float* ab, float* scales,
                               bool packed_required,
                               void* stream, const void* gamma = nullptr, float eps = 0.0f,
-                              const void* up = nullptr) {
+                              const void* up = nullptr, float* wsp = nullptr) {
   g_last_launches = 0;
   atom_status_t st = check_quant_args(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8, af8, ab,
                                       scales, packed_required);
@@ -90,7 +90,7 @@ atom_status_t quantize_common(const void* x, int64_t rows, int64_t ld, const int
   DeviceInfo dev;
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   cudaError_t e = atom::launch_reorder_quantize(x, rows, ld, perm, K, k_o, clip4, clip8, q4, q8,
-                                                af8, ab, scales,
+                                                af8, ab, scales, wsp,
                                                 static_cast<cudaStream_t>(stream), dev.num_sms,
                                                 gamma, eps, up);
   if (e != cudaSuccess) return ATOM_ERR_CUDA;
@@ -131,7 +131,8 @@ atom_status_t check_gemm_args(const uint8_t* w_q4, const int8_t* w_q8, const flo
   return ATOM_OK;
 }
 
-cudaError_t run_gemm(const uint8_t* af8, const float* ab, const uint8_t* w_q4, const int8_t* w_q8, const float* w_scales, int64_t M,
+cudaError_t run_gemm(const uint8_t* af8, const float* ab, const uint8_t* w_q4,
+                     const int8_t* w_q8, const float* w_sp, int64_t M,
                      int64_t N, int64_t K, int32_t k_outlier, void* c, int64_t ldc,
                      atom_dtype_t c_dtype, int32_t* debug_partials, void* workspace,
                      size_t workspace_bytes, void* stream, const DeviceInfo& dev, int* launches) {
@@ -140,7 +141,7 @@ cudaError_t run_gemm(const uint8_t* af8, const float* ab, const uint8_t* w_q4, c
   a.a_ab = ab;
   a.w_q4 = w_q4;
   a.w_q8 = w_q8;
-  a.w_scales = w_scales;
+  a.w_sp = w_sp;
   a.M = M;
   a.N = N;
   a.K = K;
@@ -194,9 +195,12 @@ atom_status_t atom_silu_mul_reorder_quantize(const void* gate_f16, const void* u
 atom_status_t atom_quantize_weights(const void* w_f16, int64_t N, int64_t ldw,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip_int4, float clip_int8, uint8_t* q4, int8_t* q8,
-                                    float* scales, void* stream) {
+                                    float* scales, float* w_sp, void* stream) {
+  g_last_launches = 0;
+  if (w_sp && N % 128 != 0) return ATOM_ERR_SHAPE;
+  if (w_sp && !aligned16(w_sp)) return ATOM_ERR_ALIGN;
   return quantize_common(w_f16, N, ldw, perm, K, k_outlier, clip_int4, clip_int8, q4, q8, nullptr,
-                         nullptr, scales, true, stream);
+                         nullptr, scales, true, stream, nullptr, 0.0f, nullptr, w_sp);
 }
 
 size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
@@ -205,7 +209,8 @@ size_t atom_w4a4_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_
   DeviceInfo dev;
   if (current_device(&dev) != ATOM_OK) return 0;   // no sm_100 device: the GEMM cannot run
   const atom::GemmPlan pl = atom::plan_w4a4_gemm(M, N, K, dev.num_sms);
-  return gemm_part_bytes(pl, dev.num_sms) + atom::expand_bytes(M, K);
+  return gemm_part_bytes(pl, dev.num_sms) + atom::expand_bytes(M, K) +
+         static_cast<size_t>(N) * (K / ATOM_GROUP) * sizeof(float);
 }
 
 size_t atom_w4a4_gemm_f8_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
@@ -223,12 +228,12 @@ size_t atom_w4a4_gemm_counter_bytes(void) {
 }
 
 atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const float* a_ab, const uint8_t* w_q4,
-                                const int8_t* w_q8, const float* w_scales, int64_t M, int64_t N,
+                                const int8_t* w_q8, const float* w_sp, int64_t M, int64_t N,
                                 int64_t K, int32_t k_outlier, void* c, int64_t ldc,
                                 atom_dtype_t c_dtype, int32_t* debug_partials, void* workspace,
                                 size_t workspace_bytes, void* stream) {
   g_last_launches = 0;
-  atom_status_t st = check_gemm_args(w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+  atom_status_t st = check_gemm_args(w_q4, w_q8, w_sp, M, N, K, k_outlier, c, ldc, c_dtype,
                                      debug_partials);
   if (st != ATOM_OK || M == 0) return st;
   if (!a_f8 || !a_ab) return ATOM_ERR_NULL;
@@ -239,7 +244,7 @@ atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const float* a_ab, const ui
   if (ws > 0 && (workspace == nullptr || workspace_bytes < ws || !aligned16(workspace)))
     return ATOM_ERR_WORKSPACE;
   int launches = 0;
-  if (run_gemm(a_f8, a_ab, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+  if (run_gemm(a_f8, a_ab, w_q4, w_q8, w_sp, M, N, K, k_outlier, c, ldc, c_dtype,
                debug_partials, workspace, workspace_bytes, stream, dev, &launches) != cudaSuccess)
     return ATOM_ERR_CUDA;
   g_last_launches = launches;
@@ -264,21 +269,25 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
   if ((st = current_device(&dev)) != ATOM_OK) return st;
   const atom::GemmPlan pl = atom::plan_w4a4_gemm(M, N, K, dev.num_sms);
   const size_t part = gemm_part_bytes(pl, dev.num_sms);
-  const size_t need = part + atom::expand_bytes(M, K);
+  const size_t exp = atom::expand_bytes(M, K);
+  const size_t need = part + exp + static_cast<size_t>(N) * (K / ATOM_GROUP) * sizeof(float);
   if (workspace == nullptr || workspace_bytes < need || !aligned16(workspace))
     return ATOM_ERR_WORKSPACE;
-  // the operand form lives after the GEMM's own part of the workspace
+  // the operand forms live after the GEMM's own part of the workspace
   uint8_t* af8 = static_cast<uint8_t*>(workspace) + part;
   float* ab = reinterpret_cast<float*>(af8 + ((static_cast<size_t>(M) * K + 255) / 256) * 256);
+  float* wsp = reinterpret_cast<float*>(af8 + exp);
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (atom::launch_expand_activations(a_q4, a_q8, a_scales, M, K, k_outlier, af8, ab, s,
-                                      dev.num_sms) != cudaSuccess)
+                                      dev.num_sms) != cudaSuccess ||
+      atom::launch_prepare_w_scales(w_scales, K / ATOM_GROUP, N, wsp, s, dev.num_sms) !=
+          cudaSuccess)
     return ATOM_ERR_CUDA;
   int launches = 0;
-  if (run_gemm(af8, ab, w_q4, w_q8, w_scales, M, N, K, k_outlier, c, ldc, c_dtype,
+  if (run_gemm(af8, ab, w_q4, w_q8, wsp, M, N, K, k_outlier, c, ldc, c_dtype,
                debug_partials, workspace, part, stream, dev, &launches) != cudaSuccess)
     return ATOM_ERR_CUDA;
-  g_last_launches = launches + 1;
+  g_last_launches = launches + 2;
   return ATOM_OK;
 }
 

@@ -95,7 +95,7 @@ static_assert(kRS >= kRT && kRS >= kRW, "ring sizes");
 
 struct GemmParams {
   const float* a_ab;         // [G][Mp][2] per-row dequant constants (include/atom.h "a_ab")
-  const float* w_scales;     // [G][N]
+  const float* w_sp;         // [G][N] weight scales, GEMM channel order (include/atom.h "w_sp")
   void* c;
   int64_t ldc;
   int32_t* debug;
@@ -249,6 +249,13 @@ __device__ __forceinline__ float2 ldg_f2(const float* p) {
   asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
   return v;
 }
+// 32-byte global load (LDG.E.ENL2.256 on sm_100a)
+__device__ __forceinline__ void ldg_v8(const float* p, float (&v)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                 "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -347,7 +354,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             mbar_arrive_expect_tx(&sm.go[u.i], kTileM * 128);
             // re-read by every n-tile: keep in L2
             tma_load_2d_hint(sm.a[u.i], &tm_af8, &sm.go[u.i], t * 128, w.m0, pol_a);
-            prefetch_l2_bulk(p.w_scales + static_cast<int64_t>(t) * p.N + w.n0, sw_bytes);
+            prefetch_l2_bulk(p.w_sp + static_cast<int64_t>(t) * p.N + w.n0, sw_bytes);
             prefetch_l2_bulk(p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + w.m0), kTileM * 8);
           }
         }
@@ -415,10 +422,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     // phases of opposite parity, so the stores are bank-conflict-free.
     const int ut = threadIdx.x - kUnpackWarp0 * 32;
     const uint32_t r0 = static_cast<uint32_t>(ut) >> 2, c = static_cast<uint32_t>(ut) & 3u;
-#ifndef ATOM_PERM
-#define ATOM_PERM 0
-#endif
-    const uint32_t jb = ATOM_PERM ? 8 * (r0 >> 1) + (r0 & 1) : r0;   // operand row of k = 0
+    const uint32_t jb = r0;              // operand row of k = 0
     uint32_t m0f = 0x0F0F0F0Fu, x08 = 0x08080808u;
     asm volatile("" : "+r"(m0f), "+r"(x08));   // keep the LOP3 constants in registers
     Ring<kKS> st;
@@ -449,8 +453,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             if constexpr ((ATOM_PROBE_MODE & 1) != 0) break;
-            const uint32_t row = ATOM_PERM ? 128 * (j >> 2) + jb + 2 * (j & 3) : jb + 32 * j;
-            const uint32_t ph = ATOM_PERM ? (2 * (j & 3) + (r0 & 1)) & 7 : r0 & 7;
+            const uint32_t row = jb + 32 * j, ph = r0 & 7;
             uint8_t* d = dst + row * 128;
             *reinterpret_cast<uint4*>(d + (((2 * c) ^ ph) << 4)) =
                 make_uint4(lop_and_xor(v[j].x, m0f, x08), lop_and_xor(v[j].y, m0f, x08),
@@ -474,8 +477,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             for (int j = 0; j < 8; ++j) v[j] = *reinterpret_cast<const uint4*>(src + j * 32 * 64);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const uint32_t row = ATOM_PERM ? 128 * (j >> 2) + jb + 2 * (j & 3) : jb + 32 * j;
-              const uint32_t ph = ATOM_PERM ? (2 * (j & 3) + (r0 & 1)) & 7 : r0 & 7;
+              const uint32_t row = jb + 32 * j, ph = r0 & 7;
               *reinterpret_cast<uint4*>(dst + row * 128 + (((4 * h + c) ^ ph) << 4)) = v[j];
             }
             __syncwarp();
@@ -497,45 +499,43 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     const int half = e >> 2;             // column half
     const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * 128;
     const int rl = q * 32 + (lane >> 2);           // + 8 ri: the thread's 4 tile rows
-    // + 2k (+1): its 16 channel pairs (ATOM_PERM: 32 consecutive channels)
-    const int cl = half * 128 + (ATOM_PERM ? 32 : 2) * (lane & 3);
-    constexpr int kPairStride = ATOM_PERM ? 2 : 8;   // channel distance of consecutive pairs
+    const int cl = half * 128 + 2 * (lane & 3);    // + 8 k (+1): its 16 channel pairs
     griddep_wait();
     if (lane == 0)                       // the first kRT groups find their TMEM buffers free
       for (int b = 0; b < kRT; ++b) mbar_arrive(&sm.go[b % kRS]);
 
     // scales of the group being drained: 16 channel-pair weight scales and per-row alpha /
     // beta, loaded (LDG: unaffected by the tensor core's shared-memory traffic, unlike LDS)
-    // one group ahead, the weight scales block by block as their registers fall free.  The
-    // right half of a partial n-tile (N % 256 == 128) reads the left half's scales (its
-    // outputs are never stored); rows past M are clamped (separate, rarely taken path).
-    const int cl_ld = cl - ((half == 1 && (p.N & 255) != 0) ? 128 : 0);
+    // one group ahead, the weight scales 4 pairs at a time as their registers fall free.
+    // w_sp holds each thread's 4 pairs of a load in 32 contiguous bytes, the 4 threads of a
+    // pair column in one 128-byte line (include/atom.h "w_sp"): 4 32-byte loads per group.  The right half of a partial n-tile (N % 256 == 128) reads the left half's
+    // scales (its outputs are never stored).
+    const int cs_off = half * 128 + 8 * (lane & 3);
+    const int cs_ld = cs_off - ((half == 1 && (p.N & 255) != 0) ? 128 : 0);
     float2 sw[16];
     float al[4], be[4];
     auto sw_base = [&](int t, int n0) {
-      return p.w_scales + static_cast<int64_t>(t) * p.N + n0 + ((n0 + kTileN <= p.N) ? cl : cl_ld);
+      return p.w_sp + static_cast<int64_t>(t) * p.N + n0 + ((n0 + kTileN <= p.N) ? cs_off : cs_ld);
     };
-    auto load_sw = [&](const float* ws, int k0, int nk) {   // channel pairs k0 .. k0+nk (even)
+    auto load_sw = [&](const float* ws, int k0, int nk) {   // channel pairs k0 .. k0+nk (k0 % 4 == 0)
 #pragma unroll
-      for (int k = 0; k < 16; k += 2)
+      for (int k = 0; k < 16; k += 4)
         if (k >= k0 && k < k0 + nk) {
-          if constexpr (ATOM_PERM) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(ws) + k / 2);
-            sw[k] = make_float2(v.x, v.y);
-            sw[k + 1] = make_float2(v.z, v.w);
-          } else {
-            sw[k] = ldg_f2(ws + 8 * k);
-            sw[k + 1] = ldg_f2(ws + 8 * k + 8);
-          }
+          float v[8];
+          ldg_v8(ws + 8 * k, v);     // pairs k..k+3: 32 (k / 4) floats in
+          sw[k] = make_float2(v[0], v[1]);
+          sw[k + 1] = make_float2(v[2], v[3]);
+          sw[k + 2] = make_float2(v[4], v[5]);
+          sw[k + 3] = make_float2(v[6], v[7]);
         }
     };
     // per-row alpha / beta of rows rl + 8 ri: two 16-byte loads (a_ab row order)
     auto load_ab = [&](int t, int m0, float* a, float* bb) {
-      const float4* pa = reinterpret_cast<const float4*>(
-          p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + m0 + q * 32 + 4 * (lane >> 2)));
-      const float4 v0 = __ldg(pa), v1 = __ldg(pa + 1);
-      a[0] = v0.x; bb[0] = v0.y; a[1] = v0.z; bb[1] = v0.w;
-      a[2] = v1.x; bb[2] = v1.y; a[3] = v1.z; bb[3] = v1.w;
+      const float* pa = p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + m0 + q * 32 + 4 * (lane >> 2));
+      float v[8];
+      ldg_v8(pa, v);
+      a[0] = v[0]; bb[0] = v[1]; a[1] = v[2]; bb[1] = v[3];
+      a[2] = v[4]; bb[2] = v[5]; a[3] = v[6]; bb[3] = v[7];
     };
     if (n_items > 0) {
       const Item w0 = get_item(p, sch, 0);
@@ -628,7 +628,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                                    __int2float_rn(static_cast<int>(x1)));
                 if constexpr (kDebug) {
                   const int m = w.m0 + rl + 8 * ri;
-                  const int n = w.n0 + cl + kPairStride * kc;
+                  const int n = w.n0 + cl + 8 * kc;
                   if (m < p.M && n < p.N) {
                     int p0, p1;
                     if constexpr (kInt4) {   // P = P' * 2^18 - 8 ca, exact
@@ -657,7 +657,8 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             }
             // block cb done for both lane halves: its channel scales are free for the next group
             if constexpr ((ATOM_PROBE_MODE & 16) == 0)
-              if (hh == 1) load_sw(xws, cb * kLdX, kLdX);
+              // blocks cb - 1, cb done for both lane halves: 4 pairs of scales free
+              if (hh == 1 && ((cb + 1) * kLdX) % 4 == 0) load_sw(xws, (cb + 1) * kLdX - 4, 4);
           }
         };
         if (t < G4) drain(std::true_type{});
@@ -721,41 +722,16 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       for (int ri = 0; ri < 4; ++ri) {
         const int m = w.m0 + rl + 8 * ri;
         if (m >= p.M) continue;
-        if constexpr (ATOM_PERM) {
-          if (!p.c_f32) {
-            uint4* crow = reinterpret_cast<uint4*>(static_cast<__half*>(p.c) +
+        if (!p.c_f32) {
+          __half2* crow = reinterpret_cast<__half2*>(static_cast<__half*>(p.c) +
+                                                     static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
+#pragma unroll
+          for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = __float22half2_rn(acc[ri][kc]);
+        } else {
+          float2* crow = reinterpret_cast<float2*>(static_cast<float*>(p.c) +
                                                    static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 o;
-              __half2 h0 = __float22half2_rn(acc[ri][4 * v]), h1 = __float22half2_rn(acc[ri][4 * v + 1]);
-              __half2 h2 = __float22half2_rn(acc[ri][4 * v + 2]), h3 = __float22half2_rn(acc[ri][4 * v + 3]);
-              o.x = *reinterpret_cast<uint32_t*>(&h0);
-              o.y = *reinterpret_cast<uint32_t*>(&h1);
-              o.z = *reinterpret_cast<uint32_t*>(&h2);
-              o.w = *reinterpret_cast<uint32_t*>(&h3);
-              crow[v] = o;
-            }
-          } else {
-            float4* crow = reinterpret_cast<float4*>(static_cast<float*>(p.c) +
-                                                     static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
-#pragma unroll
-            for (int v = 0; v < 8; ++v)
-              crow[v] = make_float4(acc[ri][2 * v].x, acc[ri][2 * v].y, acc[ri][2 * v + 1].x,
-                                    acc[ri][2 * v + 1].y);
-          }
-        } else {
-          if (!p.c_f32) {
-            __half2* crow = reinterpret_cast<__half2*>(static_cast<__half*>(p.c) +
-                                                       static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
-#pragma unroll
-            for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = __float22half2_rn(acc[ri][kc]);
-          } else {
-            float2* crow = reinterpret_cast<float2*>(static_cast<float*>(p.c) +
-                                                     static_cast<int64_t>(m) * p.ldc + w.n0 + cl);
-#pragma unroll
-            for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = acc[ri][kc];
-          }
+          for (int kc = 0; kc < 16; ++kc) crow[4 * kc] = acc[ri][kc];
         }
       }
     }
@@ -845,6 +821,29 @@ expand_activations_kernel(const uint8_t* __restrict__ q4, const int8_t* __restri
       reinterpret_cast<float2*>(ab)[static_cast<int64_t>(t) * Mp + pos] = v;
     }
   }
+}
+
+// w_scales [G][N] -> w_sp: within every 128 channels, channel 8k + 2c + b (k < 16, c < 4,
+// b < 2) moves to 32 (k / 4) + 8c + 2 (k % 4) + b: the 4 pairs k = 4i..4i+3 of the epilogue
+// thread with lane % 4 = c are 32 contiguous bytes, and the 4 threads c = 0..3 read one line.
+__global__ void __launch_bounds__(256)
+prepare_w_scales_kernel(const float* __restrict__ ws, int64_t total, float* __restrict__ wsp) {
+  griddep_wait();
+  griddep_launch();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t nl = i & 127, k = nl >> 3;
+    wsp[(i - nl) + 32 * (k >> 2) + 8 * ((nl & 7) >> 1) + 2 * (k & 3) + (nl & 1)] = ws[i];
+  }
+}
+
+cudaError_t launch_prepare_w_scales(const float* w_scales, int64_t G, int64_t N, float* w_sp,
+                                    cudaStream_t stream, int num_sms) {
+  const int64_t total = G * N;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 8LL * num_sms) blocks = 8LL * num_sms;
+  return launch_pdl(prepare_w_scales_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0,
+                    stream, w_scales, total, w_sp);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -968,7 +967,7 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   GemmParams p;
   p.a_ab = a.a_ab;
   p.Mp = static_cast<int>(ab_rows(a.M));
-  p.w_scales = a.w_scales;
+  p.w_sp = a.w_sp;
   p.c = a.c;
   p.ldc = a.ldc;
   p.debug = a.debug_partials;

@@ -31,7 +31,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    uint8_t* af8, float* ab, float* scales,
+                                    uint8_t* af8, float* ab, float* scales, float* wsp,
                                     cudaStream_t stream, int num_sms,
                                     const void* gamma = nullptr, float eps = 0.0f,
                                     const void* up = nullptr);
@@ -44,7 +44,7 @@ struct GemmArgs {
   const float* a_ab;
   const uint8_t* w_q4;
   const int8_t* w_q8;
-  const float* w_scales;
+  const float* w_sp;        // weight scales in the GEMM channel order (include/atom.h "w_sp")
   int64_t M, N, K;
   int32_t k_outlier;
   void* c;
@@ -73,6 +73,10 @@ size_t expand_bytes(int64_t M, int64_t K);
 cudaError_t launch_expand_activations(const uint8_t* q4, const int8_t* q8, const float* scales,
                                       int64_t M, int64_t K, int32_t k_outlier, uint8_t* af8,
                                       float* ab, cudaStream_t stream, int num_sms);
+
+// w_scales [G][N] -> w_sp (the GEMM's channel order), for atom_w4a4_gemm.
+cudaError_t launch_prepare_w_scales(const float* w_scales, int64_t G, int64_t N, float* w_sp,
+                                    cudaStream_t stream, int num_sms);
 
 // Returns the number of kernel launches issued through *launches.
 cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,

@@ -49,7 +49,7 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
                         int32_t groups_per_cta, float clip4, float clip8,
                         uint8_t* __restrict__ q4, int8_t* __restrict__ q8,
                         uint8_t* __restrict__ af8, float* __restrict__ ab, int64_t Mp,
-                        int64_t K, float* __restrict__ scales,
+                        int64_t K, float* __restrict__ scales, float* __restrict__ wsp,
                         const __half* __restrict__ gamma, float eps,
                         const __half* __restrict__ up) {
   constexpr bool kNorm = kPre == 1;
@@ -62,11 +62,23 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
   // PDL: x (and the outputs) may belong to the previous kernel of the stream
   griddep_wait();
   griddep_launch();
-  // Stage the whole source row (the gather may touch any channel).
+  // Stage the whole source row (the gather may touch any channel).  Plain a1: one bulk copy
+  // (a single HBM round trip per row, no per-thread load -> store chains).
   const uint4* src = reinterpret_cast<const uint4*>(x + row * ldx);
   const int n16 = static_cast<int>(ldx / 8);
   double ss = 0.0;
-  for (int i = threadIdx.x; i < n16; i += kQuantThreads) {
+  if constexpr (kPre == 0) {
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(ldx) * 2);
+      bulk_g2s(srow4, src, static_cast<uint32_t>(ldx) * 2, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+  }
+  for (int i = threadIdx.x; kPre != 0 && i < n16; i += kQuantThreads) {
     uint4 v = ld_stream_u4(src + i);
     if constexpr (kPre == 2) {
       const uint4 w = ld_stream_u4(reinterpret_cast<const uint4*>(up + row * ldx) + i);
@@ -207,6 +219,12 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
       }
       if (hl == 0) {
         scales[static_cast<int64_t>(t) * rows + row] = s;
+        if (wsp) {   // weights: the GEMM's channel order of the scales (include/atom.h "w_sp")
+          const int64_t nl = row & 127, k = nl >> 3;
+          const int64_t pos = (row - nl) + 32 * (k >> 2) + 8 * ((nl & 7) >> 1) + 2 * (k & 3) +
+                              (nl & 1);
+          wsp[static_cast<int64_t>(t) * rows + pos] = s;
+        }
         if (ab) {   // (alpha, beta) of include/atom.h "a_ab", in its row order
           const int64_t r = row & 31;
           const int64_t pos = (row - r) + 4 * (r & 7) + (r >> 3);
@@ -223,7 +241,7 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
 cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
                                     const int32_t* perm, int64_t K, int32_t k_outlier,
                                     float clip4, float clip8, uint8_t* q4, int8_t* q8,
-                                    uint8_t* af8, float* ab, float* scales,
+                                    uint8_t* af8, float* ab, float* scales, float* wsp,
                                     cudaStream_t stream, int num_sms, const void* gamma,
                                     float eps, const void* up) {
   const int G = static_cast<int>(K / 128);
@@ -244,7 +262,7 @@ cudaError_t launch_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
   }
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(splits));
   return launch_pdl(kern, grid, dim3(kQuantThreads), smem, stream, static_cast<const __half*>(x),
-                    rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, af8, ab, ab_rows(rows), K, scales,
+                    rows, ldx, perm, G, G4, gpc, clip4, clip8, q4, q8, af8, ab, ab_rows(rows), K, scales, wsp,
                     static_cast<const __half*>(gamma), eps, static_cast<const __half*>(up));
 }
 

@@ -73,7 +73,7 @@ def test_host_validation_without_device(lib):
     assert lib.atom_reorder_quantize(None, 4, 256, None, 256, 128, f(0.9), f(1.0), *z5,
                                      None) == 1
     assert lib.atom_quantize_weights(None, 4, 250, None, 256, 128, f(0.85), f(1.0), None, None,
-                                     None, None) == 2
+                                     None, None, None) == 2
     z6 = (None,) * 6
     for gemm, zp in ((lib.atom_w4a4_gemm, z6), (lib.atom_w4a4_gemm_f8, z6[:5])):
         assert gemm(*zp, 4, 100, 256, 128, None, 128, 0, None, None, 0, None) == 2

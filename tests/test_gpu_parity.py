@@ -108,6 +108,14 @@ def assert_quant_equal(q, ref):
         np.testing.assert_array_equal(got_ab.view(np.uint32), ab.view(np.uint32))
     got = host(q.scales)
     np.testing.assert_array_equal(got.view(np.uint32), osc.view(np.uint32))
+    if q.sp is not None:   # weight scales in the GEMM channel order (include/atom.h "w_sp")
+        n = np.arange(osc.shape[1])
+        nl = n % 128
+        k = nl // 8
+        pos = (n - nl) + 32 * (k // 4) + 8 * ((nl % 8) // 2) + 2 * (k % 4) + nl % 2
+        want = np.empty_like(osc)
+        want[:, pos] = osc
+        np.testing.assert_array_equal(host(q.sp).view(np.uint32), want.view(np.uint32))
 
 
 # ----------------------------------------------------------------------------------------------
@@ -313,6 +321,9 @@ def test_gemm_canonical_equals_operand_form(atom):
     a4, a8, asc = oracle.quantize_rows(X, perm, K, 128, 0.9, 1.0)
     ora = atom.Quantized(dev(a4), dev(a8), dev(asc), K, 128)
     c_ora = atom.w4a4_gemm(ora, wq)
+    w4, w8, wsc = oracle.quantize_rows(W, perm, K, 128, 0.85, 1.0)
+    c_ora2 = atom.w4a4_gemm(ora, atom.Quantized(dev(w4), dev(w8), dev(wsc), K, 128))
+    assert torch.equal(c_ora, c_ora2)
     torch.cuda.synchronize()
     assert torch.equal(c_f8, c_can) and torch.equal(c_f8, c_ora)
     assert_close_tol(host(c_f8.float()), oracle.quantized_linear(X, perm, W, K)["c"], "C")
@@ -608,7 +619,7 @@ def test_error_codes_launch_nothing(atom):
     assert torch.all(q4 == 0xAB) and torch.all(q8 == 5) and torch.all(sc == 3.0)
     # GEMM: N % 128, ldc < N, bad dtype
     args = [q4.data_ptr(), q8.data_ptr(), sc.data_ptr(), q4.data_ptr(), q8.data_ptr(),
-            sc.data_ptr()]
+            sc.data_ptr()]   # canonical entry: a_q4, a_q8, a_scales, w_q4, w_q8, w_scales
     out = torch.zeros((4, 256), dtype=torch.float16, device="cuda")
     assert L.atom_w4a4_gemm(*args, 4, 200, 256, 128, out.data_ptr(), 256, 0, None, None, 0,
                             None) == 2

@@ -12,6 +12,7 @@ import synth  # noqa: E402
 
 lib, cfg = sys.argv[1], sys.argv[2]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+what = sys.argv[4] if len(sys.argv) > 4 else "gemm"     # gemm | quant
 atom.LIB_PATH = Path(lib).resolve()
 cfgs = {"cfg5": (1024, 28672, 8192), "cfg2": (256, 4096, 4096), "cfg4": (512, 13824, 5120),
         "cfg3u": (1024, 11008, 4096), "cfg3d": (1024, 4096, 11008), "m64": (64, 11008, 4096),
@@ -27,11 +28,18 @@ ref = out.clone()
 s = torch.cuda.Stream()
 s.wait_stream(torch.cuda.current_stream())
 g = torch.cuda.CUDAGraph()
+def call():
+    if what == "quant":
+        atom.reorder_quantize(X, perm, out=aq, packed=False, stream=s)
+    else:
+        atom.w4a4_gemm(aq, wq, out=out, stream=s)
+
+
 with torch.cuda.stream(s):
-    atom.w4a4_gemm(aq, wq, out=out, stream=s)
+    call()
     with torch.cuda.graph(g, stream=s):
         for _ in range(reps):
-            atom.w4a4_gemm(aq, wq, out=out, stream=s)
+            call()
 torch.cuda.current_stream().wait_stream(s)
 flush = torch.empty(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8,
                     device="cuda")
@@ -46,4 +54,5 @@ for _ in range(9):
     ts.append(e0.elapsed_time(e1) * 1e3 / reps)
 ts.sort()
 ok = torch.equal(out, ref)
-print(f"{Path(lib).name} {cfg} {ts[len(ts) // 2]:.1f} us  (min {ts[0]:.1f}) {'ok' if ok else 'MISMATCH'}")
+print(f"{Path(lib).name} {cfg} {what} {ts[len(ts) // 2]:.1f} us  (min {ts[0]:.1f}) "
+      f"{'ok' if ok else 'MISMATCH'}")
