@@ -41,6 +41,11 @@ CONFIGS = {
     "cfg4": (512, 13824, 5120, "Llama-13B linear, M=512, K=5120, N=13824"),
     "cfg5": (1024, 28672, 8192, "Llama-70B MLP, M=1024, K=8192, N=28672"),
 }
+# BASELINE config 3 is a batch sweep (Fig 8a): the memory- to compute-bound crossover of the
+# Llama-7B MLP up/gate (K=4096 -> N=11008) and down (K=11008 -> N=4096) projections
+for _m in (8, 16, 32, 64, 128, 256, 512, 1024):
+    CONFIGS[f"cfg3_up_m{_m}"] = (_m, 11008, 4096, f"Llama-7B MLP up/gate, M={_m}, K=4096, N=11008")
+    CONFIGS[f"cfg3_down_m{_m}"] = (_m, 4096, 11008, f"Llama-7B MLP down, M={_m}, K=11008, N=4096")
 METRIC = "W4A4 mixed GEMM effective TOPS and % roofline at Llama-7B/70B shapes, 1/2/4/8 B200"
 UNIT = "TOPS"
 K_OUT = 128
@@ -443,6 +448,25 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
         swiglu_us = 1e3 * sum(a.elapsed_time(b) for a, b in es) / len(es)
         swiglu_bytes = quant_bytes(M, N) + M * N * 2        # a second fp16 input row
 
+    # the box's INT8 tensor peak, measured in this run: cuBLAS int8 GEMM (torch._int_mm, 8192^3)
+    int8_meas = None
+    if rank == 0 and not args.no_peak:
+        try:
+            a8 = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device=dev)
+            b8 = torch.randint(-128, 127, (8192, 8192), dtype=torch.int8, device=dev)
+            for _ in range(3):
+                torch._int_mm(a8, b8)
+            ep = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ep[0].record()
+            for _ in range(10):
+                torch._int_mm(a8, b8)
+            ep[1].record()
+            torch.cuda.synchronize()
+            int8_meas = 2.0 * 8192 ** 3 / (ep[0].elapsed_time(ep[1]) / 10 * 1e-3) / 1e12
+            del a8, b8
+        except Exception as ex:   # report, never fail the bench on it
+            int8_meas = f"unavailable: {type(ex).__name__}"
+
     if rank != 0:
         return
     peaks, peak_src = load_peaks()
@@ -478,7 +502,12 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
                                     f"(int8/bf16 nominal ratio)"},
         "roofline_spec": {"t_roof_us": t_roof_spec * 1e6, "t_gemm_us": g_avg * 1e3,
                           "frac": t_roof_spec / (g_avg * 1e-3),
+                          "bound": "tensor" if 2.0 * M * Nr * K_r / 4.5e15 >=
+                                   algorithmic_bytes(M, Nr, K_r) / 8e12 else "hbm",
                           "model": "max(2MNK/4.5e15, bytes/8e12) per GPU (BASELINE.json)"},
+        "int8_peak_in_run": None if int8_meas is None else {
+            "TOPS": int8_meas, "how": "torch._int_mm int8 8192^3, 10 back-to-back calls",
+            "gemm_frac": achieved / int8_meas if isinstance(int8_meas, float) else None},
         "kernels": {
             "reorder_quantize": {"us": q_avg * 1e3, "GB/s": qb / (q_avg * 1e-3) / 1e9,
                                  "frac_hbm": qb / (q_avg * 1e-3) / 1e9 / peaks["hbm_gbs"]},
@@ -560,6 +589,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the step's kernels directly instead of replaying CUDA graphs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-peak", action="store_true", help="skip the in-run int8 peak measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--dry-run", action="store_true",
                     help="multi-rank plumbing only (gloo, no GPU work): prints the shard table")
