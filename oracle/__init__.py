@@ -53,6 +53,8 @@ def lib():
         L.oracle_rmsnorm_rows.restype = ctypes.c_int
         L.oracle_silu_mul_rows.argtypes = [P, P, i64, i64, P]
         L.oracle_silu_mul_rows.restype = ctypes.c_int
+        L.oracle_expf_pinned.argtypes = [ctypes.c_float]
+        L.oracle_expf_pinned.restype = ctypes.c_float
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_max_threads.restype = ctypes.c_int
         for f in (L.oracle_quantize_rows, L.oracle_group_partials, L.oracle_gemm_output,
@@ -126,6 +128,11 @@ def rmsnorm_quantize_rows(x, gamma, perm, K: int, k_outlier: int = 128, eps: flo
     """N1 followed by O2-O6: what the fused RMSNorm + reorder + quantize kernel must produce."""
     y = rmsnorm_rows(x, gamma, eps)
     return quantize_rows(y, perm, K, k_outlier, clip_int4, clip_int8)
+
+
+def expf_pinned(x: float) -> float:
+    """The binary32 exponential of the SwiGLU reading G20 (oracle_expf_pinned)."""
+    return float(lib().oracle_expf_pinned(ctypes.c_float(x)))
 
 
 def silu_mul_rows(g, u):

@@ -152,13 +152,30 @@ int oracle_quantize_rows(const float* x, int64_t rows, int64_t ldx, const int32_
 }
 
 /*
- * N1 (NEXT-1, the "prior operator" the paper fuses reordering and quantization into: P:242 "fuses
+ * Sum of x_c^2 over fp16-valued x, EXACTLY, rounded once to double (reading G19): an
+ * fp16 value is an integer multiple of 2^-24, so x^2 * 2^48 is an integer (< 2^80) and the sum of
+ * up to 2^13 of them fits a 128-bit integer; the exact sum is then rounded to the nearest double
+ * (the compiler's __int128 -> double conversion, round-to-nearest-even) and scaled by 2^-48
+ * (exact).  Order-independent by construction.
+ */
+static double oracle_sum_squares(const float* x, int64_t C) {
+  unsigned __int128 acc = 0;
+  for (int64_t c = 0; c < C; ++c) {
+    const double v = fabs((double)x[c]) * 16777216.0;   /* |x| * 2^24: an exact integer */
+    const unsigned __int128 m = (unsigned __int128)(uint64_t)v;
+    acc += m * m;                                      /* x^2 * 2^48, exact */
+  }
+  return ldexp((double)acc, -48);
+}
+
+/*
+ * N1 (NEXT-1, the "prior operator" the paper fuses reordering and quantization into: P:242, "fuses
  * the activation matrix reordering operators into the prior operator", "we fuse the
  * quantization operator into the prior operator (e.g., LayerNorm)").  The paper does not define
  * the norm; the Llama models it evaluates use RMSNorm (reading G19):
  *     y_c = x_c / sqrt(mean_c(x_c^2) + eps) * gamma_c,   c in [0, C)
  * with the arithmetic pinned as follows (x and gamma are fp16 values widened exactly to fp32):
- *     ss = sum_c (double)x_c * (double)x_c      (each square exact in double; c ascending)
+ *     ss = RN64( sum_c x_c^2 )                   (the exact sum, one rounding: oracle_sum_squares)
  *     r  = RN32( 1.0 / sqrt(ss / C + (double)eps) )   (double ops, one final rounding to fp32)
  *     y_c = RN32( RN32(x_c * r) * gamma_c )      (two binary32 multiplies, in this order)
  * The caller rounds y to fp16 (round-to-nearest-even) before the quantizer, as an fp16 RMSNorm
@@ -171,8 +188,7 @@ int oracle_rmsnorm_rows(const float* x, int64_t rows, int64_t ldx, int64_t C, co
 #pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < rows; ++r) {
     const float* xr = x + r * ldx;
-    double ss = 0.0;
-    for (int64_t c = 0; c < C; ++c) ss += (double)xr[c] * (double)xr[c];
+    const double ss = oracle_sum_squares(xr, C);
     const float rinv = (float)(1.0 / sqrt(ss / (double)C + (double)eps));
     for (int64_t c = 0; c < C; ++c) {
       const float t = xr[c] * rinv;              /* one IEEE multiply */
@@ -183,10 +199,44 @@ int oracle_rmsnorm_rows(const float* x, int64_t rows, int64_t ldx, int64_t C, co
 }
 
 /*
+ * The binary32 exponential of the SwiGLU (reading G20), written out operation by
+ * operation so that any implementation reproduces it bit for bit (each line one IEEE operation,
+ * fmaf = fused multiply-add with one rounding):
+ *     x > 88           -> +inf              x < -87 -> 0      (beyond: silu(g) = g or -0 in fp16)
+ *     n = rint(x * L2E)                     L2E = 0x3FB8AA3B (log2 e), round half to even
+ *     r = fmaf(-n, LN2_HI, x)               LN2_HI = 0x3F317200 (0.693145751953125)
+ *     r = fmaf(-n, LN2_LO, r)               LN2_LO = 0x35BFBE8E (1.42860677e-06)
+ *     p = 1/720;  p = fmaf(p, r, 1/120);  p = fmaf(p, r, 1/24);  p = fmaf(p, r, 1/6);
+ *     p = fmaf(p, r, 1/2);  p = fmaf(p, r, 1);  p = fmaf(p, r, 1)     (Taylor, |r| <= 0.35)
+ *     e = p * 2^n                           (ldexpf: exact, normal range)
+ * Accurate to a few binary32 ulps of exp(x) on [-87, 88] (pinned against libm's double exp in
+ * tests/test_oracle_pins.py).
+ */
+float oracle_expf_pinned(float x) {
+  if (x > 88.0f) return INFINITY;
+  if (x < -87.0f) return 0.0f;
+  const float L2E = 1.44269502162933349609375f, LN2_HI = 0.693145751953125f;
+  const float LN2_LO = 1.428606765330187045037746429443359375e-06f;
+  const float n = rintf(x * L2E);
+  float r = fmaf(-n, LN2_HI, x);
+  r = fmaf(-n, LN2_LO, r);
+  float p = 1.0f / 720.0f;
+  p = fmaf(p, r, 1.0f / 120.0f);
+  p = fmaf(p, r, 1.0f / 24.0f);
+  p = fmaf(p, r, 1.0f / 6.0f);
+  p = fmaf(p, r, 0.5f);
+  p = fmaf(p, r, 1.0f);
+  p = fmaf(p, r, 1.0f);
+  return ldexpf(p, (int)n);
+}
+
+/*
  * N4 (NEXT-4 piece: the down projection's prior operator in a Llama MLP, "we fuse the
  * quantization operator into the prior operator").  The paper does not define the MLP; Llama's is
- * down(silu(gate(x)) * up(x)) (reading G20), with the elementwise step pinned as
- *     s_c = RN32( (double)g_c / (1.0 + exp(-(double)g_c)) )   (double ops, one rounding)
+ * down(silu(gate(x)) * up(x)) (reading G20), with the elementwise step pinned in
+ * binary32 as
+ *     e_c = oracle_expf_pinned(-g_c)
+ *     s_c = RN32( g_c / RN32(1 + e_c) )                        (IEEE add, IEEE division)
  *     h_c = RN32( s_c * u_c )                                  (one binary32 multiply)
  * g and u are the fp16 gate / up outputs widened exactly to fp32; the caller rounds h to fp16
  * (round-to-nearest-even) before the quantizer.  Output: h32 fp32 [rows][C], C = ldx.
@@ -197,8 +247,10 @@ int oracle_silu_mul_rows(const float* g, const float* u, int64_t rows, int64_t l
 #pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < rows; ++r)
     for (int64_t c = 0; c < ldx; ++c) {
-      const double gd = (double)g[r * ldx + c];
-      const float s = (float)(gd / (1.0 + exp(-gd)));
+      const float gc = g[r * ldx + c];
+      const float e = oracle_expf_pinned(-gc);
+      const float d = 1.0f + e;                 /* one IEEE add */
+      const float s = gc / d;                   /* one IEEE division */
       h32[r * ldx + c] = s * u[r * ldx + c];     /* one IEEE multiply */
     }
   return ORC_OK;

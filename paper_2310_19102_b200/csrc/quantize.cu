@@ -36,12 +36,56 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
 }
 
 // kNorm (NEXT-1): the RMSNorm the paper fuses the quantizer into is applied to the
-// staged row first: r = RN32(1/sqrt(sum(x^2)/ldx + eps)) from a double sum of squares, and the
-// gathered value becomes y = fp16_rn(RN32(RN32(x*r) * gamma)) (oracle N1, reading G19).
+// staged row first: r = RN32(1/sqrt(ss/ldx + eps)) where ss is the EXACT sum of squares rounded
+// once to double (128-bit integer accumulation of x^2 * 2^48: order-independent by
+// construction), and the gathered value becomes y = fp16_rn(RN32(RN32(x*r) * gamma)) (oracle N1,
+// reading G19).
 // kPre: 0 = plain a1; 1 = RMSNorm first (NEXT-1); 2 = SwiGLU first (NEXT-4 piece): x is the
 // gate projection and `up` the up projection of a Llama MLP, and the staged value is
-// h = fp16_rn(RN32(RN32(silu(g)) * u)), silu(g) = g / (1 + exp(-g)) evaluated in double (reading
-// G20), i.e. the down projection's input, quantized without an fp16 round trip through HBM.
+// h = fp16_rn(RN32(s * u)), s = RN32(g / RN32(1 + e)), e = the pinned binary32 exp(-g) of reading
+// G20 (expf_pinned below), i.e. the down projection's input, quantized without an fp16 round
+// trip through HBM.
+
+// The binary32 exponential of reading G20 (oracle_expf_pinned), one IEEE operation per step.
+__device__ __forceinline__ float expf_pinned(float x) {
+  if (x > 88.0f) return __int_as_float(0x7F800000);
+  if (x < -87.0f) return 0.0f;
+  const float L2E = 1.44269502162933349609375f, LN2_HI = 0.693145751953125f;
+  const float LN2_LO = 1.428606765330187045037746429443359375e-06f;
+  const float n = rintf(__fmul_rn(x, L2E));
+  float r = __fmaf_rn(-n, LN2_HI, x);
+  r = __fmaf_rn(-n, LN2_LO, r);
+  float p = 1.0f / 720.0f;
+  p = __fmaf_rn(p, r, 1.0f / 120.0f);
+  p = __fmaf_rn(p, r, 1.0f / 24.0f);
+  p = __fmaf_rn(p, r, 1.0f / 6.0f);
+  p = __fmaf_rn(p, r, 0.5f);
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  // p * 2^n with one rounding (= ldexpf): 2^n is a normal binary32 for n in [-126, 127]
+  return __fmul_rn(p, __int_as_float((static_cast<int>(n) + 127) << 23));
+}
+
+// 128-bit unsigned accumulator (hi, lo) of x^2 * 2^48 for fp16-valued x (exact).
+struct U128 {
+  unsigned long long lo = 0, hi = 0;
+  __device__ __forceinline__ void add(unsigned long long plo, unsigned long long phi) {
+    lo += plo;
+    hi += phi + (lo < plo ? 1ull : 0ull);
+  }
+  __device__ __forceinline__ void add_square(float x) {
+    const unsigned long long m = __float2ull_rz(fabsf(x) * 16777216.0f);   // |x| * 2^24, exact
+    add(m * m, __umul64hi(m, m));
+  }
+  // round-to-nearest-even conversion of the 128-bit integer to double
+  __device__ __forceinline__ double to_double() const {
+    if (hi == 0) return __ull2double_rn(lo);
+    const int sh = 64 - __clzll(static_cast<long long>(hi));   // bits of hi: shift right by sh
+    unsigned long long m = (hi << (64 - sh)) | (lo >> sh);
+    if ((lo & ((1ull << sh) - 1ull)) != 0) m |= 1ull;          // sticky, far below bit 11
+    return ldexp(__ull2double_rn(m), sh);
+  }
+};
 template <int kPre>
 __global__ void __launch_bounds__(kQuantThreads)
 reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
@@ -62,12 +106,13 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
   // PDL: x (and the outputs) may belong to the previous kernel of the stream
   griddep_wait();
   griddep_launch();
-  // Stage the whole source row (the gather may touch any channel).  Plain a1: one bulk copy
-  // (a single HBM round trip per row, no per-thread load -> store chains).
+  // Stage the whole source row (the gather may touch any channel).  Plain a1 and the RMSNorm:
+  // one bulk copy (a single HBM round trip per row, no per-thread load -> store chains); the
+  // SwiGLU combines two rows element-wise on the way in, with 4 loads of each in flight.
   const uint4* src = reinterpret_cast<const uint4*>(x + row * ldx);
   const int n16 = static_cast<int>(ldx / 8);
-  double ss = 0.0;
-  if constexpr (kPre == 0) {
+  U128 ss;
+  if constexpr (kPre != 2) {
     __shared__ uint64_t bar;
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
@@ -77,47 +122,67 @@ reorder_quantize_kernel(const __half* __restrict__ x, int64_t rows, int64_t ldx,
     }
     __syncthreads();
     mbar_wait(&bar, 0);
-  }
-  for (int i = threadIdx.x; kPre != 0 && i < n16; i += kQuantThreads) {
-    uint4 v = ld_stream_u4(src + i);
-    if constexpr (kPre == 2) {
-      const uint4 w = ld_stream_u4(reinterpret_cast<const uint4*>(up + row * ldx) + i);
-      __half2* hg = reinterpret_cast<__half2*>(&v);
-      const __half2* hu = reinterpret_cast<const __half2*>(&w);
+    if constexpr (kNorm) {
+      for (int i = threadIdx.x; i < n16; i += kQuantThreads) {
+        const uint4 v = srow4[i];
+        const __half2* h = reinterpret_cast<const __half2*>(&v);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 g = __half22float2(hg[k]), u = __half22float2(hu[k]);
-        const double gx = g.x, gy = g.y;
-        const float sx = __double2float_rn(__ddiv_rn(gx, __dadd_rn(1.0, exp(-gx))));
-        const float sy = __double2float_rn(__ddiv_rn(gy, __dadd_rn(1.0, exp(-gy))));
-        hg[k] = __floats2half2_rn(__fmul_rn(sx, u.x), __fmul_rn(sy, u.y));
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(h[k]);
+          ss.add_square(f.x);
+          ss.add_square(f.y);
+        }
       }
     }
-    srow4[i] = v;
-    if constexpr (kNorm) {
-      const __half2* h = reinterpret_cast<const __half2*>(&v);
+  } else {
+    const uint4* upr = reinterpret_cast<const uint4*>(up + row * ldx);
+    constexpr int U = 4;
+    for (int i0 = threadIdx.x; i0 < n16; i0 += U * kQuantThreads) {
+      uint4 gv[U], uv[U];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __half22float2(h[k]);
-        ss = __fma_rn(static_cast<double>(f.x), static_cast<double>(f.x), ss);
-        ss = __fma_rn(static_cast<double>(f.y), static_cast<double>(f.y), ss);
+      for (int j = 0; j < U; ++j) {
+        const int i = i0 + j * kQuantThreads;
+        if (i < n16) {
+          gv[j] = ld_stream_u4(src + i);
+          uv[j] = ld_stream_u4(upr + i);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = i0 + j * kQuantThreads;
+        if (i >= n16) continue;
+        __half2* hg = reinterpret_cast<__half2*>(&gv[j]);
+        const __half2* hu = reinterpret_cast<const __half2*>(&uv[j]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 g = __half22float2(hg[k]), u = __half22float2(hu[k]);
+          const float sx = __fdiv_rn(g.x, __fadd_rn(1.0f, expf_pinned(-g.x)));
+          const float sy = __fdiv_rn(g.y, __fadd_rn(1.0f, expf_pinned(-g.y)));
+          hg[k] = __floats2half2_rn(__fmul_rn(sx, u.x), __fmul_rn(sy, u.y));
+        }
+        srow4[i] = gv[j];
       }
     }
   }
   float rinv = 1.0f;
   if constexpr (kNorm) {
-    // squares of fp16 values are exact in double, so the fused multiply-adds above are plain sums
-    __shared__ double red[kQuantThreads / 32];
+    // exact 128-bit sum over the CTA (integer additions: any order gives the same sum)
+    __shared__ unsigned long long red[kQuantThreads / 32][2];
     __shared__ float rs;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = ss;
+    for (int off = 16; off > 0; off >>= 1)
+      ss.add(__shfl_xor_sync(0xffffffffu, ss.lo, off), __shfl_xor_sync(0xffffffffu, ss.hi, off));
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x / 32][0] = ss.lo;
+      red[threadIdx.x / 32][1] = ss.hi;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kQuantThreads / 32; ++w) t += red[w];
+      U128 t;
+      for (int w = 0; w < kQuantThreads / 32; ++w) t.add(red[w][0], red[w][1]);
+      const double sum = ldexp(t.to_double(), -48);          // RN64 of the exact sum
       rs = __double2float_rn(
-          __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(t, static_cast<double>(ldx)),
+          __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(sum, static_cast<double>(ldx)),
                                               static_cast<double>(eps)))));
     }
     __syncthreads();

@@ -7,6 +7,8 @@ import json
 from fractions import Fraction
 from pathlib import Path
 
+import math
+
 import numpy as np
 import pytest
 
@@ -527,6 +529,30 @@ def test_n1_eps_and_float64_reference():
     assert np.allclose(yt, 1e-3 / np.sqrt(1.0 + 1e-6), rtol=2e-3)
 
 
+def test_n1_exact_sum_of_squares_fractions_and_order():
+    """Reading G19 pins the sum of squares as the EXACT sum rounded once to double.  Pinned
+    against Python's exact rational arithmetic (fractions.Fraction, then one rounding to float64)
+    on rows built so that a running double sum depends on the order (one huge square absorbs the
+    tiny ones unless they are added first), and by order independence: reversing the channels
+    (with gamma) reverses the output bit for bit."""
+    from fractions import Fraction
+    C = 1024
+    x = np.full((2, C), np.float16(2.0 ** -12), np.float16)
+    x[0, 0] = np.float16(60000.0)            # huge first: a running sum drops the tiny squares
+    x[1, -1] = np.float16(60000.0)           # huge last: a running sum keeps them
+    x[1, :8] = np.float16(-3.0)
+    g = (1 + 0.05 * np.random.default_rng(9).standard_normal(C)).astype(np.float16)
+    eps = 1e-6
+    y = oracle.rmsnorm_rows(x, g, eps)
+    for r in range(2):
+        ss = float(sum(Fraction(float(v)) ** 2 for v in x[r].astype(np.float64)))   # exact, RN64
+        rinv = np.float32(1.0 / math.sqrt(ss / C + float(np.float64(np.float32(eps)))))
+        want = ((x[r].astype(np.float32) * rinv) * g.astype(np.float32)).astype(np.float16)
+        np.testing.assert_array_equal(y[r], want)
+    yr = oracle.rmsnorm_rows(x[:, ::-1].copy(), g[::-1].copy(), eps)
+    np.testing.assert_array_equal(yr[:, ::-1], y)
+
+
 def test_n1_fused_oracle_is_norm_then_quantize():
     rng = np.random.default_rng(5)
     K = 1024
@@ -558,6 +584,21 @@ def test_n4_special_values():
     assert np.all(h[2] == 0)
     np.testing.assert_array_equal(oracle.silu_mul_rows(rng.standard_normal((2, C)).astype(np.float16),
                                                        np.zeros((2, C), np.float16)) == 0, True)
+
+
+def test_n4_expf_pinned_accuracy_and_special_values():
+    """The binary32 exponential of reading G20 against libm's double exp on a dense grid of the
+    domain it serves (x = -g for fp16 g): within 4 binary32 ulps (relative 2^-21) on
+    [-87, 88]; exp(0) = 1 exactly; +inf above 88 and 0 below -87.  Catches a wrong constant,
+    a dropped polynomial term or a mis-scaled 2^n."""
+    xs = np.concatenate([np.linspace(-87, 88, 20001), np.float16(np.linspace(-30, 30, 4001))])
+    for x in xs.astype(np.float32):
+        got = oracle.expf_pinned(float(x))
+        want = math.exp(float(x))
+        assert abs(got / want - 1.0) <= 2.0 ** -21, (float(x), got, want)
+    assert oracle.expf_pinned(0.0) == 1.0
+    assert oracle.expf_pinned(88.5) == math.inf and oracle.expf_pinned(1e4) == math.inf
+    assert oracle.expf_pinned(-87.5) == 0.0
 
 
 def test_n4_tanh_form_and_sign():
