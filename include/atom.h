@@ -94,6 +94,13 @@ typedef enum {
 
 typedef enum { ATOM_F16 = 0, ATOM_F32 = 1 } atom_dtype_t;
 
+/* atom_w4a4_gemm_f8 flags.  ATOM_GEMM_SPLIT_FREE: no output tile is split over K between CTAs
+ * (plain round-robin tiles, no stream-K tail, no workspace), so every output is the same fp32
+ * chain -- groups ascending -- for ANY N, and a column shard of the GEMM (tensor-parallel
+ * N-sharding) reproduces the unsharded output bit for bit.  Default (0): stream-K load balance,
+ * deterministic for a given shape but with split points that depend on the shape. */
+#define ATOM_GEMM_SPLIT_FREE 1
+
 /*
  * a1: reorder + dynamic quantize activations ("fuses the activation matrix reordering
  * operators", "tailoring quantization parameters for each activation matrix").
@@ -208,15 +215,16 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
  * in the same pass as the scales: the hot path (quantize -> GEMM) then writes and reads only
  * what the GEMM consumes; the weight scales come in the GEMM channel order w_sp that
  * atom_quantize_weights writes offline.  Same results (bit for bit) and errors as
- * atom_w4a4_gemm; a_f8 and a_ab are required (the activation scales are inside a_ab).  Workspace:
+ * atom_w4a4_gemm; a_f8 and a_ab are required (the activation scales are inside a_ab).  flags: 0 or
+ * ATOM_GEMM_SPLIT_FREE (above; other bits: ATOM_ERR_ARG).  Workspace:
  * atom_w4a4_gemm_f8_workspace_size bytes (may be 0; any atom_w4a4_gemm workspace also serves).
  */
 atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const float* a_ab,
                                 const uint8_t* w_q4, const int8_t* w_q8, const float* w_sp,
                                 int64_t M, int64_t N, int64_t K, int32_t k_outlier,
                                 void* c, int64_t ldc, atom_dtype_t c_dtype,
-                                int32_t* debug_partials, void* workspace, size_t workspace_bytes,
-                                void* stream);
+                                int32_t* debug_partials, int32_t flags, void* workspace,
+                                size_t workspace_bytes, void* stream);
 
 /* Bytes of device workspace atom_w4a4_gemm needs for this shape on the CURRENT device (0 when
  * the current device is not an sm_100 GPU). */

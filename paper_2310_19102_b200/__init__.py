@@ -66,7 +66,7 @@ def _lib():
         L.atom_silu_mul_reorder_quantize.restype = ctypes.c_int
         g_tail = [i64, i64, i64, i32, P, i64, ctypes.c_int, P, P, ctypes.c_size_t, P]
         L.atom_w4a4_gemm.argtypes = [P] * 6 + g_tail
-        L.atom_w4a4_gemm_f8.argtypes = [P] * 5 + g_tail
+        L.atom_w4a4_gemm_f8.argtypes = [P] * 5 + g_tail[:8] + [i32] + g_tail[8:]
         L.atom_w4a4_gemm_f8.restype = ctypes.c_int
         for f in (L.atom_w4a4_gemm_workspace_size, L.atom_w4a4_gemm_f8_workspace_size):
             f.argtypes = [i64, i64, i64, i32]
@@ -285,14 +285,19 @@ def gemm_workspace(M: int, N: int, K: int, k_outlier: int = 128, stream=None):
     return ws
 
 
+GEMM_SPLIT_FREE = 1
+
+
 def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partials=None,
-              workspace=None, stream=None, canonical: bool = False):
+              workspace=None, stream=None, canonical: bool = False, split_free: bool = False):
     """a2-a5: C[m][n] = sum_t s_a[t][m] s_w[t][n] P_t[m][n] (fp32 accumulate), fp16 or fp32 out.
 
     Reads the activation operand form (a.f8, a.ab) through atom_w4a4_gemm_f8 when present,
     else (or with ``canonical=True``) the packed a.q4 / a.q8 through atom_w4a4_gemm.
     ``out`` may be a wider [M][ldc] view (ldc >= N) to write an N-shard in place.
     ``debug_partials``: optional int32 [K/128][M][N] CUDA tensor receiving every exact partial.
+    ``split_free``: no K-split of output tiles (include/atom.h ATOM_GEMM_SPLIT_FREE): column
+    shards then reproduce the unsharded output bit for bit (operand-form path only).
     """
     import torch
     if a.K != w.K or a.k_outlier != w.k_outlier:
@@ -314,6 +319,8 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
         raise ValueError("debug_partials must be a contiguous int32 [K/128][M][N] tensor")
     c_dtype = ATOM_F16 if out.dtype == torch.float16 else ATOM_F32
     use_f8 = a.f8 is not None and w.sp is not None and not canonical
+    if split_free and not use_f8:
+        raise ValueError("split_free needs the operand forms (a.f8 / a.ab and w.sp)")
     if not use_f8 and (a.q4 is None) != (a.K == a.k_outlier):
         raise ValueError("activations lack the packed codes (quantize with packed=True)")
     if workspace is None:
@@ -323,6 +330,7 @@ def w4a4_gemm(a: Quantized, w: Quantized, out=None, out_dtype=None, debug_partia
         st = _lib().atom_w4a4_gemm_f8(_ptr(a.f8), _ptr(a.ab), _ptr(w.q4),
                                       _ptr(w.q8), _ptr(w.sp), M, N, a.K, a.k_outlier,
                                       _ptr(out), out.stride(0), c_dtype, _ptr(debug_partials),
+                                      GEMM_SPLIT_FREE if split_free else 0,
                                       _ptr(workspace), wsz, _stream(stream))
         _check(st, "atom_w4a4_gemm_f8")
     else:

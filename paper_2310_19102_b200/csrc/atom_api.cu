@@ -135,7 +135,8 @@ cudaError_t run_gemm(const uint8_t* af8, const float* ab, const uint8_t* w_q4,
                      const int8_t* w_q8, const float* w_sp, int64_t M,
                      int64_t N, int64_t K, int32_t k_outlier, void* c, int64_t ldc,
                      atom_dtype_t c_dtype, int32_t* debug_partials, void* workspace,
-                     size_t workspace_bytes, void* stream, const DeviceInfo& dev, int* launches) {
+                     size_t workspace_bytes, void* stream, const DeviceInfo& dev, int* launches,
+                     int split_free = 0) {
   atom::GemmArgs a;
   a.a_f8 = af8;
   a.a_ab = ab;
@@ -150,6 +151,7 @@ cudaError_t run_gemm(const uint8_t* af8, const float* ab, const uint8_t* w_q4,
   a.ldc = ldc;
   a.c_f32 = c_dtype == ATOM_F32;
   a.debug_partials = debug_partials;
+  a.split_free = split_free;
   return atom::launch_w4a4_gemm(a, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
                                 dev.num_sms, launches);
 }
@@ -230,22 +232,25 @@ size_t atom_w4a4_gemm_counter_bytes(void) {
 atom_status_t atom_w4a4_gemm_f8(const uint8_t* a_f8, const float* a_ab, const uint8_t* w_q4,
                                 const int8_t* w_q8, const float* w_sp, int64_t M, int64_t N,
                                 int64_t K, int32_t k_outlier, void* c, int64_t ldc,
-                                atom_dtype_t c_dtype, int32_t* debug_partials, void* workspace,
-                                size_t workspace_bytes, void* stream) {
+                                atom_dtype_t c_dtype, int32_t* debug_partials, int32_t flags,
+                                void* workspace, size_t workspace_bytes, void* stream) {
   g_last_launches = 0;
   atom_status_t st = check_gemm_args(w_q4, w_q8, w_sp, M, N, K, k_outlier, c, ldc, c_dtype,
                                      debug_partials);
   if (st != ATOM_OK || M == 0) return st;
+  if ((flags & ~ATOM_GEMM_SPLIT_FREE) != 0) return ATOM_ERR_ARG;
   if (!a_f8 || !a_ab) return ATOM_ERR_NULL;
   if (!aligned16(a_f8) || !aligned16(a_ab)) return ATOM_ERR_ALIGN;
   DeviceInfo dev;
   if ((st = current_device(&dev)) != ATOM_OK) return st;
-  const size_t ws = atom::plan_w4a4_gemm(M, N, K, dev.num_sms).workspace_bytes;
+  const bool split_free = (flags & ATOM_GEMM_SPLIT_FREE) != 0;
+  const size_t ws = atom::plan_w4a4_gemm(M, N, K, dev.num_sms, split_free).workspace_bytes;
   if (ws > 0 && (workspace == nullptr || workspace_bytes < ws || !aligned16(workspace)))
     return ATOM_ERR_WORKSPACE;
   int launches = 0;
   if (run_gemm(a_f8, a_ab, w_q4, w_q8, w_sp, M, N, K, k_outlier, c, ldc, c_dtype,
-               debug_partials, workspace, workspace_bytes, stream, dev, &launches) != cudaSuccess)
+               debug_partials, workspace, workspace_bytes, stream, dev, &launches,
+               split_free ? 1 : 0) != cudaSuccess)
     return ATOM_ERR_CUDA;
   g_last_launches = launches;
   return ATOM_OK;

@@ -101,8 +101,8 @@ struct GemmParams {
   int32_t* debug;
   int M, N, G, G4, c_f32;
   int Mp;                    // rows of a_ab per group (M rounded up to 128)
-  int m_tiles;
-  int dp_waves;              // whole tiles per CTA dealt round-robin
+  int m_tiles, num_tiles;
+  int dp_waves;              // whole tiles per CTA dealt round-robin (at most)
   int64_t sk_base;           // first stream-K unit (= dp_waves * grid * G)
   int64_t sk_units;          // stream-K (tile, group) units
   float* partials;           // [gridDim.x][kSlotFloats] split-tile partials
@@ -178,7 +178,11 @@ __device__ __forceinline__ Sched make_sched(const GemmParams& p) {
   Sched s;
   s.u0 = sk_start(p, blockIdx.x);
   s.u1 = sk_start(p, blockIdx.x + 1);
-  s.nd = p.dp_waves;
+  // whole tiles blockIdx.x + i * grid, i < dp_waves, that exist (a split-free plan's last wave
+  // may be partial)
+  const int avail = (p.num_tiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                    static_cast<int>(gridDim.x);
+  s.nd = p.dp_waves < avail ? p.dp_waves : avail;
   if (s.u1 > s.u0) {
     s.t_hi = static_cast<int>((s.u1 - 1) / p.G);
     s.ns = s.t_hi - static_cast<int>(s.u0 / p.G) + 1;
@@ -903,10 +907,16 @@ static cudaError_t set_smem_attr(size_t smem) {
 
 // Tile plan: one persistent CTA per SM (or per unit, if fewer); whole tiles in round-robin waves
 // while at least two waves remain, then the rest as evenly divided (tile, group) units.
-GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms) {
+GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms, bool split_free) {
   GemmPlan pl;
   const int64_t G = K / 128;
   pl.num_tiles = ((N + kTileN - 1) / kTileN) * ((M + kTileM - 1) / kTileM);
+  if (split_free) {   // every tile by one CTA over all of K: the same fp32 chain for any shape
+    pl.grid = static_cast<int>(pl.num_tiles < num_sms ? pl.num_tiles : num_sms);
+    pl.dp_waves = static_cast<int>((pl.num_tiles + pl.grid - 1) / pl.grid);
+    pl.sk_units = 0;
+    return pl;
+  }
   const int64_t units = pl.num_tiles * G;
   pl.grid = static_cast<int>(units < num_sms ? units : num_sms);
   const int64_t T = pl.num_tiles, P = pl.grid;
@@ -948,7 +958,7 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
                              cudaStream_t stream, int num_sms, int* launches) {
   *launches = 0;
   if (a.M == 0) return cudaSuccess;
-  const GemmPlan plan = plan_w4a4_gemm(a.M, a.N, a.K, num_sms);
+  const GemmPlan plan = plan_w4a4_gemm(a.M, a.N, a.K, num_sms, a.split_free != 0);
   if (workspace_bytes < plan.workspace_bytes) return cudaErrorInvalidValue;
   const int M = static_cast<int>(a.M), N = static_cast<int>(a.N), K = static_cast<int>(a.K);
   const int k_o = a.k_outlier;
@@ -977,6 +987,7 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   p.G4 = (K - k_o) / 128;
   p.c_f32 = a.c_f32;
   p.m_tiles = (M + kTileM - 1) / kTileM;
+  p.num_tiles = static_cast<int>(plan.num_tiles);
   p.dp_waves = plan.dp_waves;
   p.sk_base = static_cast<int64_t>(plan.dp_waves) * plan.grid * p.G;
   p.sk_units = plan.sk_units;

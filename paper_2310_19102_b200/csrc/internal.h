@@ -51,6 +51,7 @@ struct GemmArgs {
   int64_t ldc;
   int c_f32;
   int32_t* debug_partials;
+  int split_free;           // ATOM_GEMM_SPLIT_FREE: no K-split of any output tile
 };
 
 struct GemmPlan {
@@ -62,7 +63,7 @@ struct GemmPlan {
   size_t workspace_bytes = 0;   // 0 when no tile is split between CTAs
 };
 
-GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms);
+GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms, bool split_free = false);
 
 // Rows of a_ab per group: M rounded up to the 128-token tile.
 int64_t ab_rows(int64_t M);

@@ -51,7 +51,8 @@ class TensorParallelLinear:
     """One Atom linear layer sharded over the default process group (CUDA + NCCL)."""
 
     def __init__(self, w_shard_f16, perm, K: int, shard: str, k_outlier: int = 128,
-                 clip_w: float = 0.85, clip_a: float = 0.9, clip_int8: float = 1.0):
+                 clip_w: float = 0.85, clip_a: float = 0.9, clip_int8: float = 1.0,
+                 split_free: bool = False):
         import torch
         import torch.distributed as dist
 
@@ -60,6 +61,9 @@ class TensorParallelLinear:
         init = dist.is_available() and dist.is_initialized()
         self.P, self.r = (dist.get_world_size(), dist.get_rank()) if init else (1, 0)
         self.shard = shard
+        # N-shard with split_free: every output is the unsharded GEMM's fp32 chain (bit-identical
+        # to one GPU running the same split-free GEMM, include/atom.h ATOM_GEMM_SPLIT_FREE)
+        self.split_free = split_free
         self.clip_a, self.clip_int8 = clip_a, clip_int8
         if shard == "n":
             self.perm, self.K, self.ko = perm, K, k_outlier
@@ -80,7 +84,8 @@ class TensorParallelLinear:
 
     def gemm(self, a, out=None):
         dt = self.torch.float16 if self.shard == "n" else self.torch.float32
-        return self.atom.w4a4_gemm(a, self.w, out=out, out_dtype=dt)
+        return self.atom.w4a4_gemm(a, self.w, out=out, out_dtype=dt,
+                                   split_free=self.split_free and self.shard == "n")
 
     def combine(self, local, gathered=None):
         """The collective step (a6).  NCCL in production; the gloo branch (CPU staging) exists

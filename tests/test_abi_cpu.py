@@ -75,13 +75,13 @@ def test_host_validation_without_device(lib):
     assert lib.atom_quantize_weights(None, 4, 250, None, 256, 128, f(0.85), f(1.0), None, None,
                                      None, None, None) == 2
     z6 = (None,) * 6
-    for gemm, zp in ((lib.atom_w4a4_gemm, z6), (lib.atom_w4a4_gemm_f8, z6[:5])):
-        assert gemm(*zp, 4, 100, 256, 128, None, 128, 0, None, None, 0, None) == 2
-        assert gemm(*zp, 4, 128, 256, 128, None, 128, 3, None, None, 0, None) == 4
-        assert gemm(*zp, 4, 128, 256, 128, None, 128, 0, None, None, 0, None) == 1
-        assert gemm(*zp, 4, 128, 256, 128, None, 100, 0, None, None, 0, None) == 2   # ldc < N
+    for gemm, zp, fl in ((lib.atom_w4a4_gemm, z6, ()), (lib.atom_w4a4_gemm_f8, z6[:5], (0,))):
+        assert gemm(*zp, 4, 100, 256, 128, None, 128, 0, None, *fl, None, 0, None) == 2
+        assert gemm(*zp, 4, 128, 256, 128, None, 128, 3, None, *fl, None, 0, None) == 4
+        assert gemm(*zp, 4, 128, 256, 128, None, 128, 0, None, *fl, None, 0, None) == 1
+        assert gemm(*zp, 4, 128, 256, 128, None, 100, 0, None, *fl, None, 0, None) == 2   # ldc < N
         # M == 0 is a no-op that succeeds without a device
-        assert gemm(*zp, 0, 128, 256, 128, None, 128, 0, None, None, 0, None) == 0
+        assert gemm(*zp, 0, 128, 256, 128, None, 128, 0, None, *fl, None, 0, None) == 0
     assert lib.atom_w4a4_gemm_workspace_size(1024, 28672, 8192, 128) == 0
     assert lib.atom_w4a4_gemm_f8_workspace_size(1024, 28672, 8192, 128) == 0
     assert lib.atom_last_launch_count() == 0
@@ -101,6 +101,24 @@ def test_silu_mul_quantize_host_validation(lib):
     assert lib.atom_silu_mul_reorder_quantize(None, None, 0, 256, None, 256, 128, f(0.9), f(1.0),
                                               *z6) == 0
     assert lib.atom_last_launch_count() == 0
+
+
+def test_bench_gpus_2_spawns_two_ranks_dry_run():
+    """`python bench.py --gpus 2` (the driver's launch form) starts two ranks itself (torchrun on
+    127.0.0.1); --dry-run exercises that rank plumbing with gloo on CPU: both ranks report their
+    N-shard and K-shard ranges, which tile the full problem."""
+    import json
+    import subprocess
+    import sys
+    for shard, total in (("n", 28672), ("k", 8192)):
+        out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run",
+                              "--shard", shard], capture_output=True, text=True, timeout=240,
+                             cwd=str(ROOT))
+        line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
+        d = json.loads(line)
+        assert d["n_gpus"] == 2 and [r[0] for r in d["ranks"]] == [0, 1]
+        assert d["ranks"][0][1] == 0 and d["ranks"][0][2] == d["ranks"][1][1]
+        assert d["ranks"][1][2] == total
 
 
 def test_product_package_does_not_import_oracle():

@@ -452,6 +452,35 @@ def test_n_shard_columns(atom):
     assert_close_tol(host(out.float()), ref["c"], "N-shard")
 
 
+@pytest.mark.parametrize("M,N,K,P", [(96, 1024, 2048, 2), (200, 1536, 1024, 3),
+                                     (1024, 28672, 8192, 4), (512, 13824, 5120, 2)])
+def test_n_shard_bit_identical_split_free(atom, M, N, K, P):
+    """with ATOM_GEMM_SPLIT_FREE every output is the same fp32 chain (groups
+    ascending) whatever the tile schedule, so column shards written into place reproduce the
+    unsharded GEMM on one GPU bit for bit (the default stream-K schedule splits tiles at
+    shape-dependent K points: equal there only within the tolerance, test_n_shard_columns)."""
+    import torch
+    X, W, perm = synth.problem(M, N, K, seed=P)
+    pd = dev(perm)
+    aq = atom.reorder_quantize(dev(X), pd)
+    full = atom.w4a4_gemm(aq, atom.quantize_weights(dev(W), pd), split_free=True)
+    out = torch.empty_like(full)
+    nb = N // 128
+    for r in range(P):
+        sl = slice(128 * (r * nb // P), 128 * ((r + 1) * nb // P))
+        wq = atom.quantize_weights(dev(W[sl]), pd)
+        atom.w4a4_gemm(aq, wq, out=out[:, sl], split_free=True)
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
+    dflt = atom.w4a4_gemm(aq, atom.quantize_weights(dev(W), pd))
+    rows = np.unique(np.concatenate([[0, M - 1], np.random.default_rng(P).integers(0, M, 6)]))
+    a4, a8, asc = oracle.quantize_rows(X, perm, K, 128, 0.9, 1.0)
+    w4, w8, wsc = oracle.quantize_rows(W, perm, K, 128, 0.85, 1.0)
+    ref = oracle.output_rows(a4, a8, asc, w4, w8, wsc, M, N, K, 128, rows)
+    assert_close_tol(host(full.float())[rows], ref, "split-free")
+    assert_close_tol(host(dflt.float())[rows], ref, "stream-K")
+
+
 def test_gemm_cuda_graph_replay(atom):
     """The GEMM (and the quantize kernel) captured in a CUDA graph and replayed: identical to
     eager launches (the split-tile counters are self-cleaning, so replays need no memset)."""
@@ -642,4 +671,4 @@ def test_empty_m_is_noop(atom):
     assert L.atom_w4a4_gemm(None, None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
                             None, None, 0, None) == 0
     assert L.atom_w4a4_gemm_f8(None, None, None, None, None, 0, 128, 256, 128, None, 128, 0,
-                               None, None, 0, None) == 0
+                               None, 0, None, 0, None) == 0

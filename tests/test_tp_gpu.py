@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, shard, M, N, K, q):
+def _worker(rank, world, port, shard, M, N, K, q, split_free=False):
     import torch.distributed as dist
     import paper_2310_19102_b200 as atom
     from paper_2310_19102_b200 import tp
@@ -38,7 +38,8 @@ def _worker(rank, world, port, shard, M, N, K, q):
         else:
             W = synth.weights(N, K, 5)
         pd = torch.from_numpy(perm).cuda()
-        layer = tp.TensorParallelLinear(torch.from_numpy(W).cuda(), pd, K, shard)
+        layer = tp.TensorParallelLinear(torch.from_numpy(W).cuda(), pd, K, shard,
+                                        split_free=split_free)
         out = layer(torch.from_numpy(X).cuda())
         if shard == "n":
             out = tp.blocks_to_matrix(out)
@@ -132,3 +133,75 @@ def test_tp_paired_mlp(world):
         assert p.exitcode == 0
     err = np.abs(y.astype(np.float64) - ref)
     assert np.all(err <= 2.0 ** -10 + 1e-3 * np.abs(ref)), np.max(err)
+
+
+def test_tp_n_shard_split_free_bit_identical_to_one_gpu():
+    """Two N-shard ranks (gloo, one GPU) with the split-free GEMM: the gathered output equals the
+    single-GPU split-free GEMM of the whole layer bit for bit."""
+    import paper_2310_19102_b200 as atom
+    from paper_2310_19102_b200 import tp
+    M, N, K = 64, 1024, 2048
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, "n", M, N, K, q, True)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=600)
+    for p in ps:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    X, perm = synth.activations(M, K, 5), synth.perm_for(K, 5)
+    W = synth.weights(N, K, 5)
+    pd = torch.from_numpy(perm).cuda()
+    one = tp.TensorParallelLinear(torch.from_numpy(W).cuda(), pd, K, "n", split_free=True)
+    full = one(torch.from_numpy(X).cuda())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.view(np.uint16), full.cpu().numpy().view(np.uint16))
+
+
+def _nccl_worker(rank, world, port, M, N, K, q):
+    import torch.distributed as dist
+    from paper_2310_19102_b200 import tp
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        X, perm = synth.activations(M, K, 6), synth.perm_for(K, 6)
+        n0, n1 = tp.n_shard_rows(N, world, rank)
+        W = synth.weights(N, K, 6, rows=(n0, n1))
+        layer = tp.TensorParallelLinear(torch.from_numpy(W).cuda(), torch.from_numpy(perm).cuda(),
+                                        K, "n", split_free=True)
+        out = tp.blocks_to_matrix(layer(torch.from_numpy(X).cuda()))
+        torch.cuda.synchronize()
+        if rank == 0:
+            q.put(out.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs 2 GPUs (NCCL world 2)")
+def test_tp_nccl_world2_n_shard():
+    """NCCL, one rank per GPU (the production collective): the all-gathered N-shard output of a
+    split-free layer equals the single-GPU split-free GEMM bit for bit."""
+    from paper_2310_19102_b200 import tp
+    M, N, K = 128, 2048, 4096
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_nccl_worker, args=(r, 2, port, M, N, K, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=600)
+    for p in ps:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    X, perm = synth.activations(M, K, 6), synth.perm_for(K, 6)
+    W = synth.weights(N, K, 6)
+    one = tp.TensorParallelLinear(torch.from_numpy(W).cuda(), torch.from_numpy(perm).cuda(), K,
+                                  "n", split_free=True)
+    full = one(torch.from_numpy(X).cuda())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.view(np.uint16), full.cpu().numpy().view(np.uint16))
