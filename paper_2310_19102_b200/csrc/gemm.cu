@@ -83,6 +83,9 @@ constexpr int kLdX = ATOM_LDX;  // 8-column chunks per 16x256b TMEM load
 #ifndef ATOM_PROBE_MODE
 #define ATOM_PROBE_MODE 0
 #endif
+#if ATOM_PROBE_MODE != 0 && !defined(ATOM_DEV_PROBES)
+#error "ATOM_PROBE_MODE is a development probe: build with -DATOM_DEV_PROBES"
+#endif
 #ifndef ATOM_LD_AHEAD
 #define ATOM_LD_AHEAD 1
 #endif
@@ -229,11 +232,7 @@ __device__ __forceinline__ Item get_item(const GemmParams& p, const Sched& s, in
 // weight expansion): hardware-suspended try_wait, so they do not take issue slots from the
 // epilogue warps of their SM sub-partition.
 __device__ __forceinline__ void wait_off(uint64_t* bar, uint32_t parity) {
-#if defined(ATOM_SPIN_OFF)
-  mbar_wait_test(bar, parity);
-#else
   mbar_wait(bar, parity);
-#endif
 }
 
 // ring position: slot index + phase parity, advanced one step at a time (no division)
@@ -248,20 +247,12 @@ struct Ring {
   }
 };
 
-__device__ __forceinline__ float2 ldg_f2(const float* p) {
-  float2 v;
-  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  return v;
-}
 // 32-byte global load (LDG.E.ENL2.256 on sm_100a)
 __device__ __forceinline__ void ldg_v8(const float* p, float (&v)[8]) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
                  "=f"(v[6]), "=f"(v[7])
                : "l"(p));
-}
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 __device__ __forceinline__ float2 u2f2(uint32_t a, uint32_t b) {
   return make_float2(__uint_as_float(a), __uint_as_float(b));
