@@ -59,7 +59,7 @@ constexpr int kNumUnpackWarps = 4;
 constexpr int kEpiWarp0 = 8;
 constexpr int kNumEpiWarps = 8;
 constexpr int kEpiThreads = kNumEpiWarps * 32;
-constexpr int kRegsProd = 32, kRegsUnpack = 56, kRegsHigh = 208;   // 128*(32+56) + 256*208 <= 65536
+constexpr int kRegsProd = 24, kRegsUnpack = 48, kRegsHigh = 216;   // 128*(24+48) + 256*216 <= 65536
 constexpr int kTileM = 128;     // tokens per tile (MMA M, TMEM lanes)
 constexpr int kTileN = 256;     // output channels per tile (MMA N, TMEM columns)
 #ifndef ATOM_RW
@@ -563,6 +563,11 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         const float* xws = sw_base(xt, xn0);
         float al_n[4], be_n[4];
         if constexpr ((ATOM_PROBE_MODE & 32) == 0) load_ab(xt, xm0, al_n, be_n);
+        // the next group's last 4 channel pairs are loaded now too (into temporaries): a load
+        // issued at the very end of the group would hold the scoreboard that the next group's
+        // first instructions wait on
+        float sw_last[8];
+        ldg_v8(xws + 8 * 12, sw_last);
         mbar_wait_test(&sm.mdone[u.i], u.ph);
         if (e == 0 && lane == 0) TRACE(5, ge);
         if (lane == 0) TRACE(17 + e, ge);
@@ -653,7 +658,14 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             // block cb done for both lane halves: its channel scales are free for the next group
             if constexpr ((ATOM_PROBE_MODE & 16) == 0)
               // blocks cb - 1, cb done for both lane halves: 4 pairs of scales free
-              if (hh == 1 && ((cb + 1) * kLdX) % 4 == 0) load_sw(xws, (cb + 1) * kLdX - 4, 4);
+              if (hh == 1 && ((cb + 1) * kLdX) % 4 == 0) {
+                if ((cb + 1) * kLdX < 16) {
+                  load_sw(xws, (cb + 1) * kLdX - 4, 4);
+                } else {
+#pragma unroll
+                  for (int v = 0; v < 4; ++v) sw[12 + v] = make_float2(sw_last[2 * v], sw_last[2 * v + 1]);
+                }
+              }
           }
         };
         if (t < G4) drain(std::true_type{});
