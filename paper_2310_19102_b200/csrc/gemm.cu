@@ -60,8 +60,6 @@ constexpr int kEpiWarp0 = 8;
 constexpr int kNumEpiWarps = 8;
 constexpr int kEpiThreads = kNumEpiWarps * 32;
 constexpr int kRegsProd = 24, kRegsUnpack = 48, kRegsHigh = 216;   // 128*(24+48) + 256*216 <= 65536
-constexpr int kTileM = 128;     // tokens per tile (MMA M, TMEM lanes)
-constexpr int kTileN = 256;     // output channels per tile (MMA N, TMEM columns)
 #ifndef ATOM_RW
 #define ATOM_RW 2
 #endif
@@ -71,10 +69,8 @@ constexpr int kTileN = 256;     // output channels per tile (MMA N, TMEM columns
 #ifndef ATOM_LDX
 #define ATOM_LDX 2
 #endif
-constexpr int kRS = 4;          // activation slots (= go / mdone ring)
-constexpr int kRW = ATOM_RW;    // expanded weight slots
-constexpr int kRT = 2;          // TMEM accumulator buffers (kTileN columns each)
-constexpr int kKS = ATOM_KS;    // packed INT4 weight stages (one group: kTileN x 64 B)
+constexpr int kRS0 = 4;         // activation slots (= go / mdone ring), kBT = 0 tiles
+constexpr int kRW0 = ATOM_RW;   // expanded weight slots, kBT = 0 tiles
 constexpr int kLdX = ATOM_LDX;  // 8-column chunks per 16x256b TMEM load
 // development timing probes (results wrong by design; only with -DATOM_PROBE_MODE=n):
 // bit 0 = the weight expansion moves no data; bit 1 = the epilogue skips its arithmetic;
@@ -90,11 +86,42 @@ constexpr int kLdX = ATOM_LDX;  // 8-column chunks per 16x256b TMEM load
 #define ATOM_LD_AHEAD 1
 #endif
 constexpr int kLdAhead = ATOM_LD_AHEAD;   // TMEM loads in flight ahead of the one being used
-constexpr uint32_t kTmemCols = kRT * kTileN;
 // split-tile partial of one CTA: [epi warps][32 float4][32 lanes]
 constexpr size_t kSlotFloats = static_cast<size_t>(kNumEpiWarps) * 128 * 32;
-static_assert(kTmemCols <= 512, "TMEM holds at most 512 columns");
-static_assert(kRS >= kRT && kRS >= kRW, "ring sizes");
+
+// Tile configuration.  kBT = 0: the throughput tile, 128 tokens (MMA M, TMEM lanes) x 256 output
+// channels (MMA N, TMEM columns).  kBT in {16, 32, 64} (small M, weight streaming): swap-AB,
+// the weights are the MMA A operand (128 channels = TMEM lanes) and the kBT tokens the B operand
+// (TMEM columns), so the epilogue drains 128 x kBT values per group instead of 128 x 256 of
+// which all but M rows would be padding.
+template <int kBT>
+struct TileCfg {
+  static constexpr bool kSwap = kBT > 0;
+  static constexpr int TT = kSwap ? kBT : 128;      // tokens per tile
+  static constexpr int TN = kSwap ? 128 : 256;      // output channels per tile
+  // swap-AB tiles are cheap to drain, so the rings are deeper there: the loop MMA(g - RW) done
+  // -> expand group g -> MMA(g) would otherwise bound the group rate (~900 clk per group with
+  // 2 expanded-weight slots)
+  static constexpr int RS = kSwap ? 8 : kRS0;       // activation slots (= go / mdone ring)
+  static constexpr int RW = kSwap ? 4 : kRW0;       // expanded weight slots
+  static constexpr int KS = kSwap ? 8 : ATOM_KS;    // packed weight stages (TN x 64 B each)
+  static constexpr int RT = kSwap ? 8 : 2;          // TMEM accumulator buffers
+  // swap-AB: per-group scales staged in shared memory by the activation loader (bulk copies
+  // counted on go[]): the 128 weight scales of the tile (w_sp order) and the a_ab rows of the
+  // 32-row block(s) holding the tile's tokens.  The loader writes group g's slot once MMA(g - RS)
+  // is done, i.e. after the epilogue released group g - RS - RT, so RA > RS + RT slots never
+  // overwrite a slot the epilogue still reads.
+  static constexpr int AB_ROWS = kBT < 32 ? 32 : kBT;
+  static constexpr int RA = kSwap ? 32 : 1;
+  static constexpr int SC_FLOATS = kSwap ? 128 + 2 * AB_ROWS : 4;
+  static_assert(!kSwap || RA > RS + RT, "scale ring");
+  static constexpr int TC = kSwap ? kBT : 256;      // TMEM columns per buffer
+  static constexpr uint32_t kTmemCols = RT * TC < 32 ? 32u : static_cast<uint32_t>(RT * TC);
+  static_assert(RT * TC <= 512, "TMEM holds at most 512 columns");
+  static_assert((kTmemCols & (kTmemCols - 1)) == 0, "TMEM allocations are powers of two");
+  static_assert(RS >= RT && RS >= RW, "ring sizes");
+  static_assert(!kSwap || (kBT == 16 || kBT == 32 || kBT == 64), "swap-AB token tiles");
+};
 
 struct GemmParams {
   const float* a_ab;         // [G][Mp][2] per-row dequant constants (include/atom.h "a_ab")
@@ -118,7 +145,7 @@ struct GemmParams {
 #ifdef ATOM_DEV_PROBES
 // Development-only timeline probe (never in the shipped library): clock64 of event ev for group
 // g of CTA 0.  Built with ATOM_NVCC_EXTRA=-DATOM_DEV_PROBES, enabled by ATOM_GEMM_TRACE=1.
-constexpr int kTraceN = 512, kTraceEv = 25;
+constexpr int kTraceN = 512, kTraceEv = 27;
 #define TRACE(ev, g)                                                                      \
   do {                                                                                    \
     if (p.trace != nullptr && blockIdx.x == 0 && (g) < kTraceN)                           \
@@ -130,18 +157,22 @@ constexpr int kTraceN = 512, kTraceEv = 25;
   } while (0)
 #endif
 
+template <class C>
 struct __align__(1024) GemmSmem {
-  uint8_t a[kRS][kTileM * 128];          // activation group, E4M3 / int8, SW128 K-major (TMA)
-  uint8_t w[kRW][kTileN * 128];          // expanded weight group, SW128 K-major
-  uint8_t stage[kKS][kTileN * 64];       // packed weight group (TMA, no swizzle)
-  uint64_t full[kKS], empty[kKS];
+  uint8_t a[C::RS][C::TT * 128];           // activation group, E4M3 / int8, SW128 K-major (TMA)
+  uint8_t w[C::RW][C::TN * 128];           // expanded weight group, SW128 K-major
+  uint8_t stage[C::KS][C::TN * 64];      // packed weight group (TMA, no swizzle)
+  float sc[C::RA][C::SC_FLOATS];          // swap-AB: staged group scales (16-byte aligned rows)
+  uint64_t full[C::KS], empty[C::KS];
   // go[u]: group g (slot u = g % kRS) may be issued -- its weights are expanded (4 arrivals),
   // its activations landed (1 arrival + tx bytes) and its TMEM buffer was drained (8 epilogue
   // arrivals, made when group g - kRT was released).
-  uint64_t go[kRS];
-  uint64_t mdone[kRS];                   // MMAs of a group done: slots free + partial ready
+  uint64_t go[C::RS];
+  uint64_t mdone[C::RS];                   // MMAs of a group done: slots free + partial ready
   uint32_t tmem_base;
 };
+static_assert(sizeof(GemmSmem<TileCfg<0>>) + 1024 <= 232448, "shared memory");
+static_assert(sizeof(GemmSmem<TileCfg<64>>) + 1024 <= 232448, "shared memory");
 
 // Packed INT4 weights -> E4M3 offset-binary bytes (nibble ^ 8 = q + 8 in [0, 15]: the E4M3 byte
 // of (q + 8) * 2^-9).  Low nibbles (even channels) and high nibbles (odd channels) of a 16-byte
@@ -199,6 +230,7 @@ __device__ __forceinline__ Sched make_sched(const GemmParams& p) {
 struct Item {
   int n0, m0, t0, t1, tile;
 };
+template <class C>
 __device__ __forceinline__ Item get_item(const GemmParams& p, const Sched& s, int k) {
   Item it;
   int tile;
@@ -223,8 +255,8 @@ __device__ __forceinline__ Item get_item(const GemmParams& p, const Sched& s, in
     it.t0 = 0;
     it.t1 = p.G;
   }
-  it.n0 = (tile / p.m_tiles) * kTileN;
-  it.m0 = (tile % p.m_tiles) * kTileM;
+  it.n0 = (tile / p.m_tiles) * C::TN;
+  it.m0 = (tile % p.m_tiles) * C::TT;
   return it;
 }
 
@@ -258,13 +290,24 @@ __device__ __forceinline__ float2 u2f2(uint32_t a, uint32_t b) {
   return make_float2(__uint_as_float(a), __uint_as_float(b));
 }
 
-template <bool kDebug>
+template <int kBT, bool kDebug>
 __global__ void __launch_bounds__(kThreads, 1)
 w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
                  const __grid_constant__ CUtensorMap tm_wq8,
                  const __grid_constant__ CUtensorMap tm_af8, const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
-  GemmSmem& sm = *reinterpret_cast<GemmSmem*>(
+#ifdef ATOM_DEV_PROBES
+  auto gtimer = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return static_cast<long long>(t);
+  };
+  if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceN)
+    p.trace[25 * kTraceN + blockIdx.x] = gtimer();
+#endif
+  using C = TileCfg<kBT>;
+  constexpr int kKS = C::KS, kRT = C::RT, kRS = C::RS, kRW = C::RW;
+  GemmSmem<C>& sm = *reinterpret_cast<GemmSmem<C>*>(
       smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -272,10 +315,10 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
   if (threadIdx.x == 0) {
     for (int s = 0; s < kKS; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kNumUnpackWarps);
+      mbar_init(&sm.empty[s], C::kSwap ? 1 : kNumUnpackWarps);
     }
     for (int u = 0; u < kRS; ++u) {
-      mbar_init(&sm.go[u], kNumUnpackWarps + 1 + kNumEpiWarps);
+      mbar_init(&sm.go[u], (C::kSwap ? 1 : kNumUnpackWarps) + 1 + kNumEpiWarps);
       mbar_init(&sm.mdone[u], 1);
     }
     fence_mbar_init();
@@ -285,7 +328,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     tma_prefetch_desc(&tm_wq8);
     tma_prefetch_desc(&tm_af8);
   }
-  if (warp == 1) tmem_alloc(&sm.tmem_base, kTmemCols);
+  if (warp == 1) tmem_alloc(&sm.tmem_base, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -306,20 +349,20 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         Ring<kKS> st;
         const uint64_t pol_w = l2_policy_evict_first();
         if (n_items > 0) {   // PDL: warm L2 with the first weight groups while the previous ends
-          const Item w = get_item(p, sch, 0);
+          const Item w = get_item<C>(p, sch, 0);
           for (int t = w.t0, s = 0; t < w.t1 && t < G4 && s < kKS; ++t, ++s)
             tma_prefetch_2d(&tm_wq4, t * 64, w.n0);
         }
         griddep_wait();
         int gp = 0;
         for (int k = 0; k < n_items; ++k) {
-          const Item w = get_item(p, sch, k);
+          const Item w = get_item<C>(p, sch, k);
           for (int t = w.t0; t < w.t1; ++t, ++gp) {
             const int nst = t < G4 ? 1 : 2;
             for (int h = 0; h < nst; ++h, st.next()) {
               mbar_wait(&sm.empty[st.i], st.ph ^ 1);
               TRACE(0, gp);
-              mbar_arrive_expect_tx(&sm.full[st.i], kTileN * 64);
+              mbar_arrive_expect_tx(&sm.full[st.i], C::TN * 64);
               // read by the m-tiles of this n-tile at about the same time, then dead
               if (t < G4)
                 tma_load_2d_hint(sm.stage[st.i], &tm_wq4, &sm.full[st.i], t * 64, w.n0, pol_w);
@@ -341,16 +384,25 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         griddep_wait();                  // activations and scales come from the previous kernel
         int ga = 0;
         for (int k = 0; k < n_items; ++k) {
-          const Item w = get_item(p, sch, k);
-          const uint32_t sw_bytes = static_cast<uint32_t>(min(kTileN, p.N - w.n0)) * 4;
+          const Item w = get_item<C>(p, sch, k);
+          const uint32_t sw_bytes = static_cast<uint32_t>(min(C::TN, p.N - w.n0)) * 4;
           for (int t = w.t0; t < w.t1; ++t, u.next(), ++ga) {
             wait_off(&sm.mdone[u.i], u.ph ^ 1);
             TRACE(1, ga);
-            mbar_arrive_expect_tx(&sm.go[u.i], kTileM * 128);
+            if constexpr (C::kSwap) {
+              float* sc = sm.sc[ga % C::RA];
+              mbar_arrive_expect_tx(&sm.go[u.i], C::TT * 128 + 512 + C::AB_ROWS * 8);
+              tma_load_2d_hint(sm.a[u.i], &tm_af8, &sm.go[u.i], t * 128, w.m0, pol_a);
+              bulk_g2s(sc, p.w_sp + static_cast<int64_t>(t) * p.N + w.n0, 512, &sm.go[u.i]);
+              bulk_g2s(sc + 128, p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + (w.m0 & ~31)),
+                       C::AB_ROWS * 8, &sm.go[u.i]);
+              continue;
+            }
+            mbar_arrive_expect_tx(&sm.go[u.i], C::TT * 128);
             // re-read by every n-tile: keep in L2
             tma_load_2d_hint(sm.a[u.i], &tm_af8, &sm.go[u.i], t * 128, w.m0, pol_a);
             prefetch_l2_bulk(p.w_sp + static_cast<int64_t>(t) * p.N + w.n0, sw_bytes);
-            prefetch_l2_bulk(p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + w.m0), kTileM * 8);
+            prefetch_l2_bulk(p.a_ab + 2 * (static_cast<int64_t>(t) * p.Mp + w.m0), C::TT * 8);
           }
         }
       }
@@ -361,7 +413,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         Ring<kRS> u;
         int go_ = 0;
         for (int k = 0; k < n_items; ++k) {
-          const Item w = get_item(p, sch, k);
+          const Item w = get_item<C>(p, sch, k);
           for (int t = w.t0; t < w.t1; ++t, u.next(), ++go_) {
             mbar_wait_spin(&sm.mdone[u.i], u.ph);
             TRACE(8, go_);
@@ -373,10 +425,13 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       // ===================== MMA issuer (single thread) =====================
       // Every instruction this thread executes between dispatches idles the tensor pipe for as
       // long (tcgen05.mma issue returns only as the previous dispatch drains), so the loop is
-      // one barrier probe, 4 dispatches and one commit per group.
+      // one barrier probe, 4 dispatches and one commit per group.  (Swap-AB: a 128 x kBT x 32
+      // dispatch takes ~130 clk from issue to drain whatever kBT is; a second issuing thread
+      // for alternate groups measured no faster.)
       if (lane == 0) {
-        constexpr uint32_t id4 = umma_idesc_e4m3(kTileM, kTileN);
-        constexpr uint32_t id8 = umma_idesc_i8(kTileM, kTileN);
+        // swap-AB: A = the weights (128 channels), B = the kBT tokens
+        constexpr uint32_t id4 = umma_idesc_e4m3(128, C::kSwap ? kBT : C::TN);
+        constexpr uint32_t id8 = umma_idesc_i8(128, C::kSwap ? kBT : C::TN);
         const uint64_t da0 = umma_desc_sw128(smem_u32(sm.a[0]));
         const uint64_t db0 = umma_desc_sw128(smem_u32(sm.w[0]));
         Ring<kRS> u;
@@ -384,21 +439,22 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         Ring<kRT> b;
         int gm = 0;
         for (int k = 0; k < n_items; ++k) {
-          const Item w = get_item(p, sch, k);
+          const Item w = get_item<C>(p, sch, k);
           for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), b.next(), ++gm) {
             mbar_wait_test(&sm.go[u.i], u.ph);
             TRACE(3, gm);
             tc_fence_after();
-            const uint32_t d = tmem + b.i * kTileN;
+            const uint32_t d = tmem + b.i * C::TC;
             // descriptor start address field counts 16-byte units: slot, K step kk (32 bytes)
-            const uint64_t da = da0 + u.i * (kTileM * 128 / 16);
-            const uint64_t db = db0 + uw.i * (kTileN * 128 / 16);
+            const uint64_t da = da0 + u.i * (C::TT * 128 / 16);
+            const uint64_t db = db0 + uw.i * (C::TN * 128 / 16);
+            const uint64_t dA = C::kSwap ? db : da, dB = C::kSwap ? da : db;
             if (t < G4) {
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) umma_e4m3(d, da + 2 * kk, db + 2 * kk, id4, kk > 0);
+              for (int kk = 0; kk < 4; ++kk) umma_e4m3(d, dA + 2 * kk, dB + 2 * kk, id4, kk > 0);
             } else {
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) umma_i8(d, da + 2 * kk, db + 2 * kk, id8, kk > 0);
+              for (int kk = 0; kk < 4; ++kk) umma_i8(d, dA + 2 * kk, dB + 2 * kk, id8, kk > 0);
             }
             umma_commit(&sm.mdone[u.i]);
           }
@@ -407,14 +463,95 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     }
   } else if (warp < kEpiWarp0) {
     setmaxnreg_dec<kRegsUnpack>();
+    if constexpr (C::kSwap) {
+      // ===== swap-AB weight expansion: unpack warp uw expands every 4th group on its own
+      //       (groups g = uw mod 4), so 4 groups are in flight (one warp per group keeps the
+      //       expansion off the MMA's critical loop; the cooperative 4-warp form of kBT = 0
+      //       took ~850 clk per group there).  Lane l owns 16-byte chunk c = l & 3 of stage
+      //       rows (l >> 2) + 8 j, j < 16; row r is operand row r (TMEM lane r), swizzle phase
+      //       r & 7 = l >> 2. ----
+      const int uwi = warp - kUnpackWarp0;
+      const uint32_t rr = static_cast<uint32_t>(lane) >> 2, cc = static_cast<uint32_t>(lane) & 3u;
+      uint32_t m0f = 0x0F0F0F0Fu, x08 = 0x08080808u;
+      asm volatile("" : "+r"(m0f), "+r"(x08));
+      Ring<kKS> st;
+      Ring<kRS> u;
+      Ring<kRS> lag;                     // mdone slot of group g - kRW
+      Ring<kRW> uw;
+      int gu = 0;
+      griddep_wait();
+      for (int k = 0; k < n_items; ++k) {
+        const Item w = get_item<C>(p, sch, k);
+        for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), ++gu) {
+          const int nst = t < G4 ? 1 : 2;
+          if ((gu & 3) != uwi) {         // another warp's group: advance the rings only
+            for (int h = 0; h < nst; ++h) st.next();
+            if (gu >= kRW) lag.next();
+            continue;
+          }
+          if (gu >= kRW) {               // MMAs of group g - kRW finished with this slot
+            wait_off(&sm.mdone[lag.i], lag.ph);
+            lag.next();
+          }
+          if (lane == 0) TRACE(2, gu);
+          uint8_t* dst = sm.w[uw.i];
+          if (t < G4) {
+            wait_off(&sm.full[st.i], st.ph);
+            const uint8_t* src = sm.stage[st.i] + rr * 64 + cc * 16;
+#pragma unroll
+            for (int j0 = 0; j0 < 16; j0 += 4) {
+              uint4 v[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                v[j] = *reinterpret_cast<const uint4*>(src + (j0 + j) * 8 * 64);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint8_t* d = dst + (rr + 8 * (j0 + j)) * 128;
+                *reinterpret_cast<uint4*>(d + (((2 * cc) ^ rr) << 4)) =
+                    make_uint4(lop_and_xor(v[j].x, m0f, x08), lop_and_xor(v[j].y, m0f, x08),
+                               lop_and_xor(v[j].z, m0f, x08), lop_and_xor(v[j].w, m0f, x08));
+                *reinterpret_cast<uint4*>(d + (((2 * cc + 1) ^ rr) << 4)) = make_uint4(
+                    lop_and_xor(v[j].x >> 4, m0f, x08), lop_and_xor(v[j].y >> 4, m0f, x08),
+                    lop_and_xor(v[j].z >> 4, m0f, x08), lop_and_xor(v[j].w >> 4, m0f, x08));
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[st.i]);
+            st.next();
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              wait_off(&sm.full[st.i], st.ph);
+              const uint8_t* src = sm.stage[st.i] + rr * 64 + cc * 16;
+#pragma unroll
+              for (int j0 = 0; j0 < 16; j0 += 4) {
+                uint4 v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  v[j] = *reinterpret_cast<const uint4*>(src + (j0 + j) * 8 * 64);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  *reinterpret_cast<uint4*>(dst + (rr + 8 * (j0 + j)) * 128 +
+                                            (((4 * h + cc) ^ rr) << 4)) = v[j];
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&sm.empty[st.i]);
+              st.next();
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) TRACE(4, gu);
+          if (lane == 0) mbar_arrive(&sm.go[u.i]);
+        }
+      }
+    } else {
     // ===================== weight expansion -> E4M3 offset-binary / int8, SW128 =============
     // 128 threads: thread ut owns 16-byte chunk c = ut & 3 of the 64-byte stage rows
-    // r0 + 32k, k < 8 (r0 = ut >> 2).  Weight row r of the tile goes to operand row
-    // j(r) = 128 (r / 128) + 8 ((r % 32) / 2) + 2 ((r / 32) % 4) + r % 2, so that TMEM column j
-    // holds output channel r and a 16x256b-loading epilogue thread (columns 8k + 2 (lane % 4)
-    // + {0,1}) owns 32 consecutive output channels (contiguous scales and stores).  The
-    // swizzle phase of row j is (2 k + r0 % 2) & 7 (k < 4): the two rows a quarter-warp writes have
-    // phases of opposite parity, so the stores are bank-conflict-free.
+    // r0 + 32k, k < TN / 32 (r0 = ut >> 2).  Weight row r of the tile is operand row r: TMEM
+    // column r (kBT = 0, B operand) or TMEM lane r (swap-AB, A operand) holds output channel
+    // n0 + r.  The SW128 swizzle phase of row r is r0 & 7.
+    constexpr int kRowsPT = C::TN / 32;
     const int ut = threadIdx.x - kUnpackWarp0 * 32;
     const uint32_t r0 = static_cast<uint32_t>(ut) >> 2, c = static_cast<uint32_t>(ut) & 3u;
     const uint32_t jb = r0;              // operand row of k = 0
@@ -427,7 +564,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     int gu = 0;
     griddep_wait();
     for (int k = 0; k < n_items; ++k) {
-      const Item w = get_item(p, sch, k);
+      const Item w = get_item<C>(p, sch, k);
       for (int t = w.t0; t < w.t1; ++t, u.next(), uw.next(), ++gu) {
         if (gu >= kRW) {                 // MMAs of group g - kRW finished with this slot
           wait_off(&sm.mdone[lag.i], lag.ph);
@@ -440,13 +577,13 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           const uint8_t* src = sm.stage[st.i] + r0 * 64 + c * 16;
           // all 8 shared-memory loads first: their latency grows several-fold while the tensor
           // core streams operands, so it is paid once per group
-          uint4 v[8];
+          uint4 v[kRowsPT];
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < kRowsPT; ++j)
             if constexpr ((ATOM_PROBE_MODE & 1) == 0)
               v[j] = *reinterpret_cast<const uint4*>(src + j * 32 * 64);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < kRowsPT; ++j) {
             if constexpr ((ATOM_PROBE_MODE & 1) != 0) break;
             const uint32_t row = jb + 32 * j, ph = r0 & 7;
             uint8_t* d = dst + row * 128;
@@ -467,11 +604,12 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           for (int h = 0; h < 2; ++h) {
             wait_off(&sm.full[st.i], st.ph);
             const uint8_t* src = sm.stage[st.i] + r0 * 64 + c * 16;
-            uint4 v[8];
+            uint4 v[kRowsPT];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = *reinterpret_cast<const uint4*>(src + j * 32 * 64);
+            for (int j = 0; j < kRowsPT; ++j)
+              v[j] = *reinterpret_cast<const uint4*>(src + j * 32 * 64);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < kRowsPT; ++j) {
               const uint32_t row = jb + 32 * j, ph = r0 & 7;
               *reinterpret_cast<uint4*>(dst + row * 128 + (((4 * h + c) ^ ph) << 4)) = v[j];
             }
@@ -486,9 +624,123 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (lane == 0) mbar_arrive(&sm.go[u.i]);
       }
     }
+    }   // kBT = 0 weight expansion
   } else {
     // ===================== epilogue warps =====================
     setmaxnreg_inc<kRegsHigh>();
+    if constexpr (C::kSwap) {
+      // ---- swap-AB (small M): thread = TMEM lane = output channel n0 + 32 q + lane; the two
+      //      warps of a lane quarter drain token columns [h * kBT/2, (h + 1) * kBT/2).  Per
+      //      output and group the same two fp32 operations as the kBT = 0 epilogue:
+      //      h = fma(P', alpha_m, beta_m), acc = fma(s_w[n], h, acc). ----
+      constexpr int NH = kBT / 2;
+      const int e = warp - kEpiWarp0;
+      const int q = warp & 3, hf = e >> 2;
+      const int nl = q * 32 + lane;
+      const int et = e * 32 + lane;
+      const uint32_t tq = tmem + (static_cast<uint32_t>(q * 32) << 16) + hf * NH;
+      const int kq = nl >> 3;   // position of channel nl in the w_sp order (include/atom.h)
+      const int spos = 32 * (kq >> 2) + 8 * ((nl & 7) >> 1) + 2 * (kq & 3) + (nl & 1);
+      griddep_wait();
+      if (lane == 0)
+        for (int bb = 0; bb < kRT; ++bb) mbar_arrive(&sm.go[bb % kRS]);
+      // token m0 + hf NH + i of group t sits at a_ab row t Mp + (m0 & ~31) + tb + 4 (i % 8) + i / 8
+      // (include/atom.h "a_ab"): tb = mb - rb + rb / 8, mb = m0 % 32 + hf NH, rb = mb % 32
+      auto tok_base = [&](int m0) {
+        const int mb = (m0 & 31) + hf * NH, rb = mb & 31;
+        return mb - rb + (rb >> 3);
+      };
+      constexpr auto ab_off = [](int i) { return 4 * (i & 7) + (i >> 3); };
+      Ring<kRS> u;
+      Ring<kRT> b;
+      int ge = 0;
+      for (int k = 0; k < n_items; ++k) {
+        const Item w = get_item<C>(p, sch, k);
+        const int tb = tok_base(w.m0);
+        float acc[NH];
+#pragma unroll
+        for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
+        for (int t = w.t0; t < w.t1; ++t, u.next(), b.next(), ++ge) {
+          mbar_wait_test(&sm.mdone[u.i], u.ph);
+          // the group's staged scales: go[u] (completed by the bulk copies) cannot advance
+          // before this warp's release below, so the probe returns at once and makes the
+          // async-proxy writes visible here
+          mbar_wait_test(&sm.go[u.i], u.ph);
+          if (e == 0 && lane == 0) TRACE(5, ge);
+          const float* sc = sm.sc[ge % C::RA];
+          const float sw_c = sc[spos];
+          const float2* abr = reinterpret_cast<const float2*>(sc + 128) + tb;
+          float2 ab_c[NH];
+#pragma unroll
+          for (int i = 0; i < NH; ++i) ab_c[i] = abr[ab_off(i)];
+          tc_fence_after();
+          uint32_t r[NH];
+          tmem_ld_32x32b<NH>(tq + b.i * C::TC, r);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          const uint32_t go_next = u.i + kRT >= kRS ? u.i + kRT - kRS : u.i + kRT;
+          if (lane == 0) mbar_arrive(&sm.go[go_next]);
+          if (e == 0 && lane == 0) TRACE(6, ge);
+          const bool int4 = t < G4;
+#pragma unroll
+          for (int i = 0; i < NH; ++i) {
+            const float pv = int4 ? __uint_as_float(r[i]) : __int2float_rn(static_cast<int>(r[i]));
+            if constexpr (kDebug) {
+              const int m = w.m0 + hf * NH + i, n = w.n0 + nl;
+              if (m < p.M) {
+                int pi;
+                if (int4) {   // P = P' * 2^18 - 8 ca, exact (see the kBT = 0 epilogue)
+                  const int ca = __double2int_rn(-static_cast<double>(ab_c[i].y) * 32768.0 /
+                                                 static_cast<double>(ab_c[i].x));
+                  pi = __float2int_rn(pv * 262144.0f) - 8 * ca;
+                } else {
+                  pi = static_cast<int>(r[i]);
+                }
+                p.debug[(static_cast<int64_t>(t) * p.M + m) * p.N + n] = pi;
+              }
+            }
+            acc[i] = __fmaf_rn(sw_c, __fmaf_rn(pv, ab_c[i].x, ab_c[i].y), acc[i]);
+          }
+          if (e == 0 && lane == 0) TRACE(7, ge);
+        }
+        // split tile: publish / reduce as in the kBT = 0 epilogue (thread-linear slot layout)
+        if (w.t1 < p.G || w.t0 > 0) {
+          if (w.t1 < p.G) {
+            float* slot = p.partials + static_cast<int64_t>(blockIdx.x) * kSlotFloats;
+#pragma unroll
+            for (int i = 0; i < NH; ++i) __stcg(slot + i * kEpiThreads + et, acc[i]);
+            __threadfence();
+            named_bar_sync(1, kEpiThreads);
+            if (e == 0 && lane == 0)
+              red_release_add(p.counters + cta_of(p, static_cast<int64_t>(w.tile + 1) * p.G - 1), 1);
+            continue;
+          }
+          const int first = cta_of(p, static_cast<int64_t>(w.tile) * p.G);
+          const int nseg = static_cast<int>(blockIdx.x) - first;
+          if (e == 0 && lane == 0) {
+            while (ld_acquire(p.counters + blockIdx.x) < nseg) __nanosleep(64);
+            p.counters[blockIdx.x] = 0;
+          }
+          named_bar_sync(1, kEpiThreads);
+          for (int i0 = first; i0 < static_cast<int>(blockIdx.x); ++i0) {
+            const float* slot = p.partials + static_cast<int64_t>(i0) * kSlotFloats;
+#pragma unroll
+            for (int i = 0; i < NH; ++i) acc[i] += __ldcg(slot + i * kEpiThreads + et);
+          }
+        }
+        const int n = w.n0 + nl;
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+          const int m = w.m0 + hf * NH + i;
+          if (m >= p.M) continue;
+          if (!p.c_f32)
+            static_cast<__half*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = __float2half_rn(acc[i]);
+          else
+            static_cast<float*>(p.c)[static_cast<int64_t>(m) * p.ldc + n] = acc[i];
+        }
+      }
+    } else {
     const int e = warp - kEpiWarp0;
     const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int half = e >> 2;             // column half
@@ -510,7 +762,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     float2 sw[16];
     float al[4], be[4];
     auto sw_base = [&](int t, int n0) {
-      return p.w_sp + static_cast<int64_t>(t) * p.N + n0 + ((n0 + kTileN <= p.N) ? cs_off : cs_ld);
+      return p.w_sp + static_cast<int64_t>(t) * p.N + n0 + ((n0 + C::TN <= p.N) ? cs_off : cs_ld);
     };
     auto load_sw = [&](const float* ws, int k0, int nk) {   // channel pairs k0 .. k0+nk (k0 % 4 == 0)
 #pragma unroll
@@ -533,7 +785,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
       a[2] = v[4]; bb[2] = v[5]; a[3] = v[6]; bb[3] = v[7];
     };
     if (n_items > 0) {
-      const Item w0 = get_item(p, sch, 0);
+      const Item w0 = get_item<C>(p, sch, 0);
       load_ab(w0.t0, w0.m0, al, be);
       load_sw(sw_base(w0.t0, w0.n0), 0, 16);
     }
@@ -541,12 +793,12 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
     Ring<kRT> b;
     int ge = 0;
     for (int k = 0; k < n_items; ++k) {
-      const Item w = get_item(p, sch, k);
+      const Item w = get_item<C>(p, sch, k);
       // first group of the next item (after the last group, "next" is the last group itself:
       // harmless reloads, no branches)
       int nt0 = w.t1 - 1, nn0 = w.n0, nm0 = w.m0;
       if (k + 1 < n_items) {
-        const Item wn = get_item(p, sch, k + 1);
+        const Item wn = get_item<C>(p, sch, k + 1);
         nt0 = wn.t0;
         nn0 = wn.n0;
         nm0 = wn.m0;
@@ -572,7 +824,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         if (e == 0 && lane == 0) TRACE(5, ge);
         if (lane == 0) TRACE(17 + e, ge);
         tc_fence_after();
-        const uint32_t taddr = tq + b.i * kTileN;
+        const uint32_t taddr = tq + b.i * C::TC;
         const uint32_t go_next = u.i + kRT >= kRS ? u.i + kRT - kRS : u.i + kRT;
         // loads j = 2 cb + hh: 16 lanes (half hh of the quarter) x kLdX chunks (block cb),
         // software-pipelined kLdAhead loads ahead
@@ -742,13 +994,18 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
         }
       }
     }
+    }   // kBT = 0 epilogue
   }
 
   tc_fence_before();
   __syncthreads();
+#ifdef ATOM_DEV_PROBES
+  if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceN)
+    p.trace[26 * kTraceN + blockIdx.x] = gtimer();
+#endif
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, kTmemCols);
+    tmem_dealloc(tmem, C::kTmemCols);
   }
 }
 
@@ -891,7 +1148,7 @@ static bool make_map_u8(CUtensorMap* map, const void* base, uint64_t cols, uint6
 }
 
 // cudaFuncSetAttribute once per (device, kernel instantiation).
-template <bool kDebug>
+template <int kBT, bool kDebug>
 static cudaError_t set_smem_attr(size_t smem) {
   constexpr int kMaxDev = 64;
   static std::once_flag once[kMaxDev];
@@ -901,7 +1158,7 @@ static cudaError_t set_smem_attr(size_t smem) {
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
   std::call_once(once[dev], [&]() {
-    err[dev] = cudaFuncSetAttribute(w4a4_gemm_kernel<kDebug>,
+    err[dev] = cudaFuncSetAttribute(w4a4_gemm_kernel<kBT, kDebug>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem));
   });
@@ -910,10 +1167,14 @@ static cudaError_t set_smem_attr(size_t smem) {
 
 // Tile plan: one persistent CTA per SM (or per unit, if fewer); whole tiles in round-robin waves
 // while at least two waves remain, then the rest as evenly divided (tile, group) units.
+// Small M (<= 64 tokens) takes the swap-AB tile of kBT = 16 / 32 / 64 tokens x 128 channels.
 GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms, bool split_free) {
   GemmPlan pl;
   const int64_t G = K / 128;
-  pl.num_tiles = ((N + kTileN - 1) / kTileN) * ((M + kTileM - 1) / kTileM);
+  pl.bt = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 0;
+  pl.tile_m = pl.bt ? pl.bt : 128;
+  pl.tile_n = pl.bt ? 128 : 256;
+  pl.num_tiles = ((N + pl.tile_n - 1) / pl.tile_n) * ((M + pl.tile_m - 1) / pl.tile_m);
   if (split_free) {   // every tile by one CTA over all of K: the same fp32 chain for any shape
     pl.grid = static_cast<int>(pl.num_tiles < num_sms ? pl.num_tiles : num_sms);
     pl.dp_waves = static_cast<int>((pl.num_tiles + pl.grid - 1) / pl.grid);
@@ -939,7 +1200,7 @@ GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms, bool split
   return pl;
 }
 
-int64_t ab_rows(int64_t M) { return ((M + kTileM - 1) / kTileM) * kTileM; }
+int64_t ab_rows(int64_t M) { return ((M + 127) / 128) * 128; }
 
 size_t expand_bytes(int64_t M, int64_t K) {
   const size_t f8 = ((static_cast<size_t>(M) * K + 255) / 256) * 256;
@@ -972,9 +1233,10 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   const void* w4 = kp ? static_cast<const void*>(a.w_q4) : static_cast<const void*>(a.w_q8);
   const void* w8 = k_o ? static_cast<const void*>(a.w_q8) : static_cast<const void*>(a.w_q4);
   const uint64_t c4 = kp ? kp : 128, c8 = k_o ? 128 : kp;
-  if (!make_map_u8(&m_wq4, w4, c4, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_map_u8(&m_wq8, w8, c8, N, 64, kTileN, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_map_u8(&m_af8, a.a_f8, K, M, 128, kTileM, CU_TENSOR_MAP_SWIZZLE_128B))
+  const uint32_t tn = static_cast<uint32_t>(plan.tile_n), tt = static_cast<uint32_t>(plan.tile_m);
+  if (!make_map_u8(&m_wq4, w4, c4, N, 64, tn, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map_u8(&m_wq8, w8, c8, N, 64, tn, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map_u8(&m_af8, a.a_f8, K, M, 128, tt, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
 
   GemmParams p;
@@ -989,7 +1251,7 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   p.G = K / 128;
   p.G4 = (K - k_o) / 128;
   p.c_f32 = a.c_f32;
-  p.m_tiles = (M + kTileM - 1) / kTileM;
+  p.m_tiles = (M + plan.tile_m - 1) / plan.tile_m;
   p.num_tiles = static_cast<int>(plan.num_tiles);
   p.dp_waves = plan.dp_waves;
   p.sk_base = static_cast<int64_t>(plan.dp_waves) * plan.grid * p.G;
@@ -1000,7 +1262,7 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
     p.counters = static_cast<int*>(workspace);
     p.partials = reinterpret_cast<float*>(static_cast<char*>(workspace) + plan.counter_bytes);
   }
-  const size_t smem = sizeof(GemmSmem) + 1024;
+
 #ifdef ATOM_DEV_PROBES
   static long long* trace = nullptr;
   static const bool want_trace = std::getenv("ATOM_GEMM_TRACE") != nullptr;
@@ -1009,16 +1271,24 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
   p.trace = want_trace ? trace : nullptr;
   if (want_trace) cudaMemsetAsync(trace, 0, kTraceBytes, stream);
 #endif
-  cudaError_t e;
-  if (p.debug) {
-    if ((e = set_smem_attr<true>(smem)) != cudaSuccess) return e;
-    e = launch_pdl(w4a4_gemm_kernel<true>, dim3(plan.grid), dim3(kThreads), smem, stream, m_wq4,
-                   m_wq8, m_af8, p);
-  } else {
-    if ((e = set_smem_attr<false>(smem)) != cudaSuccess) return e;
-    e = launch_pdl(w4a4_gemm_kernel<false>, dim3(plan.grid), dim3(kThreads), smem, stream, m_wq4,
-                   m_wq8, m_af8, p);
-  }
+  auto go = [&](auto bt_tag, auto dbg_tag) {
+    constexpr int kBT = decltype(bt_tag)::value;
+    constexpr bool kDbg = decltype(dbg_tag)::value;
+    const size_t smem = sizeof(GemmSmem<TileCfg<kBT>>) + 1024;
+    cudaError_t err = set_smem_attr<kBT, kDbg>(smem);
+    if (err != cudaSuccess) return err;
+    return launch_pdl(w4a4_gemm_kernel<kBT, kDbg>, dim3(plan.grid), dim3(kThreads), smem, stream,
+                      m_wq4, m_wq8, m_af8, p);
+  };
+  auto go_bt = [&](auto dbg_tag) {
+    switch (plan.bt) {
+      case 16: return go(std::integral_constant<int, 16>{}, dbg_tag);
+      case 32: return go(std::integral_constant<int, 32>{}, dbg_tag);
+      case 64: return go(std::integral_constant<int, 64>{}, dbg_tag);
+      default: return go(std::integral_constant<int, 0>{}, dbg_tag);
+    }
+  };
+  const cudaError_t e = p.debug ? go_bt(std::true_type{}) : go_bt(std::false_type{});
   if (e != cudaSuccess) return e;
   ++*launches;
 #ifdef ATOM_DEV_PROBES
@@ -1028,10 +1298,25 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
     std::fprintf(stderr, "plan grid=%d dp_waves=%d sk_units=%lld\n", plan.grid, plan.dp_waves,
                  static_cast<long long>(plan.sk_units));
     std::fprintf(stderr, "g  W_tma A_tma unp_start unp_done mma_issue mma_done epi_start epi_release epi_end\n");
+    {
+      long long s0 = -1, s1 = 0, e0 = -1, e1 = 0;
+      for (int b = 0; b < plan.grid && b < kTraceN; ++b) {
+        const long long a = h[25 * kTraceN + b], z = h[26 * kTraceN + b];
+        if (s0 < 0 || a < s0) s0 = a;
+        if (a > s1) s1 = a;
+        if (e0 < 0 || z < e0) e0 = z;
+        if (z > e1) e1 = z;
+      }
+      std::fprintf(stderr, "CTA globaltimer ns: start spread %lld, end first %lld last %lld\n",
+                   s1 - s0, e0 - s0, e1 - s0);
+      for (int b = 0; b < plan.grid && b < kTraceN; b += 8)
+        std::fprintf(stderr, "  cta %3d start %6lld end %6lld\n", b, h[25 * kTraceN + b] - s0,
+                     h[26 * kTraceN + b] - s0);
+    }
     const long long t0 = h[3 * kTraceN];
     for (int g = 0; g < kTraceN; ++g) {
       if (h[3 * kTraceN + g] == 0) break;
-      if (g > 40 && g % 20 != 0) continue;
+      if (g > 40 && g % 4 != 0) continue;
       std::fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld |", g,
                    h[g] - t0, h[kTraceN + g] - t0, h[2 * kTraceN + g] - t0,
                    h[4 * kTraceN + g] - t0, h[3 * kTraceN + g] - t0, h[8 * kTraceN + g] - t0,

@@ -59,13 +59,15 @@ struct GemmPlan {
   int dp_waves = 0;             // whole-tile round-robin waves
   int64_t sk_units = 0;         // (tile, group) units divided evenly after the waves
   int64_t num_tiles = 0;
+  int bt = 0;                   // 0: 128-token x 256-channel tiles; 16/32/64: swap-AB small-M tiles
+  int tile_m = 128, tile_n = 256;   // tokens / channels per tile
   size_t counter_bytes = 0;
   size_t workspace_bytes = 0;   // 0 when no tile is split between CTAs
 };
 
 GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms, bool split_free = false);
 
-// Rows of a_ab per group: M rounded up to the 128-token tile.
+// Rows of a_ab per group: M rounded up to a multiple of 128.
 int64_t ab_rows(int64_t M);
 
 // Bytes of workspace the canonical entry needs for a_f8 + a_ab (after the GEMM's own part).

@@ -306,6 +306,42 @@ def test_gemm_partials_bitexact(atom, M, N, K, k_o, canonical):
     assert __import__("torch").equal(c, c2)
 
 
+@pytest.mark.parametrize("M,N,K,k_o", [
+    (1, 384, 1024, 128),     # swap-AB kBT = 16
+    (16, 256, 640, 128),
+    (17, 640, 1152, 0),      # kBT = 32, pure INT4
+    (32, 11008, 512, 128),   # kBT = 32, many channel tiles, stream-K segments
+    (33, 384, 4096, 128),    # kBT = 64
+    (64, 4096, 1408, 128),   # kBT = 64, ragged stream-K split points
+])
+def test_gemm_small_m_swap_partials_bitexact(atom, M, N, K, k_o):
+    """The small-M swap-AB tiles (weights on the MMA M side, kBT = 16/32/64 tokens): every exact
+    group partial, the output within tolerance, and the production kernel's bits equal to the
+    debug kernel's."""
+    X, W, perm = synth.problem(M, N, K, seed=M * 11 + K, k_outlier=k_o)
+    aq, wq, c, dbg = run_gemm(atom, X, W, perm, K, k_o, debug=True)
+    ref = oracle.quantized_linear(X, perm, W, K, k_o)
+    np.testing.assert_array_equal(host(dbg), ref["partials"])
+    assert_close_tol(host(c.float()), ref["c"], "C")
+    assert __import__("torch").equal(c, atom.w4a4_gemm(aq, wq))
+
+
+def test_gemm_split_free_same_chain_every_tile(atom):
+    """Split-free outputs are one fp32 chain per output (groups ascending, h = fma(P', alpha,
+    beta), acc = fma(s_w, h, acc)) in both epilogues: the same token rows computed inside a
+    16-, 32-, 64-token swap-AB tile and a 128-token tile give identical bits."""
+    import torch
+    N, K = 1024, 2048
+    X, W, perm = synth.problem(200, N, K, seed=5)
+    pd = dev(perm)
+    wq = atom.quantize_weights(dev(W), pd)
+    full = atom.w4a4_gemm(atom.reorder_quantize(dev(X), pd), wq, split_free=True)
+    for m in (5, 16, 30, 64):
+        sub = atom.w4a4_gemm(atom.reorder_quantize(dev(X[:m]), pd), wq, split_free=True)
+        torch.cuda.synchronize()
+        assert torch.equal(sub, full[:m]), m
+
+
 def test_gemm_canonical_equals_operand_form(atom):
     """atom_w4a4_gemm on the packed codes (expanded on the device) and atom_w4a4_gemm_f8 on the
     quantizer's operand form give identical bits; so does the oracle's packed activation bytes
@@ -338,7 +374,7 @@ def test_gemm_output_config1_family(atom, M):
     assert_close_tol(host(c.float()), ref["c"], f"M={M}")
 
 
-@pytest.mark.parametrize("M", [16, 40, 100, 300, 1024])
+@pytest.mark.parametrize("M", [1, 16, 33, 40, 64, 100, 300, 1024])
 def test_gemm_unit_scale_exact_integer(atom, M):
     """P3 on the GPU, production kernel (no debug stores), fp32 output: clip 1 and integer-valued
     groups -> C is the exact integer GEMM (every split / tile path must be exact)."""

@@ -15,7 +15,8 @@ import synth  # noqa: E402
 atom.LIB_PATH = ROOT / "ab" / "libatom_probe.so"
 cfgs = {"cfg5": (1024, 28672, 8192), "cfg2": (256, 4096, 4096), "cfg4": (512, 13824, 5120),
         "cfg3u": (1024, 11008, 4096)}
-M, N, K = cfgs[sys.argv[1] if len(sys.argv) > 1 else "cfg5"]
+arg = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
+M, N, K = cfgs[arg] if arg in cfgs else tuple(int(v) for v in arg.split(","))
 X = torch.from_numpy(synth.activations(M, K, 0)).cuda()
 perm = torch.from_numpy(synth.perm_for(K, 0)).cuda()
 W = torch.from_numpy(synth.weights(N, K, 0)).cuda()
