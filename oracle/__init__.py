@@ -19,6 +19,7 @@ import numpy as np
 GROUP = 128
 _HERE = Path(__file__).resolve().parent
 _SRC = _HERE / "atom_oracle.c"
+_SRCS = [_SRC, _HERE / "mx_oracle.c"]   # mx_oracle.c: Atom (FP) on the MX format (NEXT-2)
 _LIB = _HERE / "liboracle.so"
 
 ORC_OK, ORC_ERR_NULL, ORC_ERR_SHAPE, ORC_ERR_ARG, ORC_ERR_OVERFLOW = 0, 1, 2, 4, 8
@@ -26,11 +27,11 @@ ORC_OK, ORC_ERR_NULL, ORC_ERR_SHAPE, ORC_ERR_ARG, ORC_ERR_OVERFLOW = 0, 1, 2, 4,
 
 def build(force: bool = False) -> Path:
     """Compile the oracle with pinned IEEE semantics (no contraction, no fast-math)."""
-    if force or not _LIB.exists() or _LIB.stat().st_mtime < _SRC.stat().st_mtime:
+    if force or not _LIB.exists() or any(_LIB.stat().st_mtime < s.stat().st_mtime for s in _SRCS):
         tmp = _LIB.with_suffix(f".so.tmp{os.getpid()}")
         subprocess.run(
             ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
-             "-fPIC", "-shared", "-o", str(tmp), str(_SRC), "-lm"],
+             "-fPIC", "-shared", "-o", str(tmp), *[str(s) for s in _SRCS], "-lm"],
             check=True)
         os.replace(tmp, _LIB)
     return _LIB
@@ -55,6 +56,19 @@ def lib():
         L.oracle_silu_mul_rows.restype = ctypes.c_int
         L.oracle_expf_pinned.argtypes = [ctypes.c_float]
         L.oracle_expf_pinned.restype = ctypes.c_float
+        u8p = P
+        L.oracle_mx_quantize_rows.argtypes = [P, i64, i64, P, i64, i32, u8p, u8p, u8p]
+        L.oracle_mx_quantize_rows.restype = ctypes.c_int
+        L.oracle_mx_output_rows.argtypes = [P, P, P, P, P, P, i64, i64, i64, i32, P, i64, P]
+        L.oracle_mx_output_rows.restype = ctypes.c_int
+        for f in (L.oracle_e2m1_value, L.oracle_e4m3_value):
+            f.argtypes = [ctypes.c_int]
+            f.restype = ctypes.c_double
+        for f in (L.oracle_e2m1_code, L.oracle_e4m3_code):
+            f.argtypes = [ctypes.c_float]
+            f.restype = ctypes.c_int
+        L.oracle_mx_scale_byte.argtypes = [ctypes.c_float, ctypes.c_int]
+        L.oracle_mx_scale_byte.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_max_threads.restype = ctypes.c_int
         for f in (L.oracle_quantize_rows, L.oracle_group_partials, L.oracle_gemm_output,
@@ -200,3 +214,66 @@ def quantized_linear(x, perm, w, K: int, k_outlier: int = 128, clip_a: float = 0
     C = gemm_output(P, a_s, w_s)
     return dict(a_q4=a_q4, a_q8=a_q8, a_scales=a_s, w_q4=w_q4, w_q8=w_q8, w_scales=w_s,
                 partials=P, c=C)
+
+
+# ---------------------------------------------------------------------------------------------
+# Atom (FP) on the MX format (NEXT-2, mx_oracle.c): readings G21-G24 of DESIGN.md
+# ---------------------------------------------------------------------------------------------
+MX_BLOCK = 32
+
+
+def e2m1_value(code: int) -> float:
+    return float(lib().oracle_e2m1_value(int(code)))
+
+
+def e4m3_value(code: int) -> float:
+    return float(lib().oracle_e4m3_value(int(code)))
+
+
+def e2m1_code(x: float) -> int:
+    return int(lib().oracle_e2m1_code(ctypes.c_float(x)))
+
+
+def e4m3_code(x: float) -> int:
+    return int(lib().oracle_e4m3_code(ctypes.c_float(x)))
+
+
+def mx_scale_byte(amax: float, emax_elem: int) -> int:
+    return int(lib().oracle_mx_scale_byte(ctypes.c_float(amax), int(emax_elem)))
+
+
+def mx_quantize_rows(x, perm, K: int, k_outlier: int = 128):
+    """Reorder + MX quantization of every row (mx_oracle.c).  Returns (fp4 uint8
+    [rows][(K-k_o)/2] packed E2M1, fp8 uint8 [rows][k_o] E4M3 or None, sexp uint8 [rows][K/32]
+    UE8M0 block-scale bytes)."""
+    x32 = np.ascontiguousarray(np.asarray(x).astype(np.float32))
+    rows, ldx = x32.shape
+    perm = np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    assert perm.shape == (K,)
+    f4 = np.zeros((rows, (K - k_outlier) // 2), dtype=np.uint8)
+    f8 = np.zeros((rows, k_outlier), dtype=np.uint8) if k_outlier else None
+    se = np.zeros((rows, K // MX_BLOCK), dtype=np.uint8)
+    st = lib().oracle_mx_quantize_rows(_ptr(x32), rows, ldx, _ptr(perm), K, k_outlier, _ptr(f4),
+                                       _ptr(f8), _ptr(se))
+    _check(st, "oracle_mx_quantize_rows")
+    return f4, f8, se
+
+
+def mx_output_rows(a, w, M: int, N: int, K: int, k_outlier: int, rows=None):
+    """G24 for the selected token rows (default: all): sum_j deq(a[m][j]) deq(w[n][j]) in
+    float64.  ``a`` / ``w`` are mx_quantize_rows results."""
+    rows = np.arange(M) if rows is None else rows
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    c = np.zeros((rows.size, N), dtype=np.float64)
+    st = lib().oracle_mx_output_rows(_ptr(_c(a[0])), _ptr(_c(a[1])), _ptr(_c(a[2])),
+                                     _ptr(_c(w[0])), _ptr(_c(w[1])), _ptr(_c(w[2])), M, N, K,
+                                     k_outlier, _ptr(rows), rows.size, _ptr(c))
+    _check(st, "oracle_mx_output_rows")
+    return c
+
+
+def mx_quantized_linear(x, perm, w, K: int, k_outlier: int = 128):
+    """Atom (FP) on the CPU: MX-quantize W (offline) and X, then the double output."""
+    a = mx_quantize_rows(x, perm, K, k_outlier)
+    wq = mx_quantize_rows(w, perm, K, k_outlier)
+    return dict(a=a, w=wq, c=mx_output_rows(a, wq, x.shape[0], w.shape[0], K, k_outlier))
