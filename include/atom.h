@@ -78,7 +78,7 @@
 extern "C" {
 #endif
 
-#define ATOM_ABI_VERSION 3
+#define ATOM_ABI_VERSION 4
 #define ATOM_GROUP 128
 
 typedef enum {
@@ -237,6 +237,41 @@ size_t atom_w4a4_gemm_f8_workspace_size(int64_t M, int64_t N, int64_t K, int32_t
 /* Size of the leading counter region of every GEMM workspace on the CURRENT device (the part
  * that must be zero before first use; 0 when the device is not an sm_100 GPU). */
 size_t atom_w4a4_gemm_counter_bytes(void);
+
+/* ------------------------------------------------------------------------------------------
+ * Atom (FP) on the MX format (NEXT-2).  The paper's FP4 variant: "quantizing both weights and
+ * activations into FP4" with "group quantization with the MX format ... supported by NVIDIA
+ * Blackwell GPUs" (Section 6; Table 5).  Same reorder and outlier split
+ * as above; readings G21-G24 of DESIGN.md fix the format:
+ *   fp4   uint8 [rows][(K - k_outlier)/2]  MXFP4 elements, E2M1 nibbles (sign, 2-bit exponent
+ *         with bias 1, 1 mantissa bit), low nibble = even reordered channel
+ *   fp8   uint8 [rows][k_outlier]          MXFP8 elements of the outlier channels, E4M3
+ *   sf    uint8 [rows][ldsf]               UE8M0 block scales: byte b of a row = 127 + the
+ *         shared exponent of reordered channels [32b, 32b + 32) (b < K/32; the last k_o/32 are
+ *         the outlier blocks); ldsf >= K/32 and a multiple of 16; bytes past K/32 are not written
+ *   Conversion (OCP MX v1.0 6.3): shared_exp = floor(log2(amax of the block)) - emax_elem
+ *   (2 for E2M1, 8 for E4M3), byte 0 for an all-zero block; element = x / 2^shared_exp rounded
+ *   to nearest-even in the element format, saturating to +-6 / +-448, the sign of x kept on
+ *   zero.  Bit-exact with oracle/mx_oracle.c.
+ * ------------------------------------------------------------------------------------------ */
+
+/* Reorder + MX-quantize `rows` fp16 rows (x[r * ldx + perm[j]] is reordered channel j).  Used
+ * online for activations and offline for weights (rows = N).  K % 128 == 0, k_outlier in {0, 128},
+ * ldx % 8 == 0, ldx >= max(perm) + 1, 2 * ldx <= 227 KiB.  fp4 NULL iff K == k_outlier, fp8 NULL
+ * iff k_outlier == 0. */
+atom_status_t atom_mx_reorder_quantize(const void* x_f16, int64_t rows, int64_t ldx,
+                                       const int32_t* perm, int64_t K, int32_t k_outlier,
+                                       uint8_t* fp4, uint8_t* fp8, uint8_t* sf, int64_t ldsf,
+                                       void* stream);
+
+/* C[m*ldc + n] = fp16( sum_j deq(a[m][j]) * deq(w[n][j]) ), deq = element * 2^shared_exp, on
+ * tcgen05 block-scaled MMAs (kind::mxf4 for the FP4 channels, kind::mxf8f6f4 for the outliers)
+ * with fp32 accumulation.  Activations [M][..] and weights [N][..] in the formats above (weights
+ * quantized with the same perm).  N % 128 == 0, ldc >= N, ldc % 8 == 0, lda_sf / ldw_sf as ldsf. */
+atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uint8_t* a_sf,
+                           int64_t lda_sf, const uint8_t* w_fp4, const uint8_t* w_fp8,
+                           const uint8_t* w_sf, int64_t ldw_sf, int64_t M, int64_t N, int64_t K,
+                           int32_t k_outlier, void* c_f16, int64_t ldc, void* stream);
 
 /* Test helper: on `stream`, sets *ok_flag (device int32) to 1 iff perm[0..K) is a bijection of
  * [0,K) (ldx == K) or an injection into [0,ldx).  scratch: device int32 [ldx], clobbered. */

@@ -23,6 +23,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #define MX_OK 0
@@ -121,15 +122,18 @@ int oracle_mx_quantize_rows(const float* x, int64_t rows, int64_t ldx, const int
   return MX_OK;
 }
 
-/* Dequantized reordered element j of a row. */
-static double mx_element(const uint8_t* q4row, const uint8_t* q8row, const uint8_t* srow,
-                         int64_t K4, int64_t j) {
-  const double X = ldexp(1.0, (int)srow[j / MX_BLOCK] - 127);
-  if (j < K4) {
-    const uint8_t byte = q4row[j / 2];
-    return X * oracle_e2m1_value((j & 1) ? (byte >> 4) : (byte & 15));
+/* Dequantized reordered row: out[j] = element j * 2^(scale byte of block j/32 - 127). */
+static void mx_dequant_row(const uint8_t* q4row, const uint8_t* q8row, const uint8_t* srow,
+                           int64_t K, int64_t K4, double* out) {
+  for (int64_t j = 0; j < K; ++j) {
+    const double X = ldexp(1.0, (int)srow[j / MX_BLOCK] - 127);
+    if (j < K4) {
+      const uint8_t byte = q4row[j / 2];
+      out[j] = X * oracle_e2m1_value((j & 1) ? (byte >> 4) : (byte & 15));
+    } else {
+      out[j] = X * oracle_e4m3_value(q8row[j - K4]);
+    }
   }
-  return X * oracle_e4m3_value(q8row[j - K4]);
 }
 
 /* G24: out[i][n] = sum_j deq(a[rows[i]][j]) deq(w[n][j]), j ascending, double. */
@@ -141,16 +145,26 @@ int oracle_mx_output_rows(const uint8_t* a4, const uint8_t* a8, const uint8_t* a
   const int64_t K4 = K - k_o, nb = K / MX_BLOCK;
   for (int64_t i = 0; i < nrows; ++i)
     if (rows[i] < 0 || rows[i] >= M) return MX_ERR_SHAPE;
-#pragma omp parallel for schedule(static)
+  double* ad = (double*)malloc(sizeof(double) * (size_t)(nrows * K));
+  if (!ad) return MX_ERR_SHAPE;
   for (int64_t i = 0; i < nrows; ++i) {
     const int64_t m = rows[i];
-    for (int64_t n = 0; n < N; ++n) {
-      double acc = 0.0;
-      for (int64_t j = 0; j < K; ++j)
-        acc += mx_element(a4 + m * (K4 / 2), a8 + m * k_o, asf + m * nb, K4, j) *
-               mx_element(w4 + n * (K4 / 2), w8 + n * k_o, wsf + n * nb, K4, j);
-      out[i * N + n] = acc;
-    }
+    mx_dequant_row(a4 + m * (K4 / 2), a8 + m * k_o, asf + m * nb, K, K4, ad + i * K);
   }
+#pragma omp parallel
+  {
+    double* wd = (double*)malloc(sizeof(double) * (size_t)K);
+#pragma omp for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+      mx_dequant_row(w4 + n * (K4 / 2), w8 + n * k_o, wsf + n * nb, K, K4, wd);
+      for (int64_t i = 0; i < nrows; ++i) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < K; ++j) acc += ad[i * K + j] * wd[j];
+        out[i * N + n] = acc;
+      }
+    }
+    free(wd);
+  }
+  free(ad);
   return MX_OK;
 }

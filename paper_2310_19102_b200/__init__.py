@@ -8,6 +8,7 @@ Names follow the ABI and the paper:
   reorder_quantize(x, perm)        a1  online activation reorder + dynamic quantize
   quantize_weights(w, perm)        a0  offline weight reorder + quantize
   w4a4_gemm(a, w)                  a2-a5 fused group GEMM with INT8 outliers
+  mx_quantize(x, perm) / mx_gemm(a, w)   NEXT-2 Atom (FP) on the MX format
 """
 from __future__ import annotations
 
@@ -32,6 +33,7 @@ ABI_SYMBOLS = ("atom_reorder_quantize", "atom_rmsnorm_reorder_quantize",
                "atom_w4a4_gemm", "atom_w4a4_gemm_f8",
                "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_f8_workspace_size",
                "atom_w4a4_gemm_counter_bytes",
+               "atom_mx_reorder_quantize", "atom_mx_gemm",
                "atom_validate_perm", "atom_status_string",
                "atom_abi_version", "atom_last_launch_count")
 
@@ -72,6 +74,10 @@ def _lib():
             f.argtypes = [i64, i64, i64, i32]
             f.restype = ctypes.c_size_t
         L.atom_w4a4_gemm_counter_bytes.restype = ctypes.c_size_t
+        L.atom_mx_reorder_quantize.argtypes = [P, i64, i64, P, i64, i32, P, P, P, i64, P]
+        L.atom_mx_reorder_quantize.restype = ctypes.c_int
+        L.atom_mx_gemm.argtypes = [P, P, P, i64, P, P, P, i64, i64, i64, i64, i32, P, i64, P]
+        L.atom_mx_gemm.restype = ctypes.c_int
         L.atom_validate_perm.argtypes = [P, i64, i64, P, P, P]
         L.atom_status_string.argtypes = [ctypes.c_int]
         L.atom_status_string.restype = ctypes.c_char_p
@@ -369,3 +375,67 @@ class QuantizedLinear:
         a = reorder_quantize(x, self.perm, k_outlier=self.k_outlier, clip_int4=self.clip_a,
                              clip_int8=self.clip_int8, stream=stream)
         return w4a4_gemm(a, self.w, out=out, stream=stream)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-2: Atom (FP) on the MX format (include/atom.h "Atom (FP)")
+# ---------------------------------------------------------------------------------------------
+MX_BLOCK = 32
+
+
+@dataclass
+class MxQuantized:
+    """MX-quantized operand: fp4 uint8 [rows][(K-k_o)/2] (E2M1 nibbles), fp8 uint8 [rows][k_o]
+    (E4M3, or None), sf uint8 [rows][ldsf] (UE8M0 block scales, bytes [0, K/32) used)."""
+    fp4: Optional[object]
+    fp8: Optional[object]
+    sf: object
+    K: int
+    k_outlier: int
+
+    @property
+    def rows(self) -> int:
+        return self.sf.shape[0]
+
+
+def mx_quantize(x, perm, K: Optional[int] = None, k_outlier: int = 128, out=None,
+                stream=None) -> MxQuantized:
+    """Reorder + MX-quantize fp16 rows (activations online, weights offline)."""
+    import torch
+    if x.dtype != torch.float16 or x.dim() != 2 or x.stride(1) != 1:
+        raise TypeError("x must be a 2-D fp16 tensor with contiguous rows")
+    rows, ldx = x.shape[0], x.stride(0)
+    K = perm.numel() if K is None else int(K)
+    if perm.dtype != torch.int32 or K > perm.numel():
+        raise ValueError("perm must be int32 with at least K entries")
+    ldsf = ((K // MX_BLOCK + 15) // 16) * 16
+    if out is None:
+        dev = x.device
+        fp4 = torch.empty((rows, (K - k_outlier) // 2), dtype=torch.uint8, device=dev) \
+            if K > k_outlier else None
+        fp8 = torch.empty((rows, k_outlier), dtype=torch.uint8, device=dev) if k_outlier else None
+        sf = torch.zeros((rows, ldsf), dtype=torch.uint8, device=dev)
+        out = MxQuantized(fp4, fp8, sf, K, k_outlier)
+    st = _lib().atom_mx_reorder_quantize(_ptr(x), rows, ldx, _ptr(perm), K, k_outlier,
+                                         _ptr(out.fp4), _ptr(out.fp8), _ptr(out.sf),
+                                         out.sf.stride(0), _stream(stream))
+    _check(st, "atom_mx_reorder_quantize")
+    return out
+
+
+def mx_gemm(a: MxQuantized, w: MxQuantized, out=None, stream=None):
+    """C[m][n] = fp16(sum_j deq(a[m][j]) deq(w[n][j])) on tcgen05 block-scaled MMAs."""
+    import torch
+    if a.K != w.K or a.k_outlier != w.k_outlier:
+        raise ValueError("activation and weight quantization disagree on K / k_outlier")
+    M, N = a.rows, w.rows
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float16, device=a.sf.device)
+    if out.dtype != torch.float16 or out.dim() != 2 or out.stride(1) != 1 or \
+            out.shape[0] < M or out.shape[1] < N:
+        raise ValueError("out must be an fp16 [M][>=N] tensor with contiguous rows")
+    st = _lib().atom_mx_gemm(_ptr(a.fp4), _ptr(a.fp8), _ptr(a.sf), a.sf.stride(0), _ptr(w.fp4),
+                             _ptr(w.fp8), _ptr(w.sf), w.sf.stride(0), M, N, a.K, a.k_outlier,
+                             _ptr(out), out.stride(0), _stream(stream))
+    _check(st, "atom_mx_gemm")
+    return out

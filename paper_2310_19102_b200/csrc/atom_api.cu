@@ -296,6 +296,78 @@ atom_status_t atom_w4a4_gemm(const uint8_t* a_q4, const int8_t* a_q8, const floa
   return ATOM_OK;
 }
 
+atom_status_t atom_mx_reorder_quantize(const void* x_f16, int64_t rows, int64_t ldx,
+                                       const int32_t* perm, int64_t K, int32_t k_outlier,
+                                       uint8_t* fp4, uint8_t* fp8, uint8_t* sf, int64_t ldsf,
+                                       void* stream) {
+  g_last_launches = 0;
+  if (rows < 0) return ATOM_ERR_SHAPE;
+  if (!(k_outlier == 0 || k_outlier == ATOM_GROUP)) return ATOM_ERR_ARG;
+  if (K <= 0 || K % ATOM_GROUP != 0 || K < k_outlier || K > (1LL << 30)) return ATOM_ERR_SHAPE;
+  if (rows > 0x7fffffffLL || ldx <= 0 || ldx % 8 != 0 || ldx * 2 > 227 * 1024)
+    return ATOM_ERR_SHAPE;
+  if (ldsf < K / 32 || ldsf % 16 != 0) return ATOM_ERR_SHAPE;
+  if (rows == 0) return ATOM_OK;
+  if (!x_f16 || !perm || !sf) return ATOM_ERR_NULL;
+  if ((K > k_outlier) != (fp4 != nullptr) || (k_outlier > 0) != (fp8 != nullptr))
+    return ATOM_ERR_NULL;
+  if (!aligned16(x_f16) || !aligned16(perm) || !aligned16(sf) || (fp4 && !aligned16(fp4)) ||
+      (fp8 && !aligned16(fp8)))
+    return ATOM_ERR_ALIGN;
+  DeviceInfo dev;
+  atom_status_t st = current_device(&dev);
+  if (st != ATOM_OK) return st;
+  if (atom::launch_mx_reorder_quantize(x_f16, rows, ldx, perm, K, k_outlier, fp4, fp8, sf, ldsf,
+                                       static_cast<cudaStream_t>(stream), dev.num_sms) !=
+      cudaSuccess)
+    return ATOM_ERR_CUDA;
+  g_last_launches = 1;
+  return ATOM_OK;
+}
+
+atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uint8_t* a_sf,
+                           int64_t lda_sf, const uint8_t* w_fp4, const uint8_t* w_fp8,
+                           const uint8_t* w_sf, int64_t ldw_sf, int64_t M, int64_t N, int64_t K,
+                           int32_t k_outlier, void* c_f16, int64_t ldc, void* stream) {
+  g_last_launches = 0;
+  if (M < 0 || N <= 0 || N % 128 != 0) return ATOM_ERR_SHAPE;
+  if (!(k_outlier == 0 || k_outlier == ATOM_GROUP)) return ATOM_ERR_ARG;
+  if (K <= 0 || K % ATOM_GROUP != 0 || K < k_outlier || K > (1LL << 30)) return ATOM_ERR_SHAPE;
+  if (M > 0x7fffffffLL || N > 0x7fffffffLL || ldc < N || ldc % 8 != 0) return ATOM_ERR_SHAPE;
+  if (lda_sf < K / 32 || lda_sf % 16 != 0 || ldw_sf < K / 32 || ldw_sf % 16 != 0)
+    return ATOM_ERR_SHAPE;
+  if (M == 0) return ATOM_OK;
+  const bool has4 = K > k_outlier, has8 = k_outlier > 0;
+  if (!a_sf || !w_sf || !c_f16 || has4 != (a_fp4 != nullptr) || has4 != (w_fp4 != nullptr) ||
+      has8 != (a_fp8 != nullptr) || has8 != (w_fp8 != nullptr))
+    return ATOM_ERR_NULL;
+  if (!aligned16(a_sf) || !aligned16(w_sf) || !aligned16(c_f16) || (a_fp4 && !aligned16(a_fp4)) ||
+      (w_fp4 && !aligned16(w_fp4)) || (a_fp8 && !aligned16(a_fp8)) || (w_fp8 && !aligned16(w_fp8)))
+    return ATOM_ERR_ALIGN;
+  DeviceInfo dev;
+  atom_status_t st = current_device(&dev);
+  if (st != ATOM_OK) return st;
+  atom::MxGemmArgs a;
+  a.a_fp4 = a_fp4;
+  a.a_fp8 = a_fp8;
+  a.a_sf = a_sf;
+  a.lda_sf = lda_sf;
+  a.w_fp4 = w_fp4;
+  a.w_fp8 = w_fp8;
+  a.w_sf = w_sf;
+  a.ldw_sf = ldw_sf;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.k_outlier = k_outlier;
+  a.c = c_f16;
+  a.ldc = ldc;
+  if (atom::launch_mx_gemm(a, static_cast<cudaStream_t>(stream), dev.num_sms) != cudaSuccess)
+    return ATOM_ERR_CUDA;
+  g_last_launches = 1;
+  return ATOM_OK;
+}
+
 atom_status_t atom_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
                                  int32_t* ok_flag, void* stream) {
   g_last_launches = 0;

@@ -85,4 +85,26 @@ cudaError_t launch_prepare_w_scales(const float* w_scales, int64_t G, int64_t N,
 cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspace_bytes,
                              cudaStream_t stream, int num_sms, int* launches);
 
+// NEXT-2, Atom (FP) on the MX format (mxfp.cu, include/atom.h "Atom (FP)")
+cudaError_t launch_mx_reorder_quantize(const void* x, int64_t rows, int64_t ldx,
+                                       const int32_t* perm, int64_t K, int32_t k_outlier,
+                                       uint8_t* fp4, uint8_t* fp8, uint8_t* sf, int64_t ldsf,
+                                       cudaStream_t stream, int num_sms);
+
+struct MxGemmArgs {
+  const uint8_t* a_fp4;
+  const uint8_t* a_fp8;
+  const uint8_t* a_sf;
+  int64_t lda_sf;
+  const uint8_t* w_fp4;
+  const uint8_t* w_fp8;
+  const uint8_t* w_sf;
+  int64_t ldw_sf;
+  int64_t M, N, K;
+  int32_t k_outlier;
+  void* c;
+  int64_t ldc;
+};
+cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms);
+
 }  // namespace atom
