@@ -448,6 +448,11 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
         swiglu_us = 1e3 * sum(a.elapsed_time(b) for a, b in es) / len(es)
         swiglu_bytes = quant_bytes(M, N) + M * N * 2        # a second fp16 input row
 
+    # ---------------- NEXT-2: Atom (FP) on the MX format, same workload (not the headline) ----------
+    mx = None
+    if not args.no_graph and not args.no_mx and P == 1:
+        mx = time_atom_fp(atom, xd, layer.perm, M, N, K, args, dev, flush_l2)
+
     # the box's INT8 tensor peak, measured in this run: cuBLAS int8 GEMM (torch._int_mm, 8192^3)
     int8_meas = None
     if rank == 0 and not args.no_peak:
@@ -524,12 +529,66 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
             "collective": {"us": c_avg * 1e3},
         },
         "gpu_launches": gpu_launches,
+        "atom_fp": None if mx is None else dict(mx, roofline={
+            "bound": "tensor", "achieved": ops / (mx["gemm_us"] * 1e-6) / 1e12,
+            "peak": 4.0 * peaks["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": ops / (mx["gemm_us"] * 1e-6) / 1e12 / (4.0 * peaks["bf16_tflops"]),
+            "kernel": "atom::mx_gemm_kernel",
+            "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} x 4 (fp4/bf16 nominal "
+                           f"ratio, 9 / 2.25 PFLOP/s)"}),
         "clocks": sampler.summary(),
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(M, N, K, target_s=args.cpu_seconds)
     print(json.dumps(line), flush=True)
+
+
+def time_atom_fp(atom, xd, perm, M, N, K, args, dev, flush_l2):
+    """NEXT-2: the same layer as Atom (FP) -- MXFP4 E2M1 blocks of 32 + MXFP8 E4M3 outliers
+    with UE8M0 scales on tcgen05 block-scaled MMAs.  Weights MX-quantized offline (untimed); the
+    step (activation quantize + GEMM) and each kernel alone timed as CUDA graphs, L2 flushed
+    before every replay."""
+    import torch
+    W = torch.from_numpy(synth.weights(N, K, args.seed)).to(dev)
+    wq = atom.mx_quantize(W, perm)
+    del W
+    aq = atom.mx_quantize(xd, perm)
+    c = atom.mx_gemm(aq, wq)
+    graphs = {}
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for name, fn in (("quant", lambda: atom.mx_quantize(xd, perm, out=aq, stream=side)),
+                         ("gemm", lambda: atom.mx_gemm(aq, wq, out=c, stream=side)),
+                         ("step", lambda: (atom.mx_quantize(xd, perm, out=aq, stream=side),
+                                           atom.mx_gemm(aq, wq, out=c, stream=side)))):
+            fn()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                fn()
+            graphs[name] = g
+    torch.cuda.current_stream().wait_stream(side)
+    out = {}
+    n = max(5, args.steps // 2)
+    for name, g in graphs.items():
+        for _ in range(3):
+            g.replay()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n)]
+        for i in range(n):
+            if not args.no_flush:
+                flush_l2()
+            ev[i][0].record()
+            g.replay()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        out[f"{name}_us"] = 1e3 * sum(a.elapsed_time(b) for a, b in ev) / n
+    ops = 2.0 * M * N * K
+    out["TOPS_step"] = ops / (out["step_us"] * 1e-6) / 1e12
+    out["TOPS_gemm"] = ops / (out["gemm_us"] * 1e-6) / 1e12
+    out["format"] = "MXFP4 E2M1 (blocks of 32) + 128 MXFP8 E4M3 outlier channels, UE8M0 scales"
+    out["gpu_launches_per_step"] = 2
+    return out
 
 
 def _spawn_ranks(args) -> int:
@@ -590,6 +649,7 @@ def main():
                     help="launch the step's kernels directly instead of replaying CUDA graphs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-peak", action="store_true", help="skip the in-run int8 peak measurement")
+    ap.add_argument("--no-mx", action="store_true", help="skip the NEXT-2 Atom (FP) MX timing")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--dry-run", action="store_true",
                     help="multi-rank plumbing only (gloo, no GPU work): prints the shard table")
