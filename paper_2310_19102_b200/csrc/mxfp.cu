@@ -157,27 +157,43 @@ constexpr int kMxThreads = 384;
 #ifndef ATOM_MX_TN
 #define ATOM_MX_TN 224
 #endif
-#ifndef ATOM_MX_KS
-#define ATOM_MX_KS 4
-#endif
-constexpr int kMxTM = 128, kMxTN = ATOM_MX_TN, kMxKS = ATOM_MX_KS;
+constexpr int kMxTN = ATOM_MX_TN;
 constexpr int kMxEpi0 = 4, kMxNumEpi = 8;
-constexpr uint32_t kMxSfaCol = 2 * kMxTN;           // 448: A scale columns (2 chunks x 4)
-constexpr uint32_t kMxSfbCol = kMxSfaCol + 8;       // 456: B scale columns (2 chunks x 2 x 4)
-static_assert(kMxSfaCol + 2 * 24 <= 512, "two scale-column sets");
 constexpr uint32_t kMxTmemCols = 512;
 
+// Token-tile configurations: kTM = 128 (two accumulator buffers: the epilogue of tile i overlaps
+// the MMAs of tile i + 1) or kTM = 256 (two 128-row MMA halves sharing the weight tile: 32% fewer
+// operand bytes into the SM per MMA, which bounds this kernel (an MMA-free variant of it runs at
+// 125 us at cfg5), one accumulator buffer).  The launcher picks per shape (waves x bytes).
+template <int kTM>
+struct MxCfg {
+  static constexpr int TM = kTM, TN = ATOM_MX_TN;
+  static constexpr int H = TM / 128;                  // 128-row MMA halves per tile
+  static constexpr int AB = H == 1 ? 2 : 1;           // accumulator buffers (TMEM: 512 columns)
+  static constexpr int KS = H == 1 ? 4 : 3;           // pipeline stages (shared memory)
+  static constexpr uint32_t AccCols = AB * H * TN;    // 448
+  static constexpr uint32_t SfaCol = AccCols;         // A scales: (half h, chunk c) at + 8h + 4c
+  static constexpr uint32_t SfbCol = SfaCol + 8 * H;  // B scales: (chunk c, block k) at + 8c + 4k
+  static constexpr uint32_t SfSet = 8 * H + 16;       // columns of one scale set
+  static constexpr int Imgs = 2 * H + 4;              // tcgen05.cp images per stage
+  static_assert(TM == 128 || TM == 256, "token tile");
+  static_assert(SfaCol + 2 * SfSet <= 512, "two scale-column sets");
+};
+
+template <class C>
 struct __align__(1024) MxSmem {
-  uint8_t a[kMxKS][kMxTM * 128];         // packed E2M1 (or E4M3) activation stage, SW128
-  uint8_t b[kMxKS][kMxTN * 128];         // weight stage, SW128
-  uint8_t sfa[kMxKS][kMxTM * 16];        // canonical scale bytes of the stage, [row][16 B]
-  uint8_t sfb[kMxKS][kMxTN * 16];
-  uint32_t img[kMxKS][6][128];           // tcgen05.cp images: A c0, A c1, B c0 k0, B c0 k1, B c1 k0, B c1 k1
-  uint64_t full[kMxKS], sfready[kMxKS], empty[kMxKS];
-  uint64_t tfull[2], tempty[2];
+  uint8_t a[C::KS][C::TM * 128];         // packed E2M1 (or E4M3) activation stage, SW128
+  uint8_t b[C::KS][C::TN * 128];         // weight stage, SW128
+  uint8_t sfa[C::KS][C::TM * 16];        // canonical scale bytes of the stage, [row][16 B]
+  uint8_t sfb[C::KS][C::TN * 16];
+  uint32_t img[C::KS][C::Imgs][128];     // tcgen05.cp images: A (h, c) at 2h + c, then
+                                         // B (c, k) at 2H + 2c + k
+  uint64_t full[C::KS], sfready[C::KS], empty[C::KS];
+  uint64_t tfull[C::AB], tempty[C::AB];
   uint32_t tmem_base;
 };
-static_assert(sizeof(MxSmem) + 1024 <= 232448, "shared memory");
+static_assert(sizeof(MxSmem<MxCfg<128>>) + 1024 <= 232448, "shared memory");
+static_assert(sizeof(MxSmem<MxCfg<256>>) + 1024 <= 232448, "shared memory");
 
 // Instruction descriptor, block-scaled kinds: F32 accumulate, K-major A/B, UE8M0 scales.
 __host__ __device__ constexpr uint32_t mx_idesc(uint32_t fmt, uint32_t m, uint32_t n,
@@ -233,14 +249,18 @@ struct MxParams {
   int m_tiles, num_tiles;
 };
 
+template <int kTM>
 __global__ void __launch_bounds__(kMxThreads, 1)
 mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant__ CUtensorMap tm_b4,
                const __grid_constant__ CUtensorMap tm_a8, const __grid_constant__ CUtensorMap tm_b8,
                const __grid_constant__ CUtensorMap tm_asf,
                const __grid_constant__ CUtensorMap tm_bsf, const MxParams p) {
   extern __shared__ uint8_t smem_raw[];
-  MxSmem& sm = *reinterpret_cast<MxSmem*>(smem_raw +
-                                          ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  using C = MxCfg<kTM>;
+  constexpr int kMxTM = C::TM, kMxKS = C::KS, kMxH = C::H, kMxAB = C::AB;
+  constexpr uint32_t kMxSfaCol = C::SfaCol, kMxSfbCol = C::SfbCol, kMxSfSet = C::SfSet;
+  MxSmem<C>& sm = *reinterpret_cast<MxSmem<C>*>(smem_raw +
+                                                ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMxKS; ++s) {
@@ -248,7 +268,7 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
       mbar_init(&sm.sfready[s], 1);
       mbar_init(&sm.empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kMxAB; ++b) {
       mbar_init(&sm.tfull[b], 1);
       mbar_init(&sm.tempty[b], kMxNumEpi);
     }
@@ -300,12 +320,12 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
       const uint64_t da0 = umma_desc_sw128(smem_u32(sm.a[0]));
       const uint64_t db0 = umma_desc_sw128(smem_u32(sm.b[0]));
       MxRing<kMxKS> st;
-      MxRing<2> tb;
+      MxRing<kMxAB> tb;
       uint32_t sfpar = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, tb.next()) {
         mbar_wait(&sm.tempty[tb.i], tb.ph ^ 1);        // the epilogue drained this buffer
         tc_fence_after();
-        const uint32_t d = tmem + tb.i * kMxTN;
+        const uint32_t d = tmem + tb.i * (kMxH * kMxTN);   // half h at + h kMxTN
         for (int s = 0; s < nst; ++s, st.next()) {
           mbar_wait(&sm.full[st.i], st.ph);
           mbar_wait(&sm.sfready[st.i], st.ph);
@@ -314,28 +334,35 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
           const int nch = fp8 ? 1 : (s + 1 == p.s4 ? p.ch_last : 2);
           // scale columns alternate between two sets by stage parity, so a copy never overwrites
           // scales the previous stage's MMAs may still read
-          const uint32_t sfa = tmem + kMxSfaCol + (sfpar ? 24u : 0u);
-          const uint32_t sfb = tmem + kMxSfbCol + (sfpar ? 24u : 0u);
+          const uint32_t sfa = tmem + kMxSfaCol + (sfpar ? kMxSfSet : 0u);
+          const uint32_t sfb = tmem + kMxSfbCol + (sfpar ? kMxSfSet : 0u);
           sfpar ^= 1u;
           for (int c = 0; c < nch; ++c) {
-            tmem_cp_32x128b_x4(sfa + 4 * c, smem_u32(sm.img[st.i][c]));
-            tmem_cp_32x128b_x4(sfb + 8 * c, smem_u32(sm.img[st.i][2 + 2 * c]));
-            tmem_cp_32x128b_x4(sfb + 8 * c + 4, smem_u32(sm.img[st.i][3 + 2 * c]));
+#pragma unroll
+            for (int h = 0; h < kMxH; ++h)
+              tmem_cp_32x128b_x4(sfa + 8 * h + 4 * c, smem_u32(sm.img[st.i][2 * h + c]));
+            tmem_cp_32x128b_x4(sfb + 8 * c, smem_u32(sm.img[st.i][2 * kMxH + 2 * c]));
+            tmem_cp_32x128b_x4(sfb + 8 * c + 4, smem_u32(sm.img[st.i][2 * kMxH + 2 * c + 1]));
           }
           const uint64_t da = da0 + st.i * (kMxTM * 128 / 16), db = db0 + st.i * (kMxTN * 128 / 16);
           if (!fp8) {
             // K = 64 per MMA (32 bytes of packed E2M1): chunk c = k / 2, scale bytes 2 (k % 2), +1
             for (int k = 0; k < 2 * nch; ++k) {
               const uint32_t c = k >> 1, id = (k & 1) * 2;
-              umma_mxf4(d, da + 2 * k, db + 2 * k, mx_idesc(kFmtE2M1, kMxTM, kMxTN, id),
-                        sfa + 4 * c, sfb + 8 * c, (s > 0 || k > 0));
+#pragma unroll
+              for (int h = 0; h < kMxH; ++h)
+                umma_mxf4(d + h * kMxTN, da + h * (128 * 128 / 16) + 2 * k, db + 2 * k,
+                          mx_idesc(kFmtE2M1, 128, kMxTN, id), sfa + 8 * h + 4 * c, sfb + 8 * c,
+                          (s > 0 || k > 0));
             }
           } else {
             // K = 32 per MMA (32 bytes of E4M3): scale byte k
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              umma_mxf8(d, da + 2 * k, db + 2 * k, mx_idesc(kFmtE4M3, kMxTM, kMxTN, k), sfa, sfb,
-                        (s > 0 || k > 0));
+#pragma unroll
+              for (int h = 0; h < kMxH; ++h)
+                umma_mxf8(d + h * kMxTN, da + h * (128 * 128 / 16) + 2 * k, db + 2 * k,
+                          mx_idesc(kFmtE4M3, 128, kMxTN, k), sfa + 8 * h, sfb, (s > 0 || k > 0));
           }
           umma_commit(&sm.empty[st.i]);
         }
@@ -353,21 +380,29 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
         const int nch = fp8 ? 1 : (s + 1 == p.s4 ? p.ch_last : 2);
         const int off = (fp8 ? p.sf_off8 : 8 * s) & 15;   // the stage's bytes in the 16-byte box
         for (int c = 0; c < nch; ++c) {
-          uint32_t wa[4], wb0[4], wb1[4];
           const int o = off + 4 * c;
+#pragma unroll
+          for (int h = 0; h < kMxH; ++h) {
+            uint32_t wa[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              wa[q] = *reinterpret_cast<const uint32_t*>(sm.sfa[st.i] +
+                                                         (128 * h + 32 * q + lane) * 16 + o);
+            reinterpret_cast<uint4*>(sm.img[st.i][2 * h + c])[lane] =
+                make_uint4(wa[0], wa[1], wa[2], wa[3]);
+          }
+          uint32_t wb0[4], wb1[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int r = 32 * q + lane;
-            wa[q] = *reinterpret_cast<const uint32_t*>(sm.sfa[st.i] + r * 16 + o);
             wb0[q] = *reinterpret_cast<const uint32_t*>(sm.sfb[st.i] + r * 16 + o);
             wb1[q] = r + 128 < kMxTN
                          ? *reinterpret_cast<const uint32_t*>(sm.sfb[st.i] + (r + 128) * 16 + o)
                          : 0u;
           }
-          reinterpret_cast<uint4*>(sm.img[st.i][c])[lane] = make_uint4(wa[0], wa[1], wa[2], wa[3]);
-          reinterpret_cast<uint4*>(sm.img[st.i][2 + 2 * c])[lane] =
+          reinterpret_cast<uint4*>(sm.img[st.i][2 * kMxH + 2 * c])[lane] =
               make_uint4(wb0[0], wb0[1], wb0[2], wb0[3]);
-          reinterpret_cast<uint4*>(sm.img[st.i][3 + 2 * c])[lane] =
+          reinterpret_cast<uint4*>(sm.img[st.i][2 * kMxH + 2 * c + 1])[lane] =
               make_uint4(wb1[0], wb1[1], wb1[2], wb1[3]);
         }
         fence_proxy_async_smem();
@@ -377,38 +412,47 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
     }
   } else if (warp >= kMxEpi0) {
     // ============ epilogue: TMEM fp32 -> fp16 C, once per tile ============
+    // kMxH = 2: warp e drains row half e / 4 (TMEM lane quarter e % 4), all kMxTN columns in
+    // two passes of 112; kMxH = 1: column half e / 4.
     const int e = warp - kMxEpi0, q = warp & 3, hf = e >> 2;
+    constexpr int kPasses = kMxH == 2 ? 2 : 1;
     griddep_wait();
-    MxRing<2> tb;
+    MxRing<kMxAB> tb;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, tb.next()) {
       const int m0 = (tile % p.m_tiles) * kMxTM, n0 = (tile / p.m_tiles) * kMxTN;
       mbar_wait(&sm.tfull[tb.i], tb.ph);
       tc_fence_after();
-      const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + tb.i * kMxTN + hf * 112;
-      uint32_t r[7][16];
+      const int row = (kMxH == 2 ? 128 * hf : 0) + q * 32 + lane;
+      const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) +
+                          tb.i * (kMxH * kMxTN) + (kMxH == 2 ? hf * kMxTN : hf * 112);
+      const int m = m0 + row;
+      __half* crow = static_cast<__half*>(p.c) + static_cast<int64_t>(m < p.M ? m : 0) * p.ldc;
+      for (int pass = 0; pass < kPasses; ++pass) {
+        uint32_t r[7][16];
 #pragma unroll
-      for (int cb = 0; cb < 7; ++cb) tmem_ld_32x32b<16>(ta + 16 * cb, r[cb]);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tempty[tb.i]);
-      const int m = m0 + q * 32 + lane;
-      if (m < p.M) {
-        __half* crow = static_cast<__half*>(p.c) + static_cast<int64_t>(m) * p.ldc;
+        for (int cb = 0; cb < 7; ++cb) tmem_ld_32x32b<16>(ta + 112 * pass + 16 * cb, r[cb]);
+        tmem_ld_wait();
+        if (pass + 1 == kPasses) {       // every column of this thread's rows is in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tempty[tb.i]);
+        }
+        if (m < p.M) {
 #pragma unroll
-        for (int cb = 0; cb < 7; ++cb) {
-          const int n = n0 + hf * 112 + 16 * cb;
-          if (n >= p.N) break;
-          uint32_t h[8];
+          for (int cb = 0; cb < 7; ++cb) {
+            const int n = n0 + (kMxH == 2 ? 0 : hf * 112) + 112 * pass + 16 * cb;
+            if (n >= p.N) break;
+            uint32_t h[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const __half2 v = __floats2half2_rn(__uint_as_float(r[cb][2 * i]),
-                                                __uint_as_float(r[cb][2 * i + 1]));
-            h[i] = *reinterpret_cast<const uint32_t*>(&v);
+            for (int i = 0; i < 8; ++i) {
+              const __half2 v = __floats2half2_rn(__uint_as_float(r[cb][2 * i]),
+                                                  __uint_as_float(r[cb][2 * i + 1]));
+              h[i] = *reinterpret_cast<const uint32_t*>(&v);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(crow + n);
+            dst[0] = make_uint4(h[0], h[1], h[2], h[3]);
+            dst[1] = make_uint4(h[4], h[5], h[6], h[7]);
           }
-          uint4* dst = reinterpret_cast<uint4*>(crow + n);
-          dst[0] = make_uint4(h[0], h[1], h[2], h[3]);
-          dst[1] = make_uint4(h[4], h[5], h[6], h[7]);
         }
       }
     }
@@ -457,6 +501,14 @@ cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms
   const int64_t K4 = a.K - a.k_outlier;
   const void* any = K4 ? static_cast<const void*>(a.a_fp4) : static_cast<const void*>(a.a_fp8);
   const void* anyw = K4 ? static_cast<const void*>(a.w_fp4) : static_cast<const void*>(a.w_fp8);
+  // token tile: the one with fewer (waves x operand bytes into the SM per stage); the 256-row
+  // tile pays ~10% for its single accumulator buffer
+  const int64_t n_tiles = (a.N + kMxTN - 1) / kMxTN;
+  auto cost = [&](int tm, double f) {
+    const int64_t t = ((a.M + tm - 1) / tm) * n_tiles;
+    return static_cast<double>((t + num_sms - 1) / num_sms) * (tm + kMxTN) * f;
+  };
+  const int tm = cost(256, 1.1) < cost(128, 1.0) ? 256 : 128;
   CUtensorMap m_a4, m_b4, m_a8, m_b8, m_asf, m_bsf;
   // an absent operand (no FP4 channels / no outliers) aliases the other one and is never read
   const void* a4 = K4 ? a.a_fp4 : any;
@@ -465,11 +517,11 @@ cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms
   const void* b8 = a.k_outlier ? a.w_fp8 : anyw;
   const uint64_t c4 = K4 ? K4 / 2 : 128, c8 = a.k_outlier ? 128 : K4 / 2;
   const uint64_t nsf = a.K / 32;
-  if (!mx_map(&m_a4, a4, c4, c4, a.M, 128, kMxTM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+  if (!mx_map(&m_a4, a4, c4, c4, a.M, 128, tm, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !mx_map(&m_b4, b4, c4, c4, a.N, 128, kMxTN, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !mx_map(&m_a8, a8, c8, c8, a.M, 128, kMxTM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !mx_map(&m_a8, a8, c8, c8, a.M, 128, tm, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !mx_map(&m_b8, b8, c8, c8, a.N, 128, kMxTN, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !mx_map(&m_asf, a.a_sf, nsf, a.lda_sf, a.M, 16, kMxTM, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !mx_map(&m_asf, a.a_sf, nsf, a.lda_sf, a.M, 16, tm, CU_TENSOR_MAP_SWIZZLE_NONE) ||
       !mx_map(&m_bsf, a.w_sf, nsf, a.ldw_sf, a.N, 16, kMxTN, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   MxParams p;
@@ -482,21 +534,27 @@ cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms
   p.ch_last = (chunks % 2) ? 1 : 2;
   p.has8 = a.k_outlier ? 1 : 0;
   p.sf_off8 = static_cast<int>(K4 / 32);
-  p.m_tiles = static_cast<int>((a.M + kMxTM - 1) / kMxTM);
-  p.num_tiles = p.m_tiles * static_cast<int>((a.N + kMxTN - 1) / kMxTN);
+  p.m_tiles = static_cast<int>((a.M + tm - 1) / tm);
+  p.num_tiles = p.m_tiles * static_cast<int>(n_tiles);
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
-  const size_t smem = sizeof(MxSmem) + 1024;
-  static std::once_flag once[64];
-  static cudaError_t attr_err[64];
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  std::call_once(once[dev], [&]() {
-    attr_err[dev] = cudaFuncSetAttribute(mx_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-  });
-  if (attr_err[dev] != cudaSuccess) return attr_err[dev];
-  cudaError_t e = launch_pdl(mx_gemm_kernel, dim3(grid), dim3(kMxThreads), smem, stream, m_a4,
-                             m_b4, m_a8, m_b8, m_asf, m_bsf, p);
+  auto go = [&](auto tm_tag) -> cudaError_t {
+    constexpr int kTM = decltype(tm_tag)::value;
+    const size_t smem = sizeof(MxSmem<MxCfg<kTM>>) + 1024;
+    static std::once_flag once[64];
+    static cudaError_t attr_err[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::call_once(once[dev], [&]() {
+      attr_err[dev] = cudaFuncSetAttribute(mx_gemm_kernel<kTM>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+    });
+    if (attr_err[dev] != cudaSuccess) return attr_err[dev];
+    return launch_pdl(mx_gemm_kernel<kTM>, dim3(grid), dim3(kMxThreads), smem, stream, m_a4, m_b4,
+                      m_a8, m_b8, m_asf, m_bsf, p);
+  };
+  cudaError_t e = tm == 256 ? go(std::integral_constant<int, 256>{})
+                            : go(std::integral_constant<int, 128>{});
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -81,6 +81,8 @@ def test_mx_quantize_adversarial(atom):
     (200, 896, 2048, 0),     # pure MXFP4, two token tiles
     (129, 1152, 1152, 128),  # ragged token tail
     (300, 4096, 4096, 128),  # config 2 shape family
+    (512, 13824, 5120, 128), # config 4: 256-token tiles (two MMA halves), ragged channel tile
+    (1000, 28672, 1024, 128),  # 256-token tiles, ragged token tail
 ])
 def test_mx_gemm_vs_oracle(atom, M, N, K, k_o):
     import torch
