@@ -145,7 +145,7 @@ struct GemmParams {
 #ifdef ATOM_DEV_PROBES
 // Development-only timeline probe (never in the shipped library): clock64 of event ev for group
 // g of CTA 0.  Built with ATOM_NVCC_EXTRA=-DATOM_DEV_PROBES, enabled by ATOM_GEMM_TRACE=1.
-constexpr int kTraceN = 512, kTraceEv = 27;
+constexpr int kTraceN = 512, kTraceEv = 31;
 #define TRACE(ev, g)                                                                      \
   do {                                                                                    \
     if (p.trace != nullptr && blockIdx.x == 0 && (g) < kTraceN)                           \
@@ -948,15 +948,28 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           }
           __threadfence();
           named_bar_sync(1, kEpiThreads);
-          if (e == 0 && lane == 0)
+          if (e == 0 && lane == 0) {
             red_release_add(p.counters + cta_of(p, static_cast<int64_t>(w.tile + 1) * p.G - 1), 1);
+#ifdef ATOM_DEV_PROBES
+            if (p.trace != nullptr && blockIdx.x < kTraceN) p.trace[30 * kTraceN + blockIdx.x] = gtimer();
+#endif
+          }
           continue;
         }
         // reducer (this CTA's last item): the other segments belong to CTAs first..blockIdx-1
         const int first = cta_of(p, static_cast<int64_t>(w.tile) * p.G);
         const int nseg = static_cast<int>(blockIdx.x) - first;
         if (e == 0 && lane == 0) {
+#ifdef ATOM_DEV_PROBES
+          if (p.trace != nullptr && blockIdx.x < kTraceN) {
+            p.trace[27 * kTraceN + blockIdx.x] = gtimer();
+            p.trace[29 * kTraceN + blockIdx.x] = nseg;
+          }
+#endif
           while (ld_acquire(p.counters + blockIdx.x) < nseg) __nanosleep(64);
+#ifdef ATOM_DEV_PROBES
+          if (p.trace != nullptr && blockIdx.x < kTraceN) p.trace[28 * kTraceN + blockIdx.x] = gtimer();
+#endif
           p.counters[blockIdx.x] = 0;        // self-cleaning for the next launch
         }
         named_bar_sync(1, kEpiThreads);
@@ -1309,9 +1322,12 @@ cudaError_t launch_w4a4_gemm(const GemmArgs& a, void* workspace, size_t workspac
       }
       std::fprintf(stderr, "CTA globaltimer ns: start spread %lld, end first %lld last %lld\n",
                    s1 - s0, e0 - s0, e1 - s0);
-      for (int b = 0; b < plan.grid && b < kTraceN; b += 8)
-        std::fprintf(stderr, "  cta %3d start %6lld end %6lld\n", b, h[25 * kTraceN + b] - s0,
-                     h[26 * kTraceN + b] - s0);
+      for (int b = 0; b < plan.grid && b < kTraceN; b += 4)
+        std::fprintf(stderr, "  cta %3d start %6lld end %6lld published %6lld red_wait %6lld..%6lld nseg %lld\n",
+                     b, h[25 * kTraceN + b] - s0, h[26 * kTraceN + b] - s0,
+                     h[30 * kTraceN + b] ? h[30 * kTraceN + b] - s0 : -1,
+                     h[27 * kTraceN + b] ? h[27 * kTraceN + b] - s0 : -1,
+                     h[28 * kTraceN + b] ? h[28 * kTraceN + b] - s0 : -1, h[29 * kTraceN + b]);
     }
     const long long t0 = h[3 * kTraceN];
     for (int g = 0; g < kTraceN; ++g) {
