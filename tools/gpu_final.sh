@@ -12,7 +12,7 @@ timeout -s KILL 600 python bench.py > $O/bench_cfg5.json 2> $O/bench_cfg5.err; e
 timeout -s KILL 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference_cfg5.json 2> $O/bench_reference.err; echo "ref rc=$?"
 bash tools/sweep.sh $O/sweep.jsonl > $O/sweep.log 2>&1; echo "sweep done"
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file $O/launches_cfg5.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
+  --log-file $O/launches_cfg5.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline \
   --spinup 0 --no-peak > $O/launches.log 2>&1; echo "ncu launches rc=$?"
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:w4a4_gemm \
   -s 3 -c 1 -o $O/prof_gemm_cfg5 python bench.py --steps 4 --warmup 3 --no-e2e \
