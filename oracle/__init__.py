@@ -19,7 +19,8 @@ import numpy as np
 GROUP = 128
 _HERE = Path(__file__).resolve().parent
 _SRC = _HERE / "atom_oracle.c"
-_SRCS = [_SRC, _HERE / "mx_oracle.c"]   # mx_oracle.c: Atom (FP) on the MX format (NEXT-2)
+_SRCS = [_SRC, _HERE / "mx_oracle.c",   # mx_oracle.c: Atom (FP) on the MX format (NEXT-2)
+         _HERE / "kv_oracle.c"]           # kv_oracle.c: quantized KV cache + decode attention (NEXT-3)
 _LIB = _HERE / "liboracle.so"
 
 ORC_OK, ORC_ERR_NULL, ORC_ERR_SHAPE, ORC_ERR_ARG, ORC_ERR_OVERFLOW = 0, 1, 2, 4, 8
@@ -69,6 +70,10 @@ def lib():
             f.restype = ctypes.c_int
         L.oracle_mx_scale_byte.argtypes = [ctypes.c_float, ctypes.c_int]
         L.oracle_mx_scale_byte.restype = ctypes.c_int
+        L.oracle_kv_quantize.argtypes = [P, i64, i32, i32, P, P, P]
+        L.oracle_kv_quantize.restype = ctypes.c_int
+        L.oracle_decode_attention.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P, P]
+        L.oracle_decode_attention.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_max_threads.restype = ctypes.c_int
         for f in (L.oracle_quantize_rows, L.oracle_group_partials, L.oracle_gemm_output,
@@ -277,3 +282,41 @@ def mx_quantized_linear(x, perm, w, K: int, k_outlier: int = 128):
     a = mx_quantize_rows(x, perm, K, k_outlier)
     wq = mx_quantize_rows(w, perm, K, k_outlier)
     return dict(a=a, w=wq, c=mx_output_rows(a, wq, x.shape[0], w.shape[0], K, k_outlier))
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-3: quantized paged KV cache + decode attention (kv_oracle.c): readings G25-G28
+# ---------------------------------------------------------------------------------------------
+KV_PAGE = 16
+
+
+def kv_quantize(x, slots, num_pages: int, codes=None, params=None):
+    """G25/G26: quantize token vectors x [T][H][d] (fp16 or fp32) into a paged cache at the
+    given slots (page * 16 + offset).  Returns (codes uint8 [P][H][16][d/2], params fp32
+    [P][H][16][2]); pass existing arrays to append."""
+    x32 = np.ascontiguousarray(np.asarray(x).astype(np.float32))
+    T, H, d = x32.shape
+    slots = np.ascontiguousarray(np.asarray(slots, dtype=np.int64))
+    assert slots.shape == (T,) and slots.max(initial=0) < num_pages * KV_PAGE
+    if codes is None:
+        codes = np.zeros((num_pages, H, KV_PAGE, d // 2), dtype=np.uint8)
+        params = np.zeros((num_pages, H, KV_PAGE, 2), dtype=np.float32)
+    st = lib().oracle_kv_quantize(_ptr(x32), T, H, d, _ptr(slots), _ptr(codes), _ptr(params))
+    _check(st, "oracle_kv_quantize")
+    return codes, params
+
+
+def decode_attention(q, k_cache, v_cache, block_table, seq_lens):
+    """G27: out [B][H][d] (float64) of one decode step over the dequantized paged cache;
+    q [B][H][d] (fp16 values), caches as returned by kv_quantize."""
+    q32 = np.ascontiguousarray(np.asarray(q).astype(np.float32))
+    B, H, d = q32.shape
+    bt = np.ascontiguousarray(np.asarray(block_table, dtype=np.int32))
+    sl = np.ascontiguousarray(np.asarray(seq_lens, dtype=np.int32))
+    out = np.zeros((B, H, d), dtype=np.float64)
+    st = lib().oracle_decode_attention(_ptr(q32), B, H, d, _ptr(_c(k_cache[0])),
+                                       _ptr(_c(k_cache[1])), _ptr(_c(v_cache[0])),
+                                       _ptr(_c(v_cache[1])), _ptr(bt), bt.shape[1], _ptr(sl),
+                                       _ptr(out))
+    _check(st, "oracle_decode_attention")
+    return out
