@@ -78,7 +78,7 @@
 extern "C" {
 #endif
 
-#define ATOM_ABI_VERSION 4
+#define ATOM_ABI_VERSION 5
 #define ATOM_GROUP 128
 
 typedef enum {
@@ -272,6 +272,40 @@ atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uin
                            int64_t lda_sf, const uint8_t* w_fp4, const uint8_t* w_fp8,
                            const uint8_t* w_sf, int64_t ldw_sf, int64_t M, int64_t N, int64_t K,
                            int32_t k_outlier, void* c_f16, int64_t ldc, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Quantized KV cache + decode attention (NEXT-3).  "Atom loads the KV-cache in low-bit
+ * precision and directly dequantizes it before performing the FP16 calculation", "asymmetric
+ * quantization ... with the granularity of attention head" (Section 4.4), paged as in
+ * PageAttention.  Readings G25-G28 of DESIGN.md; bit-exact with oracle/kv_oracle.c.
+ *   pages of 16 tokens; head_dim = 128
+ *   codes   uint8 [num_pages][H][16][64]   INT4 codes in [0, 15], low nibble = even dimension
+ *   params  fp32  [num_pages][H][16][2]    (s, mn) per (token, head): value = code * s + mn
+ *   slot of a token = page * 16 + offset; block_table int32 [B][max_pages]: page of tokens
+ *   [16 j, 16 j + 16) of sequence b
+ *   Quantization per (token, head) vector, each step one binary32 IEEE operation:
+ *   s = RN(RN(max - min) / 15); inv = s > 0 ? RN(1 / s) : 0; code = clamp(rint(RN(RN(x - min) *
+ *   inv)), 0, 15) (round half to even).
+ * ------------------------------------------------------------------------------------------ */
+
+/* Quantize T new tokens' K (or V) vectors x_f16 [T][ldx] (head h of token t at x[t*ldx + 128h])
+ * into the cache at slots[t] (int32).  H >= 1, head_dim == 128, ldx >= 128 H, ldx % 4 == 0.  The
+ * slots must be distinct and inside the caller's cache (not checked). */
+atom_status_t atom_kv_quantize(const void* x_f16, int64_t T, int64_t ldx, int32_t H,
+                               int32_t head_dim, const int32_t* slots, uint8_t* codes,
+                               float* params, void* stream);
+
+/* One decode step: out[b][h][:] (fp32 [B][H][128]) = softmax(q k^T / sqrt(128)) v over the
+ * dequantized tokens t < seq_lens[b] of sequence b (1 <= seq_lens[b] <= max_seq_len <=
+ * 16 max_pages; seq_lens on the device, max_seq_len a host-side bound used to split the work).
+ * q_f16 [B][H][128].  workspace: atom_decode_attention_workspace_size bytes (may be 0). */
+atom_status_t atom_decode_attention(const void* q_f16, int64_t B, int32_t H, int32_t head_dim,
+                                    const uint8_t* k_codes, const float* k_params,
+                                    const uint8_t* v_codes, const float* v_params,
+                                    const int32_t* block_table, int64_t max_pages,
+                                    const int32_t* seq_lens, int32_t max_seq_len, float* out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+size_t atom_decode_attention_workspace_size(int64_t B, int32_t H, int32_t max_seq_len);
 
 /* Test helper: on `stream`, sets *ok_flag (device int32) to 1 iff perm[0..K) is a bijection of
  * [0,K) (ldx == K) or an injection into [0,ldx).  scratch: device int32 [ldx], clobbered. */

@@ -9,6 +9,7 @@ Names follow the ABI and the paper:
   quantize_weights(w, perm)        a0  offline weight reorder + quantize
   w4a4_gemm(a, w)                  a2-a5 fused group GEMM with INT8 outliers
   mx_quantize(x, perm) / mx_gemm(a, w)   NEXT-2 Atom (FP) on the MX format
+  kv_quantize / decode_attention         NEXT-3 INT4 KV cache + decode attention
 """
 from __future__ import annotations
 
@@ -34,6 +35,7 @@ ABI_SYMBOLS = ("atom_reorder_quantize", "atom_rmsnorm_reorder_quantize",
                "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_f8_workspace_size",
                "atom_w4a4_gemm_counter_bytes",
                "atom_mx_reorder_quantize", "atom_mx_gemm",
+               "atom_kv_quantize", "atom_decode_attention", "atom_decode_attention_workspace_size",
                "atom_validate_perm", "atom_status_string",
                "atom_abi_version", "atom_last_launch_count")
 
@@ -78,6 +80,13 @@ def _lib():
         L.atom_mx_reorder_quantize.restype = ctypes.c_int
         L.atom_mx_gemm.argtypes = [P, P, P, i64, P, P, P, i64, i64, i64, i64, i32, P, i64, P]
         L.atom_mx_gemm.restype = ctypes.c_int
+        L.atom_kv_quantize.argtypes = [P, i64, i64, i32, i32, P, P, P, P]
+        L.atom_kv_quantize.restype = ctypes.c_int
+        L.atom_decode_attention.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P, i32, P, P,
+                                            ctypes.c_size_t, P]
+        L.atom_decode_attention.restype = ctypes.c_int
+        L.atom_decode_attention_workspace_size.argtypes = [i64, i32, i32]
+        L.atom_decode_attention_workspace_size.restype = ctypes.c_size_t
         L.atom_validate_perm.argtypes = [P, i64, i64, P, P, P]
         L.atom_status_string.argtypes = [ctypes.c_int]
         L.atom_status_string.restype = ctypes.c_char_p
@@ -438,4 +447,69 @@ def mx_gemm(a: MxQuantized, w: MxQuantized, out=None, stream=None):
                              _ptr(w.fp8), _ptr(w.sf), w.sf.stride(0), M, N, a.K, a.k_outlier,
                              _ptr(out), out.stride(0), _stream(stream))
     _check(st, "atom_mx_gemm")
+    return out
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-3: quantized paged KV cache + decode attention (include/atom.h "KV cache")
+# ---------------------------------------------------------------------------------------------
+KV_PAGE = 16
+HEAD_DIM = 128
+
+
+@dataclass
+class KvCache:
+    """One of K or V: codes uint8 [num_pages][H][16][64], params fp32 [num_pages][H][16][2]."""
+    codes: object
+    params: object
+
+    @staticmethod
+    def empty(num_pages: int, H: int, device="cuda"):
+        import torch
+        return KvCache(torch.zeros((num_pages, H, KV_PAGE, HEAD_DIM // 2), dtype=torch.uint8,
+                                   device=device),
+                       torch.zeros((num_pages, H, KV_PAGE, 2), dtype=torch.float32,
+                                   device=device))
+
+
+def kv_quantize(x, slots, cache: KvCache, stream=None) -> KvCache:
+    """Quantize T tokens' vectors x fp16 [T][H*128] into `cache` at int32 `slots`."""
+    import torch
+    if x.dtype != torch.float16 or x.dim() != 2 or x.stride(1) != 1:
+        raise TypeError("x must be a 2-D fp16 tensor with contiguous rows")
+    H = cache.codes.shape[1]
+    if slots.dtype != torch.int32 or slots.numel() != x.shape[0] or x.shape[1] < H * HEAD_DIM:
+        raise ValueError("slots must be int32 [T] and x [T][>= H*128]")
+    st = _lib().atom_kv_quantize(_ptr(x), x.shape[0], x.stride(0), H, HEAD_DIM, _ptr(slots),
+                                 _ptr(cache.codes), _ptr(cache.params), _stream(stream))
+    _check(st, "atom_kv_quantize")
+    return cache
+
+
+_KV_WS = {}
+
+
+def decode_attention(q, k: KvCache, v: KvCache, block_table, seq_lens, max_seq_len: int,
+                     out=None, stream=None):
+    """One decode step over the quantized cache: out fp32 [B][H][128]."""
+    import torch
+    B, H = q.shape[0], q.shape[1]
+    if q.dtype != torch.float16 or tuple(q.shape[1:]) != (H, HEAD_DIM) or not q.is_contiguous():
+        raise TypeError("q must be a contiguous fp16 [B][H][128] tensor")
+    if block_table.dtype != torch.int32 or seq_lens.dtype != torch.int32:
+        raise TypeError("block_table and seq_lens must be int32")
+    if out is None:
+        out = torch.empty((B, H, HEAD_DIM), dtype=torch.float32, device=q.device)
+    n = _lib().atom_decode_attention_workspace_size(B, H, int(max_seq_len))
+    ws = None
+    if n:
+        key = (q.device.index, n)
+        ws = _KV_WS.get(key)
+        if ws is None:
+            ws = _KV_WS[key] = torch.empty(n, dtype=torch.uint8, device=q.device)
+    st = _lib().atom_decode_attention(_ptr(q), B, H, HEAD_DIM, _ptr(k.codes), _ptr(k.params),
+                                      _ptr(v.codes), _ptr(v.params), _ptr(block_table),
+                                      block_table.shape[1], _ptr(seq_lens), int(max_seq_len),
+                                      _ptr(out), _ptr(ws), n, _stream(stream))
+    _check(st, "atom_decode_attention")
     return out

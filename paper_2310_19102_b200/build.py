@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libatom.so"
-SOURCES = ["atom_api.cu", "quantize.cu", "gemm.cu", "mxfp.cu"]
+SOURCES = ["atom_api.cu", "quantize.cu", "gemm.cu", "mxfp.cu", "kvcache.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

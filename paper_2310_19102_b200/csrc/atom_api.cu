@@ -368,6 +368,67 @@ atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uin
   return ATOM_OK;
 }
 
+atom_status_t atom_kv_quantize(const void* x_f16, int64_t T, int64_t ldx, int32_t H,
+                               int32_t head_dim, const int32_t* slots, uint8_t* codes,
+                               float* params, void* stream) {
+  g_last_launches = 0;
+  if (T < 0 || H <= 0 || head_dim != 128 || ldx < 128LL * H || ldx % 4 != 0) return ATOM_ERR_SHAPE;
+  if (T == 0) return ATOM_OK;
+  if (!x_f16 || !slots || !codes || !params) return ATOM_ERR_NULL;
+  if (!aligned16(codes) || !aligned16(params) || (reinterpret_cast<uintptr_t>(x_f16) & 7u) ||
+      (reinterpret_cast<uintptr_t>(slots) & 3u))
+    return ATOM_ERR_ALIGN;
+  DeviceInfo dev;
+  atom_status_t st = current_device(&dev);
+  if (st != ATOM_OK) return st;
+  if (atom::launch_kv_quantize(x_f16, T, ldx, H, slots, codes, params,
+                               static_cast<cudaStream_t>(stream), dev.num_sms) != cudaSuccess)
+    return ATOM_ERR_CUDA;
+  g_last_launches = 1;
+  return ATOM_OK;
+}
+
+size_t atom_decode_attention_workspace_size(int64_t B, int32_t H, int32_t max_seq_len) {
+  if (B <= 0 || H <= 0 || max_seq_len <= 0) return 0;
+  DeviceInfo dev;
+  if (current_device(&dev) != ATOM_OK) return 0;
+  return atom::decode_attention_workspace_bytes(B, H, max_seq_len, dev.num_sms);
+}
+
+atom_status_t atom_decode_attention(const void* q_f16, int64_t B, int32_t H, int32_t head_dim,
+                                    const uint8_t* k_codes, const float* k_params,
+                                    const uint8_t* v_codes, const float* v_params,
+                                    const int32_t* block_table, int64_t max_pages,
+                                    const int32_t* seq_lens, int32_t max_seq_len, float* out,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  g_last_launches = 0;
+  if (B < 0 || H <= 0 || head_dim != 128 || max_pages <= 0 || max_seq_len <= 0 ||
+      max_seq_len > 16 * max_pages || B * H > 0x7fffffffLL)
+    return ATOM_ERR_SHAPE;
+  if (B == 0) return ATOM_OK;
+  if (!q_f16 || !k_codes || !k_params || !v_codes || !v_params || !block_table || !seq_lens ||
+      !out)
+    return ATOM_ERR_NULL;
+  if (!aligned16(q_f16) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(k_params) ||
+      !aligned16(v_params) || !aligned16(out))
+    return ATOM_ERR_ALIGN;
+  DeviceInfo dev;
+  atom_status_t st = current_device(&dev);
+  if (st != ATOM_OK) return st;
+  const size_t need = atom::decode_attention_workspace_bytes(B, H, max_seq_len, dev.num_sms);
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned16(workspace)))
+    return ATOM_ERR_WORKSPACE;
+  int launches = 0;
+  if (atom::launch_decode_attention(q_f16, B, H, k_codes, k_params, v_codes, v_params,
+                                    block_table, max_pages, seq_lens, max_seq_len, out,
+                                    static_cast<float*>(workspace),
+                                    static_cast<cudaStream_t>(stream), dev.num_sms,
+                                    &launches) != cudaSuccess)
+    return ATOM_ERR_CUDA;
+  g_last_launches = launches;
+  return ATOM_OK;
+}
+
 atom_status_t atom_validate_perm(const int32_t* perm, int64_t K, int64_t ldx, int32_t* scratch,
                                  int32_t* ok_flag, void* stream) {
   g_last_launches = 0;

@@ -107,4 +107,16 @@ struct MxGemmArgs {
 };
 cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms);
 
+// NEXT-3: quantized paged KV cache + decode attention (kvcache.cu, include/atom.h "KV cache")
+cudaError_t launch_kv_quantize(const void* x, int64_t T, int64_t ldx, int32_t H,
+                               const int32_t* slots, uint8_t* codes, float* params,
+                               cudaStream_t stream, int num_sms);
+cudaError_t launch_decode_attention(const void* q, int64_t B, int32_t H, const uint8_t* kc,
+                                    const float* kp, const uint8_t* vc, const float* vp,
+                                    const int32_t* block_table, int64_t max_pages,
+                                    const int32_t* seq_lens, int32_t max_seq_len, float* out,
+                                    float* workspace, cudaStream_t stream, int num_sms,
+                                    int* launches);
+size_t decode_attention_workspace_bytes(int64_t B, int32_t H, int32_t max_seq_len, int num_sms);
+
 }  // namespace atom

@@ -1,0 +1,301 @@
+// kvcache.cu -- NEXT-3: Atom's quantized KV cache and the dequantize-on-load decode attention.
+//
+// Paper (Section 4.4): "Atom loads the KV-cache in low-bit precision and directly
+// dequantizes it before performing the FP16 calculation"; "asymmetric quantization ... with the
+// granularity of attention head"; the query is multiplied by the K cache, normalised by softmax
+// and multiplied with the V cache; PageAttention manages the memory.  Readings G25-G28
+// (DESIGN.md): one (scale, min) per (token, head) vector, INT4 codes in [0, 15], 16-token pages.
+//
+// B200 design: decode attention is HBM-bound (each cached byte is used once per step); every
+// token-head vector is 64 bytes of codes + 8 bytes of (s, mn).  Split-K ("flash decoding"): a CTA
+// of 4 warps handles one (sequence, head, chunk of tokens); a warp takes 8 tokens at a time,
+// 4 lanes per token, each lane 32 dimensions = one 16-byte load of codes, so a warp reads 8
+// tokens' 64-byte vectors of one page as 512 contiguous bytes.  The dequantization is folded
+// algebraically (sum_i q_i (c_i s + mn) = s sum_i q_i c_i + mn sum_i q_i; sum_t p_t (c_t s + mn)
+// = sum_t (p_t s) c_t + sum_t p_t mn_t), so the inner loops are one code extraction and one FMA
+// per element.  Scores of the chunk are kept in shared memory (exact two-pass softmax inside the
+// chunk); chunks are merged by a small combine kernel (log-sum-exp).
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace atom {
+
+constexpr int kKvPage = 16;
+constexpr int kKvD = 128;                 // head dimension of the kernels (Llama)
+constexpr int kAttThreads = 128;
+constexpr int kMaxChunk = 1024;           // tokens per CTA (scores in shared memory)
+
+// ---------------------------------------------------------------------------------------------
+// quantize: one warp per (token, head) vector, a lane owns 4 dimensions
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+kv_quantize_kernel(const __half* __restrict__ x, int64_t T, int64_t ldx, int32_t H,
+                   const int32_t* __restrict__ slots, uint8_t* __restrict__ codes,
+                   float* __restrict__ params) {
+  griddep_wait();
+  griddep_launch();
+  const int lane = threadIdx.x % 32;
+  const int64_t nvec = T * H;
+  for (int64_t v = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32; v < nvec;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+    const int64_t t = v / H;
+    const int h = static_cast<int>(v % H);
+    const uint2 raw = *reinterpret_cast<const uint2*>(x + t * ldx + h * kKvD + 4 * lane);
+    const __half2* hp = reinterpret_cast<const __half2*>(&raw);
+    const float2 a = __half22float2(hp[0]), b = __half22float2(hp[1]);
+    const float xv[4] = {a.x, a.y, b.x, b.y};
+    float mn = fminf(fminf(xv[0], xv[1]), fminf(xv[2], xv[3]));
+    float mx = fmaxf(fmaxf(xv[0], xv[1]), fmaxf(xv[2], xv[3]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    // G25, each step one IEEE operation: s = RN(RN(mx - mn) / 15), inv = RN(1 / s)
+    const float s = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+    const float inv = s > 0.0f ? __frcp_rn(s) : 0.0f;
+    uint32_t packed = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float r = fminf(fmaxf(rintf(__fmul_rn(__fsub_rn(xv[k], mn), inv)), 0.0f), 15.0f);
+      packed |= static_cast<uint32_t>(r) << (4 * k);
+    }
+    const int64_t slot = slots[t];
+    const int64_t base = ((slot / kKvPage) * H + h) * kKvPage + slot % kKvPage;
+    reinterpret_cast<uint16_t*>(codes + base * (kKvD / 2))[lane] = static_cast<uint16_t>(packed);
+    if (lane == 0) reinterpret_cast<float2*>(params)[base] = make_float2(s, mn);
+  }
+}
+
+cudaError_t launch_kv_quantize(const void* x, int64_t T, int64_t ldx, int32_t H,
+                               const int32_t* slots, uint8_t* codes, float* params,
+                               cudaStream_t stream, int num_sms) {
+  int64_t blocks = (T * H * 32 + 255) / 256;
+  if (blocks > 16LL * num_sms) blocks = 16LL * num_sms;
+  return launch_pdl(kv_quantize_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, stream,
+                    static_cast<const __half*>(x), T, ldx, H, slots, codes, params);
+}
+
+// ---------------------------------------------------------------------------------------------
+// decode attention
+// ---------------------------------------------------------------------------------------------
+// the 8 codes of a 32-bit word as floats (exact: 2^23 + n - 2^23)
+__device__ __forceinline__ float code_f(uint32_t w, int k) {
+  return __uint_as_float(((w >> (4 * k)) & 0xFu) | 0x4B000000u) - 8388608.0f;
+}
+
+// CTA (b, h, chunk): tokens [c0, c1) of sequence b.  splits > 1: writes the chunk's (max, sum,
+// unnormalised output) to the workspace; splits == 1: the normalised output.
+__global__ void __launch_bounds__(kAttThreads)
+decode_attention_kernel(const __half* __restrict__ q, int32_t H,
+                        const uint8_t* __restrict__ kc, const float* __restrict__ kp,
+                        const uint8_t* __restrict__ vc, const float* __restrict__ vp,
+                        const int32_t* __restrict__ block_table, int64_t max_pages,
+                        const int32_t* __restrict__ seq_lens, int32_t chunk, int32_t splits,
+                        float* __restrict__ out, float* __restrict__ part) {
+  __shared__ float sc[kMaxChunk];
+  __shared__ float red[kAttThreads / 32][kKvD + 2];
+  const int bh = blockIdx.x, split = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  griddep_wait();
+  griddep_launch();
+  const int L = seq_lens[b];
+  const int c0 = split * chunk, c1 = min(L, c0 + chunk);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tj = lane >> 2, part4 = lane & 3;         // token slot within 8, dimension quarter
+  // q of this lane's 32 dimensions, scaled by 1/sqrt(d), and their sum
+  float qv[32];
+  {
+    const uint4* qp = reinterpret_cast<const uint4*>(q + static_cast<int64_t>(bh) * kKvD + 32 * part4);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 r = qp[i];
+      const __half2* hp = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(hp[k]);
+        qv[8 * i + 2 * k] = f.x;
+        qv[8 * i + 2 * k + 1] = f.y;
+      }
+    }
+  }
+  constexpr float kRsqrtD = 0.08838834764831845f;     // 1 / sqrt(128)
+  float qsum = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) qsum += qv[i];
+  const int32_t* bt = block_table + static_cast<int64_t>(b) * max_pages;
+  auto vec = [&](int t) {                             // (page, head, offset) index of token t
+    return (static_cast<int64_t>(bt[t / kKvPage]) * H + h) * kKvPage + t % kKvPage;
+  };
+
+  // ---- pass 1: scores of the chunk into shared memory ----
+  float wmax = -INFINITY;
+  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += 8 * (kAttThreads / 32)) {
+    const int t = t0 + tj;
+    float part = 0.0f;
+    if (t < c1) {
+      const int64_t v = vec(t);
+      const uint4 w = *reinterpret_cast<const uint4*>(kc + v * (kKvD / 2) + 16 * part4);
+      const float2 sm = reinterpret_cast<const float2*>(kp)[v];
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      float dot = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dot = fmaf(qv[8 * i + k], code_f(ww[i], k), dot);
+      part = fmaf(sm.x, dot, sm.y * qsum);
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (t < c1) {
+      const float score = part * kRsqrtD;
+      if (part4 == 0) sc[t - c0] = score;
+      wmax = fmaxf(wmax, score);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+  if (lane == 0) red[warp][0] = wmax;
+  __syncthreads();
+  float cmax = red[0][0];
+#pragma unroll
+  for (int w = 1; w < kAttThreads / 32; ++w) cmax = fmaxf(cmax, red[w][0]);
+  __syncthreads();
+
+  // ---- pass 2: p_t = exp(score - max), out = sum_t p_t v_t ----
+  float acc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
+  float psum = 0.0f, pmn = 0.0f;                      // sum p_t, sum p_t mn_t (this lane's tokens)
+  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += 8 * (kAttThreads / 32)) {
+    const int t = t0 + tj;
+    if (t < c1) {
+      const int64_t v = vec(t);
+      const uint4 w = *reinterpret_cast<const uint4*>(vc + v * (kKvD / 2) + 16 * part4);
+      const float2 sm = reinterpret_cast<const float2*>(vp)[v];
+      const float p = __expf(sc[t - c0] - cmax);
+      const float ps = p * sm.x;
+      psum += p;
+      pmn = fmaf(p, sm.y, pmn);
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[8 * i + k] = fmaf(ps, code_f(ww[i], k), acc[8 * i + k]);
+    }
+  }
+  // reduce over the 8 token slots of the warp (lanes with the same dimension quarter)
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+    psum += __shfl_xor_sync(0xffffffffu, psum, off);
+    pmn += __shfl_xor_sync(0xffffffffu, pmn, off);
+  }
+  // psum / pmn were counted once per token by each of its 4 lanes: use lane part4's own copy
+  if (tj == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) red[warp][32 * part4 + i] = acc[i];
+    if (part4 == 0) {
+      red[warp][kKvD] = psum;
+      red[warp][kKvD + 1] = pmn;
+    }
+  }
+  __syncthreads();
+  // combine the 4 warps: thread i < 128 owns output dimension i
+  const int i = threadIdx.x;
+  float o = 0.0f, l = 0.0f, lm = 0.0f;
+#pragma unroll
+  for (int w = 0; w < kAttThreads / 32; ++w) {
+    o += red[w][i];
+    l += red[w][kKvD];
+    lm += red[w][kKvD + 1];
+  }
+  o += lm;                                            // + sum_t p_t mn_t (same for every dim)
+  if (splits == 1) {
+    out[static_cast<int64_t>(bh) * kKvD + i] = c1 > c0 ? o / l : 0.0f;
+  } else {
+    float* pp = part + (static_cast<int64_t>(bh) * splits + split) * (kKvD + 2);
+    pp[i] = o;
+    if (i == 0) {
+      pp[kKvD] = c1 > c0 ? cmax : -INFINITY;
+      pp[kKvD + 1] = l;
+    }
+  }
+}
+
+// log-sum-exp merge of the chunks: one warp per (sequence, head), a lane owns 4 dimensions
+__global__ void __launch_bounds__(128)
+decode_combine_kernel(int64_t BH, int32_t splits, const float* __restrict__ part,
+                      float* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
+  const int lane = threadIdx.x % 32;
+  const int64_t bh = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+  if (bh >= BH) return;
+  const float* pp = part + bh * splits * (kKvD + 2);
+  float m = -INFINITY;
+  for (int s = 0; s < splits; ++s) m = fmaxf(m, pp[s * (kKvD + 2) + kKvD]);
+  float l = 0.0f, o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int s = 0; s < splits; ++s) {
+    const float ms = pp[s * (kKvD + 2) + kKvD];
+    if (ms == -INFINITY) continue;
+    const float f = __expf(ms - m);
+    l = fmaf(f, pp[s * (kKvD + 2) + kKvD + 1], l);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = fmaf(f, pp[s * (kKvD + 2) + 4 * lane + k], o[k]);
+  }
+  *reinterpret_cast<float4*>(out + bh * kKvD + 4 * lane) =
+      make_float4(o[0] / l, o[1] / l, o[2] / l, o[3] / l);
+}
+
+// chunk (multiple of the page) and split count for a batch: enough CTAs for ~2 waves
+void plan_decode_attention(int64_t BH, int32_t max_seq_len, int num_sms, int32_t* chunk,
+                           int32_t* splits) {
+  int64_t s = (2LL * num_sms + BH - 1) / BH;
+  const int64_t max_split = (max_seq_len + 63) / 64;   // at least 64 tokens per chunk
+  if (s > max_split) s = max_split;
+  if (s < 1) s = 1;
+  int64_t c = (max_seq_len + s - 1) / s;
+  c = ((c + kKvPage - 1) / kKvPage) * kKvPage;
+  if (c > kMaxChunk) c = kMaxChunk;
+  *chunk = static_cast<int32_t>(c);
+  *splits = static_cast<int32_t>((max_seq_len + c - 1) / c);
+}
+
+cudaError_t launch_decode_attention(const void* q, int64_t B, int32_t H, const uint8_t* kc,
+                                    const float* kp, const uint8_t* vc, const float* vp,
+                                    const int32_t* block_table, int64_t max_pages,
+                                    const int32_t* seq_lens, int32_t max_seq_len, float* out,
+                                    float* workspace, cudaStream_t stream, int num_sms,
+                                    int* launches) {
+  int32_t chunk, splits;
+  plan_decode_attention(B * H, max_seq_len, num_sms, &chunk, &splits);
+  cudaError_t e = launch_pdl(decode_attention_kernel,
+                             dim3(static_cast<unsigned>(B * H), static_cast<unsigned>(splits)),
+                             dim3(kAttThreads), 0, stream, static_cast<const __half*>(q), H, kc,
+                             kp, vc, vp, block_table, max_pages, seq_lens, chunk, splits, out,
+                             workspace);
+  if (e != cudaSuccess) return e;
+  *launches = 1;
+  if (splits > 1) {
+    const int64_t blocks = (B * H * 32 + 127) / 128;
+    e = launch_pdl(decode_combine_kernel, dim3(static_cast<unsigned>(blocks)), dim3(128), 0,
+                   stream, B * H, splits, static_cast<const float*>(workspace), out);
+    if (e != cudaSuccess) return e;
+    *launches = 2;
+  }
+  return cudaSuccess;
+}
+
+size_t decode_attention_workspace_bytes(int64_t B, int32_t H, int32_t max_seq_len, int num_sms) {
+  int32_t chunk, splits;
+  plan_decode_attention(B * H, max_seq_len, num_sms, &chunk, &splits);
+  return splits > 1 ? static_cast<size_t>(B * H) * splits * (kKvD + 2) * sizeof(float) : 0;
+}
+
+}  // namespace atom
