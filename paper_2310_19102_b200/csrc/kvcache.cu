@@ -83,9 +83,19 @@ cudaError_t launch_kv_quantize(const void* x, int64_t T, int64_t ldx, int32_t H,
 // ---------------------------------------------------------------------------------------------
 // decode attention
 // ---------------------------------------------------------------------------------------------
-// the 8 codes of a 32-bit word as floats (exact: 2^23 + n - 2^23)
-__device__ __forceinline__ float code_f(uint32_t w, int k) {
-  return __uint_as_float(((w >> (4 * k)) & 0xFu) | 0x4B000000u) - 8388608.0f;
+// The 8 codes of a 32-bit word (dimensions 8j .. 8j+7) as 4 float pairs (dims 2k, 2k+1):
+// the even / odd nibbles are split into bytes once, a PRMT places each byte under the exponent
+// of 2^23 (0x4B0000nn = 2^23 + n), one FFMA2 subtracts 2^23 (exact).
+__device__ __forceinline__ void code_pairs(uint32_t w, float2 (&c)[4]) {
+  const uint32_t ev = w & 0x0F0F0F0Fu, od = (w >> 4) & 0x0F0F0F0Fu;
+  const float2 one = make_float2(1.0f, 1.0f), off = make_float2(-8388608.0f, -8388608.0f);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t sel = 0x7540u | static_cast<uint32_t>(k);   // byte k of the word, then 0x4B0000
+    const float2 f = make_float2(__uint_as_float(__byte_perm(ev, 0x4B000000u, sel)),
+                                 __uint_as_float(__byte_perm(od, 0x4B000000u, sel)));
+    c[k] = __ffma2_rn(f, one, off);
+  }
 }
 
 // CTA (b, h, chunk): tokens [c0, c1) of sequence b.  splits > 1: writes the chunk's (max, sum,
@@ -108,7 +118,7 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tj = lane >> 2, part4 = lane & 3;         // token slot within 8, dimension quarter
   // q of this lane's 32 dimensions, scaled by 1/sqrt(d), and their sum
-  float qv[32];
+  float qv[32];     // dims 32 part4 + j; used as 16 float2 pairs (2k, 2k+1)
   {
     const uint4* qp = reinterpret_cast<const uint4*>(q + static_cast<int64_t>(bh) * kKvD + 32 * part4);
 #pragma unroll
@@ -128,9 +138,11 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
 #pragma unroll
   for (int i = 0; i < 32; ++i) qsum += qv[i];
   const int32_t* bt = block_table + static_cast<int64_t>(b) * max_pages;
-  auto vec = [&](int t) {                             // (page, head, offset) index of token t
-    return (static_cast<int64_t>(bt[t / kKvPage]) * H + h) * kKvPage + t % kKvPage;
+  // the 8 tokens t0 .. t0+7 of a warp step lie in one page (t0 % 8 == 0): one table lookup
+  auto vec0 = [&](int t0) {                           // (page, head, offset) index of token t0
+    return (static_cast<int64_t>(__ldg(bt + t0 / kKvPage)) * H + h) * kKvPage + t0 % kKvPage;
   };
+  const float2* q2 = reinterpret_cast<const float2*>(qv);
 
   // ---- pass 1: scores of the chunk into shared memory ----
   float wmax = -INFINITY;
@@ -138,16 +150,19 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
     const int t = t0 + tj;
     float part = 0.0f;
     if (t < c1) {
-      const int64_t v = vec(t);
+      const int64_t v = vec0(t0) + tj;
       const uint4 w = *reinterpret_cast<const uint4*>(kc + v * (kKvD / 2) + 16 * part4);
       const float2 sm = reinterpret_cast<const float2*>(kp)[v];
       const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-      float dot = 0.0f;
+      float2 d2 = make_float2(0.0f, 0.0f);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
+        float2 c[4];
+        code_pairs(ww[i], c);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) dot = fmaf(qv[8 * i + k], code_f(ww[i], k), dot);
-      part = fmaf(sm.x, dot, sm.y * qsum);
+        for (int k = 0; k < 4; ++k) d2 = __ffma2_rn(q2[4 * i + k], c[k], d2);
+      }
+      part = fmaf(sm.x, d2.x + d2.y, sm.y * qsum);
     }
     part += __shfl_xor_sync(0xffffffffu, part, 1);
     part += __shfl_xor_sync(0xffffffffu, part, 2);
@@ -168,13 +183,14 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
 
   // ---- pass 2: p_t = exp(score - max), out = sum_t p_t v_t ----
   float acc[32];
+  float2* acc2 = reinterpret_cast<float2*>(acc);
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
   float psum = 0.0f, pmn = 0.0f;                      // sum p_t, sum p_t mn_t (this lane's tokens)
   for (int t0 = c0 + 8 * warp; t0 < c1; t0 += 8 * (kAttThreads / 32)) {
     const int t = t0 + tj;
     if (t < c1) {
-      const int64_t v = vec(t);
+      const int64_t v = vec0(t0) + tj;
       const uint4 w = *reinterpret_cast<const uint4*>(vc + v * (kKvD / 2) + 16 * part4);
       const float2 sm = reinterpret_cast<const float2*>(vp)[v];
       const float p = __expf(sc[t - c0] - cmax);
@@ -182,10 +198,14 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
       psum += p;
       pmn = fmaf(p, sm.y, pmn);
       const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      const float2 ps2 = make_float2(ps, ps);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
+        float2 c[4];
+        code_pairs(ww[i], c);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[8 * i + k] = fmaf(ps, code_f(ww[i], k), acc[8 * i + k]);
+        for (int k = 0; k < 4; ++k) acc2[4 * i + k] = __ffma2_rn(ps2, c[k], acc2[4 * i + k]);
+      }
     }
   }
   // reduce over the 8 token slots of the warp (lanes with the same dimension quarter)
