@@ -453,6 +453,11 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
     if not args.no_graph and not args.no_mx and P == 1:
         mx = time_atom_fp(atom, xd, layer.perm, M, N, K, args, dev, flush_l2)
 
+    # ---------------- NEXT-3: INT4 KV cache decode attention (Llama-7B decode, batch 128) -------
+    kv = None
+    if not args.no_graph and not args.no_kv and P == 1:
+        kv = time_kv_attention(atom, dev, flush_l2, args)
+
     # the box's INT8 tensor peak, measured in this run: cuBLAS int8 GEMM (torch._int_mm, 8192^3)
     int8_meas = None
     if rank == 0 and not args.no_peak:
@@ -536,6 +541,10 @@ def run_atom(args, M, N, K, cfg_name, world, rank, local_rank):
             "kernel": "atom::mx_gemm_kernel",
             "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} x 4 (fp4/bf16 nominal "
                            f"ratio, 9 / 2.25 PFLOP/s)"}),
+        "kv_attention": None if kv is None else dict(kv, roofline={
+            "bound": "hbm", "achieved": kv["GB/s"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": kv["GB/s"] / peaks["hbm_gbs"], "kernel": "atom::decode_attention_kernel",
+            "peak_source": f"{peak_src} HBM copy bandwidth"}),
         "clocks": sampler.summary(),
         "e2e": e2e,
     }
@@ -589,6 +598,51 @@ def time_atom_fp(atom, xd, perm, M, N, K, args, dev, flush_l2):
     out["format"] = "MXFP4 E2M1 (blocks of 32) + 128 MXFP8 E4M3 outlier channels, UE8M0 scales"
     out["gpu_launches_per_step"] = 2
     return out
+
+
+def time_kv_attention(atom, dev, flush_l2, args, B=128, L=1024, H=32):
+    """NEXT-3: one decode step of Llama-7B attention (32 heads x 128) at batch 128
+    (the paper's Fig 8b batch) with 1024 cached tokens per sequence, over the INT4 paged cache;
+    the cache is built (quantized) untimed, the attention timed as a CUDA graph after an L2
+    flush.  Algorithmic bytes: K and V codes + (s, mn) per (token, head) = 2 x 72 B."""
+    import torch
+    rng = np.random.default_rng(args.seed)
+    pages = (L + 15) // 16
+    bt = torch.from_numpy(rng.permutation(B * pages).reshape(B, pages).astype(np.int32)).to(dev)
+    k, v = atom.KvCache.empty(B * pages, H, dev), atom.KvCache.empty(B * pages, H, dev)
+    slots = (bt[:, :, None] * 16 + torch.arange(16, device=dev)).reshape(B, -1)[:, :L].int()
+    gen = torch.Generator(device=dev).manual_seed(args.seed)
+    for b in range(B):
+        x = torch.randn((L, H * 128), device=dev, generator=gen).half()
+        atom.kv_quantize(x, slots[b].contiguous(), k)
+        atom.kv_quantize(x * 0.5, slots[b].contiguous(), v)
+    q = torch.randn((B, H, 128), device=dev, generator=gen).half()
+    sl = torch.full((B,), L, dtype=torch.int32, device=dev)
+    out = atom.decode_attention(q, k, v, bt, sl, L)
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        atom.decode_attention(q, k, v, bt, sl, L, out=out, stream=side)
+        launches = atom.last_launch_count()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            atom.decode_attention(q, k, v, bt, sl, L, out=out, stream=side)
+    torch.cuda.current_stream().wait_stream(side)
+    n = max(5, args.steps // 2)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n)]
+    for i in range(n):
+        if not args.no_flush:
+            flush_l2()
+        ev[i][0].record()
+        g.replay()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    us = 1e3 * sum(a.elapsed_time(b) for a, b in ev) / n
+    nbytes = 2 * B * L * H * (64 + 8)
+    return {"us": us, "GB/s": nbytes / (us * 1e-6) / 1e9, "bytes": nbytes,
+            "shape": {"batch": B, "seq_len": L, "heads": H, "head_dim": 128},
+            "format": "INT4 asymmetric per (token, head), 16-token pages",
+            "gpu_launches_per_step": launches}
 
 
 def _spawn_ranks(args) -> int:
@@ -650,6 +704,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-peak", action="store_true", help="skip the in-run int8 peak measurement")
     ap.add_argument("--no-mx", action="store_true", help="skip the NEXT-2 Atom (FP) MX timing")
+    ap.add_argument("--no-kv", action="store_true", help="skip the NEXT-3 KV attention timing")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--dry-run", action="store_true",
                     help="multi-rank plumbing only (gloo, no GPU work): prints the shard table")
