@@ -144,15 +144,28 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
   };
   const float2* q2 = reinterpret_cast<const float2*>(qv);
 
+  // a warp step's codes and (s, mn), loaded one step ahead (two steps of HBM reads in flight)
+  constexpr int kStep = 8 * (kAttThreads / 32);
+  auto load = [&](const uint8_t* codes, const float* prm, int t0, uint4& w, float2& sm) {
+    if (t0 + tj < c1) {
+      const int64_t v = vec0(t0) + tj;
+      w = __ldg(reinterpret_cast<const uint4*>(codes + v * (kKvD / 2) + 16 * part4));
+      sm = __ldg(reinterpret_cast<const float2*>(prm) + v);
+    }
+  };
+
   // ---- pass 1: scores of the chunk into shared memory ----
   float wmax = -INFINITY;
-  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += 8 * (kAttThreads / 32)) {
+  uint4 wn = make_uint4(0, 0, 0, 0);
+  float2 smn = make_float2(0.0f, 0.0f);
+  load(kc, kp, c0 + 8 * warp, wn, smn);
+  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += kStep) {
     const int t = t0 + tj;
+    const uint4 w = wn;
+    const float2 sm = smn;
+    load(kc, kp, t0 + kStep, wn, smn);
     float part = 0.0f;
     if (t < c1) {
-      const int64_t v = vec0(t0) + tj;
-      const uint4 w = *reinterpret_cast<const uint4*>(kc + v * (kKvD / 2) + 16 * part4);
-      const float2 sm = reinterpret_cast<const float2*>(kp)[v];
       const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
       float2 d2 = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -187,12 +200,13 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
   float psum = 0.0f, pmn = 0.0f;                      // sum p_t, sum p_t mn_t (this lane's tokens)
-  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += 8 * (kAttThreads / 32)) {
+  load(vc, vp, c0 + 8 * warp, wn, smn);
+  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += kStep) {
     const int t = t0 + tj;
+    const uint4 w = wn;
+    const float2 sm = smn;
+    load(vc, vp, t0 + kStep, wn, smn);
     if (t < c1) {
-      const int64_t v = vec0(t0) + tj;
-      const uint4 w = *reinterpret_cast<const uint4*>(vc + v * (kKvD / 2) + 16 * part4);
-      const float2 sm = reinterpret_cast<const float2*>(vp)[v];
       const float p = __expf(sc[t - c0] - cmax);
       const float ps = p * sm.x;
       psum += p;
