@@ -78,7 +78,7 @@
 extern "C" {
 #endif
 
-#define ATOM_ABI_VERSION 5
+#define ATOM_ABI_VERSION 6
 #define ATOM_GROUP 128
 
 typedef enum {
@@ -267,11 +267,15 @@ atom_status_t atom_mx_reorder_quantize(const void* x_f16, int64_t rows, int64_t 
 /* C[m*ldc + n] = fp16( sum_j deq(a[m][j]) * deq(w[n][j]) ), deq = element * 2^shared_exp, on
  * tcgen05 block-scaled MMAs (kind::mxf4 for the FP4 channels, kind::mxf8f6f4 for the outliers)
  * with fp32 accumulation.  Activations [M][..] and weights [N][..] in the formats above (weights
- * quantized with the same perm).  N % 128 == 0, ldc >= N, ldc % 8 == 0, lda_sf / ldw_sf as ldsf. */
+ * quantized with the same perm).  N % 128 == 0, ldc >= N, ldc % 8 == 0, lda_sf / ldw_sf as ldsf.
+ * workspace: atom_mx_gemm_workspace_size bytes (0 unless the output tiles cannot fill the GPU,
+ * when the K loop is split and an fp32 reduction in a fixed order follows). */
 atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uint8_t* a_sf,
                            int64_t lda_sf, const uint8_t* w_fp4, const uint8_t* w_fp8,
                            const uint8_t* w_sf, int64_t ldw_sf, int64_t M, int64_t N, int64_t K,
-                           int32_t k_outlier, void* c_f16, int64_t ldc, void* stream);
+                           int32_t k_outlier, void* c_f16, int64_t ldc, void* workspace,
+                           size_t workspace_bytes, void* stream);
+size_t atom_mx_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier);
 
 /* ------------------------------------------------------------------------------------------
  * Quantized KV cache + decode attention (NEXT-3).  "Atom loads the KV-cache in low-bit

@@ -34,7 +34,7 @@ ABI_SYMBOLS = ("atom_reorder_quantize", "atom_rmsnorm_reorder_quantize",
                "atom_w4a4_gemm", "atom_w4a4_gemm_f8",
                "atom_w4a4_gemm_workspace_size", "atom_w4a4_gemm_f8_workspace_size",
                "atom_w4a4_gemm_counter_bytes",
-               "atom_mx_reorder_quantize", "atom_mx_gemm",
+               "atom_mx_reorder_quantize", "atom_mx_gemm", "atom_mx_gemm_workspace_size",
                "atom_kv_quantize", "atom_decode_attention", "atom_decode_attention_workspace_size",
                "atom_validate_perm", "atom_status_string",
                "atom_abi_version", "atom_last_launch_count")
@@ -78,8 +78,11 @@ def _lib():
         L.atom_w4a4_gemm_counter_bytes.restype = ctypes.c_size_t
         L.atom_mx_reorder_quantize.argtypes = [P, i64, i64, P, i64, i32, P, P, P, i64, P]
         L.atom_mx_reorder_quantize.restype = ctypes.c_int
-        L.atom_mx_gemm.argtypes = [P, P, P, i64, P, P, P, i64, i64, i64, i64, i32, P, i64, P]
+        L.atom_mx_gemm.argtypes = [P, P, P, i64, P, P, P, i64, i64, i64, i64, i32, P, i64, P,
+                                   ctypes.c_size_t, P]
         L.atom_mx_gemm.restype = ctypes.c_int
+        L.atom_mx_gemm_workspace_size.argtypes = [i64, i64, i64, i32]
+        L.atom_mx_gemm_workspace_size.restype = ctypes.c_size_t
         L.atom_kv_quantize.argtypes = [P, i64, i64, i32, i32, P, P, P, P]
         L.atom_kv_quantize.restype = ctypes.c_int
         L.atom_decode_attention.argtypes = [P, i64, i32, i32, P, P, P, P, P, i64, P, i32, P, P,
@@ -443,9 +446,18 @@ def mx_gemm(a: MxQuantized, w: MxQuantized, out=None, stream=None):
     if out.dtype != torch.float16 or out.dim() != 2 or out.stride(1) != 1 or \
             out.shape[0] < M or out.shape[1] < N:
         raise ValueError("out must be an fp16 [M][>=N] tensor with contiguous rows")
+    n = _lib().atom_mx_gemm_workspace_size(M, N, a.K, a.k_outlier)
+    ws = None
+    if n:   # split-K partials; one buffer per (device, stream), grown on demand
+        s = torch.cuda.current_stream() if stream is None else stream
+        key = ("mx", s.device.index, s.cuda_stream)
+        ws = _WORKSPACES.get(key)
+        if ws is None or ws.numel() < n:
+            with torch.cuda.stream(s):
+                ws = _WORKSPACES[key] = torch.empty(n, dtype=torch.uint8, device=s.device)
     st = _lib().atom_mx_gemm(_ptr(a.fp4), _ptr(a.fp8), _ptr(a.sf), a.sf.stride(0), _ptr(w.fp4),
                              _ptr(w.fp8), _ptr(w.sf), w.sf.stride(0), M, N, a.K, a.k_outlier,
-                             _ptr(out), out.stride(0), _stream(stream))
+                             _ptr(out), out.stride(0), _ptr(ws), n, _stream(stream))
     _check(st, "atom_mx_gemm")
     return out
 

@@ -328,7 +328,8 @@ atom_status_t atom_mx_reorder_quantize(const void* x_f16, int64_t rows, int64_t 
 atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uint8_t* a_sf,
                            int64_t lda_sf, const uint8_t* w_fp4, const uint8_t* w_fp8,
                            const uint8_t* w_sf, int64_t ldw_sf, int64_t M, int64_t N, int64_t K,
-                           int32_t k_outlier, void* c_f16, int64_t ldc, void* stream) {
+                           int32_t k_outlier, void* c_f16, int64_t ldc, void* workspace,
+                           size_t workspace_bytes, void* stream) {
   g_last_launches = 0;
   if (M < 0 || N <= 0 || N % 128 != 0) return ATOM_ERR_SHAPE;
   if (!(k_outlier == 0 || k_outlier == ATOM_GROUP)) return ATOM_ERR_ARG;
@@ -362,10 +363,23 @@ atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uin
   a.k_outlier = k_outlier;
   a.c = c_f16;
   a.ldc = ldc;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  const size_t need = atom::mx_gemm_workspace_bytes(M, N, K, k_outlier, dev.num_sms);
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned16(workspace)))
+    return ATOM_ERR_WORKSPACE;
   if (atom::launch_mx_gemm(a, static_cast<cudaStream_t>(stream), dev.num_sms) != cudaSuccess)
     return ATOM_ERR_CUDA;
-  g_last_launches = 1;
+  g_last_launches = need > 0 ? 2 : 1;
   return ATOM_OK;
+}
+
+size_t atom_mx_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int32_t k_outlier) {
+  if (M <= 0 || N <= 0 || N % 128 != 0 || K <= 0 || K % ATOM_GROUP != 0 || K < k_outlier)
+    return 0;
+  DeviceInfo dev;
+  if (current_device(&dev) != ATOM_OK) return 0;
+  return atom::mx_gemm_workspace_bytes(M, N, K, k_outlier, dev.num_sms);
 }
 
 atom_status_t atom_kv_quantize(const void* x_f16, int64_t T, int64_t ldx, int32_t H,

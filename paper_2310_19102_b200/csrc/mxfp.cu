@@ -247,6 +247,8 @@ struct MxParams {
   int has8;        // 1 if the 128 outlier channels (one FP8 stage) are present
   int sf_off8;     // scale-byte column of the first outlier block (= (K - 128) / 32)
   int m_tiles, num_tiles;
+  int ksplit, num_items;   // split-K: item = tile * ksplit + j covers stages [j nst / ksplit, ..)
+  float* part;             // ksplit > 1: fp32 partials [ksplit][M][N]
 };
 
 template <int kTM>
@@ -288,6 +290,8 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const int nst = p.s4 + p.has8;                      // stages per tile
+  auto s_lo = [&](int it) { return (it % p.ksplit) * nst / p.ksplit; };
+  auto s_hi = [&](int it) { return (it % p.ksplit + 1) * nst / p.ksplit; };
   if (threadIdx.x == 0) griddep_launch();
 
   if (warp == 0) {
@@ -296,9 +300,10 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
       const uint64_t pol_a = l2_policy_evict_last(), pol_w = l2_policy_evict_first();
       griddep_wait();
       MxRing<kMxKS> st;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int it = blockIdx.x; it < p.num_items; it += gridDim.x) {
+        const int tile = it / p.ksplit;
         const int m0 = (tile % p.m_tiles) * kMxTM, n0 = (tile / p.m_tiles) * kMxTN;
-        for (int s = 0; s < nst; ++s, st.next()) {
+        for (int s = s_lo(it); s < s_hi(it); ++s, st.next()) {
           mbar_wait(&sm.empty[st.i], st.ph ^ 1);
           mbar_arrive_expect_tx(&sm.full[st.i], (kMxTM + kMxTN) * (128 + 16));
           const bool fp8 = s >= p.s4;
@@ -322,11 +327,12 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
       MxRing<kMxKS> st;
       MxRing<kMxAB> tb;
       uint32_t sfpar = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, tb.next()) {
+      for (int it = blockIdx.x; it < p.num_items; it += gridDim.x, tb.next()) {
         mbar_wait(&sm.tempty[tb.i], tb.ph ^ 1);        // the epilogue drained this buffer
+        const int s0 = s_lo(it);
         tc_fence_after();
         const uint32_t d = tmem + tb.i * (kMxH * kMxTN);   // half h at + h kMxTN
-        for (int s = 0; s < nst; ++s, st.next()) {
+        for (int s = s0; s < s_hi(it); ++s, st.next()) {
           mbar_wait(&sm.full[st.i], st.ph);
           mbar_wait(&sm.sfready[st.i], st.ph);
           tc_fence_after();
@@ -353,7 +359,7 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
               for (int h = 0; h < kMxH; ++h)
                 umma_mxf4(d + h * kMxTN, da + h * (128 * 128 / 16) + 2 * k, db + 2 * k,
                           mx_idesc(kFmtE2M1, 128, kMxTN, id), sfa + 8 * h + 4 * c, sfb + 8 * c,
-                          (s > 0 || k > 0));
+                          (s > s0 || k > 0));
             }
           } else {
             // K = 32 per MMA (32 bytes of E4M3): scale byte k
@@ -362,7 +368,7 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
 #pragma unroll
               for (int h = 0; h < kMxH; ++h)
                 umma_mxf8(d + h * kMxTN, da + h * (128 * 128 / 16) + 2 * k, db + 2 * k,
-                          mx_idesc(kFmtE4M3, 128, kMxTN, k), sfa + 8 * h, sfb, (s > 0 || k > 0));
+                          mx_idesc(kFmtE4M3, 128, kMxTN, k), sfa + 8 * h, sfb, (s > s0 || k > 0));
           }
           umma_commit(&sm.empty[st.i]);
         }
@@ -373,8 +379,8 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
     // ============ scale transposer: canonical [row][bytes] -> tcgen05.cp 32x128b images ============
     // image word 4l + c = the chunk's 4 scale bytes of row 32c + l of the 128-row block
     MxRing<kMxKS> st;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      for (int s = 0; s < nst; ++s, st.next()) {
+    for (int it = blockIdx.x; it < p.num_items; it += gridDim.x) {
+      for (int s = s_lo(it); s < s_hi(it); ++s, st.next()) {
         mbar_wait(&sm.full[st.i], st.ph);
         const bool fp8 = s >= p.s4;
         const int nch = fp8 ? 1 : (s + 1 == p.s4 ? p.ch_last : 2);
@@ -418,7 +424,8 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
     constexpr int kPasses = kMxH == 2 ? 2 : 1;
     griddep_wait();
     MxRing<kMxAB> tb;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, tb.next()) {
+    for (int it = blockIdx.x; it < p.num_items; it += gridDim.x, tb.next()) {
+      const int tile = it / p.ksplit;
       const int m0 = (tile % p.m_tiles) * kMxTM, n0 = (tile / p.m_tiles) * kMxTN;
       mbar_wait(&sm.tfull[tb.i], tb.ph);
       tc_fence_after();
@@ -437,7 +444,20 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.tempty[tb.i]);
         }
-        if (m < p.M) {
+        if (m < p.M && p.ksplit > 1) {   // split-K: the fp32 partial of stages [s_lo, s_hi)
+          float* prow = p.part + (static_cast<int64_t>(it % p.ksplit) * p.M + m) * p.N;
+#pragma unroll
+          for (int cb = 0; cb < 7; ++cb) {
+            const int n = n0 + (kMxH == 2 ? 0 : hf * 112) + 112 * pass + 16 * cb;
+            if (n >= p.N) break;
+            float4* dst = reinterpret_cast<float4*>(prow + n);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_float4(__uint_as_float(r[cb][4 * i]), __uint_as_float(r[cb][4 * i + 1]),
+                                   __uint_as_float(r[cb][4 * i + 2]),
+                                   __uint_as_float(r[cb][4 * i + 3]));
+          }
+        } else if (m < p.M) {
 #pragma unroll
           for (int cb = 0; cb < 7; ++cb) {
             const int n = n0 + (kMxH == 2 ? 0 : hf * 112) + 112 * pass + 16 * cb;
@@ -463,6 +483,49 @@ mx_gemm_kernel(const __grid_constant__ CUtensorMap tm_a4, const __grid_constant_
     tc_fence_after();
     tmem_dealloc(tmem, kMxTmemCols);
   }
+}
+
+// split-K reduction: C[m][n] = fp16(sum_j part[j][m][n]), j ascending (deterministic)
+__global__ void __launch_bounds__(256)
+mx_splitk_reduce_kernel(const float* __restrict__ part, int32_t ksplit, int64_t M, int64_t N,
+                        __half* __restrict__ c, int64_t ldc) {
+  griddep_wait();
+  griddep_launch();
+  const int64_t n4 = N / 4, total = M * n4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = i / n4, n = 4 * (i % n4);
+    float4 acc = reinterpret_cast<const float4*>(part + m * N + n)[0];
+    for (int j = 1; j < ksplit; ++j) {
+      const float4 v = reinterpret_cast<const float4*>(part + (j * M + m) * N + n)[0];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    const __half2 lo = __floats2half2_rn(acc.x, acc.y), hi = __floats2half2_rn(acc.z, acc.w);
+    uint2 o;
+    o.x = *reinterpret_cast<const uint32_t*>(&lo);
+    o.y = *reinterpret_cast<const uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(c + m * ldc + n) = o;
+  }
+}
+
+// Split-K factor: when the output tiles cannot fill the SMs, the K stages of a tile are divided
+// among ksplit CTAs (at least 4 stages each) and an fp32 reduction follows.
+static int mx_ksplit(int64_t tiles, int nst, int num_sms) {
+  if (tiles * 2 > num_sms) return 1;
+  int k = static_cast<int>(num_sms / tiles);
+  if (k > nst / 4) k = nst / 4;
+  return k < 1 ? 1 : k;
+}
+
+size_t mx_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int32_t k_outlier, int num_sms) {
+  const int64_t K4 = K - k_outlier, chunks = K4 / 128;
+  const int nst = static_cast<int>((chunks + 1) / 2) + (k_outlier ? 1 : 0);
+  const int64_t tiles = ((M + 127) / 128) * ((N + kMxTN - 1) / kMxTN);   // small shapes: 128-token tiles
+  const int ks = mx_ksplit(tiles, nst, num_sms);
+  return ks > 1 ? static_cast<size_t>(ks) * M * N * sizeof(float) : 0;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -509,6 +572,11 @@ cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms
     return static_cast<double>((t + num_sms - 1) / num_sms) * (tm + kMxTN) * f;
   };
   const int tm = cost(256, 1.1) < cost(128, 1.0) ? 256 : 128;
+  const int nst_h = static_cast<int>((K4 / 128 + 1) / 2) + (a.k_outlier ? 1 : 0);
+  const int ksplit = tm == 128 ? mx_ksplit(((a.M + 127) / 128) * n_tiles, nst_h, num_sms) : 1;
+  if (ksplit > 1 && (a.workspace == nullptr ||
+                     a.workspace_bytes < static_cast<size_t>(ksplit) * a.M * a.N * sizeof(float)))
+    return cudaErrorInvalidValue;
   CUtensorMap m_a4, m_b4, m_a8, m_b8, m_asf, m_bsf;
   // an absent operand (no FP4 channels / no outliers) aliases the other one and is never read
   const void* a4 = K4 ? a.a_fp4 : any;
@@ -536,7 +604,10 @@ cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms
   p.sf_off8 = static_cast<int>(K4 / 32);
   p.m_tiles = static_cast<int>((a.M + tm - 1) / tm);
   p.num_tiles = p.m_tiles * static_cast<int>(n_tiles);
-  const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+  p.ksplit = ksplit;
+  p.num_items = p.num_tiles * ksplit;
+  p.part = static_cast<float*>(a.workspace);
+  const int grid = p.num_items < num_sms ? p.num_items : num_sms;
   auto go = [&](auto tm_tag) -> cudaError_t {
     constexpr int kTM = decltype(tm_tag)::value;
     const size_t smem = sizeof(MxSmem<MxCfg<kTM>>) + 1024;
@@ -556,6 +627,14 @@ cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms
   cudaError_t e = tm == 256 ? go(std::integral_constant<int, 256>{})
                             : go(std::integral_constant<int, 128>{});
   if (e != cudaSuccess) return e;
+  if (ksplit > 1) {
+    int64_t blocks = (a.M * a.N / 4 + 255) / 256;
+    if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
+    e = launch_pdl(mx_splitk_reduce_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0,
+                   stream, static_cast<const float*>(a.workspace), ksplit, a.M, a.N,
+                   static_cast<__half*>(a.c), a.ldc);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

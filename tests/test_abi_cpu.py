@@ -53,7 +53,7 @@ def test_sm100a_only_cubin():
 
 
 def test_version_and_status_strings(lib):
-    assert lib.atom_abi_version() == 5
+    assert lib.atom_abi_version() == 6
     for s in range(8):
         assert lib.atom_status_string(s).startswith(b"ATOM_")
 

@@ -83,6 +83,8 @@ def test_mx_quantize_adversarial(atom):
     (300, 4096, 4096, 128),  # config 2 shape family
     (512, 13824, 5120, 128), # config 4: 256-token tiles (two MMA halves), ragged channel tile
     (1000, 28672, 1024, 128),  # 256-token tiles, ragged token tail
+    (8, 4096, 11008, 128),   # split-K over 7 CTAs per tile (19 tiles), fp32 reduction
+    (64, 11008, 4096, 0),    # split-K 2, pure MXFP4
 ])
 def test_mx_gemm_vs_oracle(atom, M, N, K, k_o):
     import torch
