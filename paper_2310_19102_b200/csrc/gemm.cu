@@ -61,7 +61,7 @@ constexpr int kNumEpiWarps = 8;
 constexpr int kEpiThreads = kNumEpiWarps * 32;
 constexpr int kRegsProd = 24, kRegsUnpack = 48, kRegsHigh = 216;   // 128*(24+48) + 256*216 <= 65536
 #ifndef ATOM_SWAP_MAX_M
-#define ATOM_SWAP_MAX_M 128
+#define ATOM_SWAP_MAX_M 64
 #endif
 #ifndef ATOM_RW
 #define ATOM_RW 2
@@ -1183,8 +1183,9 @@ static cudaError_t set_smem_attr(size_t smem) {
 
 // Tile plan: one persistent CTA per SM (or per unit, if fewer); whole tiles in round-robin waves
 // while at least two waves remain, then the rest as evenly divided (tile, group) units.
-// Small M (<= ATOM_SWAP_MAX_M = 128 tokens) takes the swap-AB tile of kBT = 16 / 32 / 64 tokens x
-// 128 channels (M in (64, 128]: two 64-token tiles, 5-10% faster than one 128 x 256 tile there).
+// Small M (<= ATOM_SWAP_MAX_M = 64 tokens) takes the swap-AB tile of kBT = 16 / 32 / 64 tokens x
+// 128 channels (at M = 128, two 64-token tiles measured mixed in the L2-cold sweep: down
+// projection 45 -> 41 us, up/gate 39 -> 43 us; not used).
 GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms, bool split_free) {
   GemmPlan pl;
   const int64_t G = K / 128;
