@@ -8,6 +8,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import paper_2310_19102_b200 as atom  # noqa: E402
 
+if len(sys.argv) > 2:
+    atom.LIB_PATH = Path(sys.argv[2])
 for arg in sys.argv[1].split(";"):
     B, L, H = (int(v) for v in arg.split(","))
     rng = np.random.default_rng(0)
