@@ -103,6 +103,45 @@ def test_silu_mul_quantize_host_validation(lib):
     assert lib.atom_last_launch_count() == 0
 
 
+def test_mx_and_kv_host_validation(lib):
+    """NEXT-2 / NEXT-3 entry points: shape, argument and NULL errors are decided on the host
+    before any device query; empty batches are no-ops."""
+    # atom_mx_reorder_quantize(x, rows, ldx, perm, K, k_o, fp4, fp8, sf, ldsf, stream)
+    q = lib.atom_mx_reorder_quantize
+    assert q(None, 4, 256, None, 200, 128, None, None, None, 16, None) == 2      # K % 128
+    assert q(None, 4, 256, None, 256, 64, None, None, None, 16, None) == 4       # k_outlier
+    assert q(None, 4, 256, None, 256, 128, None, None, None, 4, None) == 2       # ldsf < K/32
+    assert q(None, 4, 256, None, 256, 128, None, None, None, 16, None) == 1      # NULLs
+    assert q(None, 0, 256, None, 256, 128, None, None, None, 16, None) == 0
+    # atom_mx_gemm(a4, a8, asf, lda_sf, w4, w8, wsf, ldw_sf, M, N, K, k_o, c, ldc, ws, wsb, st)
+    g = lib.atom_mx_gemm
+    assert g(None, None, None, 16, None, None, None, 16, 4, 100, 256, 128, None, 128, None, 0,
+             None) == 2                                                          # N % 128
+    assert g(None, None, None, 16, None, None, None, 16, 4, 128, 256, 128, None, 100, None, 0,
+             None) == 2                                                          # ldc < N
+    assert g(None, None, None, 16, None, None, None, 16, 4, 128, 256, 128, None, 128, None, 0,
+             None) == 1
+    assert g(None, None, None, 16, None, None, None, 16, 0, 128, 256, 128, None, 128, None, 0,
+             None) == 0
+    assert lib.atom_mx_gemm_workspace_size(8, 4096, 11008, 128) == 0            # no device here
+    # atom_kv_quantize(x, T, ldx, H, d, slots, codes, params, stream)
+    k = lib.atom_kv_quantize
+    assert k(None, 4, 256, 2, 64, None, None, None, None) == 2                  # head_dim 128 only
+    assert k(None, 4, 200, 2, 128, None, None, None, None) == 2                 # ldx < 128 H
+    assert k(None, 4, 256, 2, 128, None, None, None, None) == 1
+    assert k(None, 0, 256, 2, 128, None, None, None, None) == 0
+    # atom_decode_attention(q, B, H, d, kc, kp, vc, vp, bt, max_pages, lens, max_len, out, ws,
+    # wsb, stream)
+    a = lib.atom_decode_attention
+    assert a(None, 2, 4, 128, None, None, None, None, None, 2, None, 40, None, None, 0,
+             None) == 2                                                          # 40 > 16 * 2
+    assert a(None, 2, 4, 128, None, None, None, None, None, 4, None, 40, None, None, 0,
+             None) == 1
+    assert a(None, 0, 4, 128, None, None, None, None, None, 4, None, 40, None, None, 0,
+             None) == 0
+    assert lib.atom_last_launch_count() == 0
+
+
 def test_bench_gpus_2_spawns_two_ranks_dry_run():
     """`python bench.py --gpus 2` (the driver's launch form) starts two ranks itself (torchrun on
     127.0.0.1); --dry-run exercises that rank plumbing with gloo on CPU: both ranks report their
