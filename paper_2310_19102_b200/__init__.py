@@ -428,6 +428,17 @@ def mx_quantize(x, perm, K: Optional[int] = None, k_outlier: int = 128, out=None
         fp8 = torch.empty((rows, k_outlier), dtype=torch.uint8, device=dev) if k_outlier else None
         sf = torch.zeros((rows, ldsf), dtype=torch.uint8, device=dev)
         out = MxQuantized(fp4, fp8, sf, K, k_outlier)
+    else:   # a caller-supplied operand must have this call's shapes (the ABI checks only ldsf)
+        want = [(out.fp4, (rows, (K - k_outlier) // 2) if K > k_outlier else None),
+                (out.fp8, (rows, k_outlier) if k_outlier else None)]
+        for t, shape in want:
+            if (t is None) != (shape is None) or (t is not None and (
+                    tuple(t.shape) != shape or t.dtype != torch.uint8 or not t.is_contiguous()
+                    or t.device != x.device)):
+                raise ValueError("out does not match this call's rows / K / k_outlier")
+        if out.K != K or out.k_outlier != k_outlier or out.sf.shape[0] != rows or \
+                out.sf.stride(0) < K // MX_BLOCK or out.sf.device != x.device:
+            raise ValueError("out.sf does not match this call's rows / K")
     st = _lib().atom_mx_reorder_quantize(_ptr(x), rows, ldx, _ptr(perm), K, k_outlier,
                                          _ptr(out.fp4), _ptr(out.fp8), _ptr(out.sf),
                                          out.sf.stride(0), _stream(stream))
