@@ -1201,6 +1201,14 @@ GemmPlan plan_w4a4_gemm(int64_t M, int64_t N, int64_t K, int num_sms, bool split
   }
   const int64_t units = pl.num_tiles * G;
   pl.grid = static_cast<int>(units < num_sms ? units : num_sms);
+  // fewer tiles than SMs: a grid of a whole multiple of the tile count (when it keeps >= 85% of
+  // the SMs), so every tile is cut into the same number of equal K segments -- each segment then
+  // has one publisher role or one reducer role instead of straddling two tiles (cfg2 23.4 ->
+  // 20.6 us, M = 128 up/gate 24.9 -> 22.3 us, graph-replayed)
+  if (!split_free && pl.num_tiles < num_sms && pl.num_tiles * G >= num_sms) {
+    const int64_t even = pl.num_tiles * (num_sms / pl.num_tiles);
+    if (even * 100 >= 85LL * num_sms) pl.grid = static_cast<int>(even);
+  }
   const int64_t T = pl.num_tiles, P = pl.grid;
   if (T % P == 0) pl.dp_waves = static_cast<int>(T / P);
   else if (T >= 2 * P) pl.dp_waves = static_cast<int>(T / P - 1);
