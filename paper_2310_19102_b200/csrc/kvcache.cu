@@ -138,51 +138,72 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
 #pragma unroll
   for (int i = 0; i < 32; ++i) qsum += qv[i];
   const int32_t* bt = block_table + static_cast<int64_t>(b) * max_pages;
-  // the 8 tokens t0 .. t0+7 of a warp step lie in one page (t0 % 8 == 0): one table lookup
+  // the 16 tokens t0 .. t0+15 of a warp step lie in one page (t0 % 16 == 0): one table lookup
   auto vec0 = [&](int t0) {                           // (page, head, offset) index of token t0
     return (static_cast<int64_t>(__ldg(bt + t0 / kKvPage)) * H + h) * kKvPage + t0 % kKvPage;
   };
   const float2* q2 = reinterpret_cast<const float2*>(qv);
 
-  // a warp step's codes and (s, mn), loaded one step ahead (two steps of HBM reads in flight)
-  constexpr int kStep = 8 * (kAttThreads / 32);
-  auto load = [&](const uint8_t* codes, const float* prm, int t0, uint4& w, float2& sm) {
-    if (t0 + tj < c1) {
-      const int64_t v = vec0(t0) + tj;
-      w = __ldg(reinterpret_cast<const uint4*>(codes + v * (kKvD / 2) + 16 * part4));
-      sm = __ldg(reinterpret_cast<const float2*>(prm) + v);
+  // A warp step covers 16 tokens of one page: lane (tj, part4) takes tokens t0 + tj and
+  // t0 + 8 + tj (two independent loads and FMA chains per lane); every step's codes and (s, mn)
+  // are loaded one step ahead.
+  constexpr int kTpl = 2;                             // tokens per lane per step
+  constexpr int kStep = 8 * kTpl * (kAttThreads / 32);
+  auto load = [&](const uint8_t* codes, const float* prm, int t0, uint4 (&w)[kTpl],
+                  float2 (&sm)[kTpl]) {
+    if (t0 < c1) {
+      const int64_t v0 = vec0(t0) + tj;
+#pragma unroll
+      for (int u = 0; u < kTpl; ++u)
+        if (t0 + 8 * u + tj < c1) {
+          const int64_t v = v0 + 8 * u;
+          w[u] = __ldg(reinterpret_cast<const uint4*>(codes + v * (kKvD / 2) + 16 * part4));
+          sm[u] = __ldg(reinterpret_cast<const float2*>(prm) + v);
+        }
     }
   };
 
   // ---- pass 1: scores of the chunk into shared memory ----
   float wmax = -INFINITY;
-  uint4 wn = make_uint4(0, 0, 0, 0);
-  float2 smn = make_float2(0.0f, 0.0f);
-  load(kc, kp, c0 + 8 * warp, wn, smn);
-  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += kStep) {
-    const int t = t0 + tj;
-    const uint4 w = wn;
-    const float2 sm = smn;
-    load(kc, kp, t0 + kStep, wn, smn);
-    float part = 0.0f;
-    if (t < c1) {
-      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-      float2 d2 = make_float2(0.0f, 0.0f);
+  uint4 wn[kTpl] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  float2 smn[kTpl] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+  load(kc, kp, c0 + 16 * warp, wn, smn);
+  for (int t0 = c0 + 16 * warp; t0 < c1; t0 += kStep) {
+    uint4 w[kTpl];
+    float2 sm[kTpl];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float2 c[4];
-        code_pairs(ww[i], c);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) d2 = __ffma2_rn(q2[4 * i + k], c[k], d2);
-      }
-      part = fmaf(sm.x, d2.x + d2.y, sm.y * qsum);
+    for (int u = 0; u < kTpl; ++u) {
+      w[u] = wn[u];
+      sm[u] = smn[u];
     }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    if (t < c1) {
-      const float score = part * kRsqrtD;
-      if (part4 == 0) sc[t - c0] = score;
-      wmax = fmaxf(wmax, score);
+    load(kc, kp, t0 + kStep, wn, smn);
+    float part[kTpl];
+#pragma unroll
+    for (int u = 0; u < kTpl; ++u) {
+      part[u] = 0.0f;
+      if (t0 + 8 * u + tj < c1) {
+        const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+        float2 d2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float2 c[4];
+          code_pairs(ww[i], c);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) d2 = __ffma2_rn(q2[4 * i + k], c[k], d2);
+        }
+        part[u] = fmaf(sm[u].x, d2.x + d2.y, sm[u].y * qsum);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kTpl; ++u) {
+      part[u] += __shfl_xor_sync(0xffffffffu, part[u], 1);
+      part[u] += __shfl_xor_sync(0xffffffffu, part[u], 2);
+      const int t = t0 + 8 * u + tj;
+      if (t < c1) {
+        const float score = part[u] * kRsqrtD;
+        if (part4 == 0) sc[t - c0] = score;
+        wmax = fmaxf(wmax, score);
+      }
     }
   }
 #pragma unroll
@@ -200,25 +221,33 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
   float psum = 0.0f, pmn = 0.0f;                      // sum p_t, sum p_t mn_t (this lane's tokens)
-  load(vc, vp, c0 + 8 * warp, wn, smn);
-  for (int t0 = c0 + 8 * warp; t0 < c1; t0 += kStep) {
-    const int t = t0 + tj;
-    const uint4 w = wn;
-    const float2 sm = smn;
+  load(vc, vp, c0 + 16 * warp, wn, smn);
+  for (int t0 = c0 + 16 * warp; t0 < c1; t0 += kStep) {
+    uint4 w[kTpl];
+    float2 sm[kTpl];
+#pragma unroll
+    for (int u = 0; u < kTpl; ++u) {
+      w[u] = wn[u];
+      sm[u] = smn[u];
+    }
     load(vc, vp, t0 + kStep, wn, smn);
-    if (t < c1) {
-      const float p = __expf(sc[t - c0] - cmax);
-      const float ps = p * sm.x;
-      psum += p;
-      pmn = fmaf(p, sm.y, pmn);
-      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-      const float2 ps2 = make_float2(ps, ps);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float2 c[4];
-        code_pairs(ww[i], c);
+    for (int u = 0; u < kTpl; ++u) {
+      const int t = t0 + 8 * u + tj;
+      if (t < c1) {
+        const float p = __expf(sc[t - c0] - cmax);
+        const float ps = p * sm[u].x;
+        psum += p;
+        pmn = fmaf(p, sm[u].y, pmn);
+        const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+        const float2 ps2 = make_float2(ps, ps);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc2[4 * i + k] = __ffma2_rn(ps2, c[k], acc2[4 * i + k]);
+        for (int i = 0; i < 4; ++i) {
+          float2 c[4];
+          code_pairs(ww[i], c);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc2[4 * i + k] = __ffma2_rn(ps2, c[k], acc2[4 * i + k]);
+        }
       }
     }
   }
