@@ -559,44 +559,37 @@ static bool mx_map(CUtensorMap* map, const void* base, uint64_t cols, uint64_t l
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms) {
-  if (a.M == 0) return cudaSuccess;
+// One launch over the output columns [n_off, n_end) with token tile tm (split-K only when
+// ksplit > 1, which implies the whole range [0, N)).
+static cudaError_t launch_mx_cols(const MxGemmArgs& a, cudaStream_t stream, int num_sms, int tm,
+                                  int64_t n_off, int64_t n_end, int ksplit) {
   const int64_t K4 = a.K - a.k_outlier;
   const void* any = K4 ? static_cast<const void*>(a.a_fp4) : static_cast<const void*>(a.a_fp8);
   const void* anyw = K4 ? static_cast<const void*>(a.w_fp4) : static_cast<const void*>(a.w_fp8);
-  // token tile: the one with fewer (waves x operand bytes into the SM per stage); the 256-row
-  // tile pays ~10% for its single accumulator buffer
-  const int64_t n_tiles = (a.N + kMxTN - 1) / kMxTN;
-  auto cost = [&](int tm, double f) {
-    const int64_t t = ((a.M + tm - 1) / tm) * n_tiles;
-    return static_cast<double>((t + num_sms - 1) / num_sms) * (tm + kMxTN) * f;
-  };
-  const int tm = cost(256, 1.1) < cost(128, 1.0) ? 256 : 128;
-  const int nst_h = static_cast<int>((K4 / 128 + 1) / 2) + (a.k_outlier ? 1 : 0);
-  const int ksplit = tm == 128 ? mx_ksplit(((a.M + 127) / 128) * n_tiles, nst_h, num_sms) : 1;
-  if (ksplit > 1 && (a.workspace == nullptr ||
-                     a.workspace_bytes < static_cast<size_t>(ksplit) * a.M * a.N * sizeof(float)))
-    return cudaErrorInvalidValue;
+  const int64_t N = n_end - n_off;
+  const int64_t n_tiles = (N + kMxTN - 1) / kMxTN;
   CUtensorMap m_a4, m_b4, m_a8, m_b8, m_asf, m_bsf;
   // an absent operand (no FP4 channels / no outliers) aliases the other one and is never read
   const void* a4 = K4 ? a.a_fp4 : any;
-  const void* b4 = K4 ? a.w_fp4 : anyw;
   const void* a8 = a.k_outlier ? a.a_fp8 : any;
-  const void* b8 = a.k_outlier ? a.w_fp8 : anyw;
   const uint64_t c4 = K4 ? K4 / 2 : 128, c8 = a.k_outlier ? 128 : K4 / 2;
   const uint64_t nsf = a.K / 32;
+  // weight rows (and their scale rows) from n_off on: every row pitch is a multiple of 16 bytes
+  const uint8_t* b4 = static_cast<const uint8_t*>(K4 ? a.w_fp4 : anyw) + n_off * c4;
+  const uint8_t* b8 = static_cast<const uint8_t*>(a.k_outlier ? a.w_fp8 : anyw) + n_off * c8;
+  const uint8_t* bsf = a.w_sf + n_off * a.ldw_sf;
   if (!mx_map(&m_a4, a4, c4, c4, a.M, 128, tm, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !mx_map(&m_b4, b4, c4, c4, a.N, 128, kMxTN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !mx_map(&m_b4, b4, c4, c4, N, 128, kMxTN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !mx_map(&m_a8, a8, c8, c8, a.M, 128, tm, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !mx_map(&m_b8, b8, c8, c8, a.N, 128, kMxTN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !mx_map(&m_b8, b8, c8, c8, N, 128, kMxTN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !mx_map(&m_asf, a.a_sf, nsf, a.lda_sf, a.M, 16, tm, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !mx_map(&m_bsf, a.w_sf, nsf, a.ldw_sf, a.N, 16, kMxTN, CU_TENSOR_MAP_SWIZZLE_NONE))
+      !mx_map(&m_bsf, bsf, nsf, a.ldw_sf, N, 16, kMxTN, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   MxParams p;
-  p.c = a.c;
+  p.c = static_cast<__half*>(a.c) + n_off;
   p.ldc = a.ldc;
   p.M = static_cast<int>(a.M);
-  p.N = static_cast<int>(a.N);
+  p.N = static_cast<int>(N);
   const int64_t chunks = K4 / 128;
   p.s4 = static_cast<int>((chunks + 1) / 2);
   p.ch_last = (chunks % 2) ? 1 : 2;
@@ -636,6 +629,41 @@ cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms) {
+  if (a.M == 0) return cudaSuccess;
+  const int64_t K4 = a.K - a.k_outlier;
+  // token tile: the one with fewer (waves x operand bytes into the SM per stage); the 256-row
+  // tile pays ~10% for its single accumulator buffer
+  const int64_t n_tiles = (a.N + kMxTN - 1) / kMxTN;
+  auto waves = [&](int64_t t) { return (t + num_sms - 1) / num_sms; };
+  auto cost = [&](int tm, double f) {
+    return static_cast<double>(waves(((a.M + tm - 1) / tm) * n_tiles)) * (tm + kMxTN) * f;
+  };
+  const int tm = cost(256, 1.1) < cost(128, 1.0) ? 256 : 128;
+  const int nst_h = static_cast<int>((K4 / 128 + 1) / 2) + (a.k_outlier ? 1 : 0);
+  const int ksplit = tm == 128 ? mx_ksplit(((a.M + 127) / 128) * n_tiles, nst_h, num_sms) : 1;
+  if (ksplit > 1 && (a.workspace == nullptr ||
+                     a.workspace_bytes < static_cast<size_t>(ksplit) * a.M * a.N * sizeof(float)))
+    return cudaErrorInvalidValue;
+  if (tm == 256) {
+    // wave tail: the 256-row tiles fill whole waves over the first n_full weight-column tiles;
+    // the remaining columns go to a second launch of 128-row tiles (twice the tiles, each ~2/3
+    // of the time of a 256-row tile), when that costs less than the partial last wave
+    const int64_t m256 = (a.M + 255) / 256, m128 = (a.M + 127) / 128;
+    const int64_t n_full = (waves(m256 * n_tiles) - 1) * num_sms / m256;
+    if (n_full > 0 && n_full < n_tiles) {
+      const double split = static_cast<double>(waves(m256 * n_full)) * (256 + kMxTN) * 1.1 +
+                           static_cast<double>(waves(m128 * (n_tiles - n_full))) * (128 + kMxTN);
+      if (split < 0.97 * cost(256, 1.1)) {
+        cudaError_t e = launch_mx_cols(a, stream, num_sms, 256, 0, n_full * kMxTN, 1);
+        if (e != cudaSuccess) return e;
+        return launch_mx_cols(a, stream, num_sms, 128, n_full * kMxTN, a.N, 1);
+      }
+    }
+  }
+  return launch_mx_cols(a, stream, num_sms, tm, 0, a.N, ksplit);
 }
 
 }  // namespace atom

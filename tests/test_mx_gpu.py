@@ -85,6 +85,8 @@ def test_mx_quantize_adversarial(atom):
     (1000, 28672, 1024, 128),  # 256-token tiles, ragged token tail
     (8, 4096, 11008, 128),   # split-K over 7 CTAs per tile (19 tiles), fp32 reduction
     (64, 11008, 4096, 0),    # split-K 2, pure MXFP4
+    (1024, 28672, 256, 128),   # wave tail: 256-token tiles over 111 column tiles, then 128-token
+    (4096, 4096, 512, 0),      # tiles over the rest (second launch); 18 + 1 column tiles
 ])
 def test_mx_gemm_vs_oracle(atom, M, N, K, k_o):
     import torch
