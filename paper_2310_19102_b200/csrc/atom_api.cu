@@ -370,7 +370,7 @@ atom_status_t atom_mx_gemm(const uint8_t* a_fp4, const uint8_t* a_fp8, const uin
     return ATOM_ERR_WORKSPACE;
   if (atom::launch_mx_gemm(a, static_cast<cudaStream_t>(stream), dev.num_sms) != cudaSuccess)
     return ATOM_ERR_CUDA;
-  g_last_launches = need > 0 ? 2 : 1;
+  g_last_launches = atom::mx_gemm_launches(M, N, K, k_outlier, dev.num_sms);
   return ATOM_OK;
 }
 

@@ -109,6 +109,7 @@ struct MxGemmArgs {
 };
 cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms);
 size_t mx_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int32_t k_outlier, int num_sms);
+int mx_gemm_launches(int64_t M, int64_t N, int64_t K, int32_t k_outlier, int num_sms);
 
 // NEXT-3: quantized paged KV cache + decode attention (kvcache.cu, include/atom.h "KV cache")
 cudaError_t launch_kv_quantize(const void* x, int64_t T, int64_t ldx, int32_t H,

@@ -520,12 +520,48 @@ static int mx_ksplit(int64_t tiles, int nst, int num_sms) {
   return k < 1 ? 1 : k;
 }
 
+// Launch plan.  Token tile: the one with fewer (waves x operand bytes into the SM per stage); the
+// 256-row tile pays ~10% for its single accumulator buffer.  Small shapes: split-K over 128-row
+// tiles.  Wave tail: when the 256-row tiles leave a partial last wave, they cover only the first
+// n_full column tiles (whole waves) and a second launch covers the rest with 128-row tiles
+// (twice the tiles, each ~2/3 of the time).  Split-K of the tail's 256-row tiles instead was
+// measured slower (cfg5 149.8 vs 137.1 us).
+struct MxPlan {
+  int tm, ksplit;
+  int64_t n_full;          // column tiles of the first launch (== all of them: one launch)
+};
+static MxPlan mx_plan(int64_t M, int64_t N, int64_t K, int32_t k_o, int num_sms) {
+  const int64_t K4 = K - k_o;
+  const int nst = static_cast<int>((K4 / 128 + 1) / 2) + (k_o ? 1 : 0);
+  const int64_t n_tiles = (N + kMxTN - 1) / kMxTN;
+  auto waves = [&](int64_t t) { return (t + num_sms - 1) / num_sms; };
+  auto cost = [&](int tm, double f) {
+    return static_cast<double>(waves(((M + tm - 1) / tm) * n_tiles)) * (tm + kMxTN) * f;
+  };
+  MxPlan pl;
+  pl.tm = cost(256, 1.1) < cost(128, 1.0) ? 256 : 128;
+  pl.ksplit = pl.tm == 128 ? mx_ksplit(((M + 127) / 128) * n_tiles, nst, num_sms) : 1;
+  pl.n_full = n_tiles;
+  if (pl.tm == 256) {
+    const int64_t m256 = (M + 255) / 256, m128 = (M + 127) / 128;
+    const int64_t nf = (waves(m256 * n_tiles) - 1) * num_sms / m256;
+    if (nf > 0 && nf < n_tiles) {
+      const double split = static_cast<double>(waves(m256 * nf)) * (256 + kMxTN) * 1.1 +
+                           static_cast<double>(waves(m128 * (n_tiles - nf))) * (128 + kMxTN);
+      if (split < 0.97 * cost(256, 1.1)) pl.n_full = nf;
+    }
+  }
+  return pl;
+}
+
+int mx_gemm_launches(int64_t M, int64_t N, int64_t K, int32_t k_outlier, int num_sms) {
+  const MxPlan pl = mx_plan(M, N, K, k_outlier, num_sms);
+  return 1 + (pl.ksplit > 1) + (pl.n_full * kMxTN < N ? 1 : 0);
+}
+
 size_t mx_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int32_t k_outlier, int num_sms) {
-  const int64_t K4 = K - k_outlier, chunks = K4 / 128;
-  const int nst = static_cast<int>((chunks + 1) / 2) + (k_outlier ? 1 : 0);
-  const int64_t tiles = ((M + 127) / 128) * ((N + kMxTN - 1) / kMxTN);   // small shapes: 128-token tiles
-  const int ks = mx_ksplit(tiles, nst, num_sms);
-  return ks > 1 ? static_cast<size_t>(ks) * M * N * sizeof(float) : 0;
+  const MxPlan pl = mx_plan(M, N, K, k_outlier, num_sms);
+  return pl.ksplit > 1 ? static_cast<size_t>(pl.ksplit) * M * N * sizeof(float) : 0;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -568,6 +604,9 @@ static cudaError_t launch_mx_cols(const MxGemmArgs& a, cudaStream_t stream, int 
   const void* anyw = K4 ? static_cast<const void*>(a.w_fp4) : static_cast<const void*>(a.w_fp8);
   const int64_t N = n_end - n_off;
   const int64_t n_tiles = (N + kMxTN - 1) / kMxTN;
+  if (ksplit > 1 && (a.workspace == nullptr ||
+                     a.workspace_bytes < static_cast<size_t>(ksplit) * a.M * N * sizeof(float)))
+    return cudaErrorInvalidValue;
   CUtensorMap m_a4, m_b4, m_a8, m_b8, m_asf, m_bsf;
   // an absent operand (no FP4 channels / no outliers) aliases the other one and is never read
   const void* a4 = K4 ? a.a_fp4 : any;
@@ -621,11 +660,11 @@ static cudaError_t launch_mx_cols(const MxGemmArgs& a, cudaStream_t stream, int 
                             : go(std::integral_constant<int, 128>{});
   if (e != cudaSuccess) return e;
   if (ksplit > 1) {
-    int64_t blocks = (a.M * a.N / 4 + 255) / 256;
+    int64_t blocks = (a.M * N / 4 + 255) / 256;
     if (blocks > 4LL * num_sms) blocks = 4LL * num_sms;
     e = launch_pdl(mx_splitk_reduce_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0,
-                   stream, static_cast<const float*>(a.workspace), ksplit, a.M, a.N,
-                   static_cast<__half*>(a.c), a.ldc);
+                   stream, static_cast<const float*>(a.workspace), ksplit, a.M, N,
+                   static_cast<__half*>(a.c) + n_off, a.ldc);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -633,37 +672,11 @@ static cudaError_t launch_mx_cols(const MxGemmArgs& a, cudaStream_t stream, int 
 
 cudaError_t launch_mx_gemm(const MxGemmArgs& a, cudaStream_t stream, int num_sms) {
   if (a.M == 0) return cudaSuccess;
-  const int64_t K4 = a.K - a.k_outlier;
-  // token tile: the one with fewer (waves x operand bytes into the SM per stage); the 256-row
-  // tile pays ~10% for its single accumulator buffer
-  const int64_t n_tiles = (a.N + kMxTN - 1) / kMxTN;
-  auto waves = [&](int64_t t) { return (t + num_sms - 1) / num_sms; };
-  auto cost = [&](int tm, double f) {
-    return static_cast<double>(waves(((a.M + tm - 1) / tm) * n_tiles)) * (tm + kMxTN) * f;
-  };
-  const int tm = cost(256, 1.1) < cost(128, 1.0) ? 256 : 128;
-  const int nst_h = static_cast<int>((K4 / 128 + 1) / 2) + (a.k_outlier ? 1 : 0);
-  const int ksplit = tm == 128 ? mx_ksplit(((a.M + 127) / 128) * n_tiles, nst_h, num_sms) : 1;
-  if (ksplit > 1 && (a.workspace == nullptr ||
-                     a.workspace_bytes < static_cast<size_t>(ksplit) * a.M * a.N * sizeof(float)))
-    return cudaErrorInvalidValue;
-  if (tm == 256) {
-    // wave tail: the 256-row tiles fill whole waves over the first n_full weight-column tiles;
-    // the remaining columns go to a second launch of 128-row tiles (twice the tiles, each ~2/3
-    // of the time of a 256-row tile), when that costs less than the partial last wave
-    const int64_t m256 = (a.M + 255) / 256, m128 = (a.M + 127) / 128;
-    const int64_t n_full = (waves(m256 * n_tiles) - 1) * num_sms / m256;
-    if (n_full > 0 && n_full < n_tiles) {
-      const double split = static_cast<double>(waves(m256 * n_full)) * (256 + kMxTN) * 1.1 +
-                           static_cast<double>(waves(m128 * (n_tiles - n_full))) * (128 + kMxTN);
-      if (split < 0.97 * cost(256, 1.1)) {
-        cudaError_t e = launch_mx_cols(a, stream, num_sms, 256, 0, n_full * kMxTN, 1);
-        if (e != cudaSuccess) return e;
-        return launch_mx_cols(a, stream, num_sms, 128, n_full * kMxTN, a.N, 1);
-      }
-    }
-  }
-  return launch_mx_cols(a, stream, num_sms, tm, 0, a.N, ksplit);
+  const MxPlan pl = mx_plan(a.M, a.N, a.K, a.k_outlier, num_sms);
+  const int64_t n_mid = pl.n_full * kMxTN < a.N ? pl.n_full * kMxTN : a.N;
+  cudaError_t e = launch_mx_cols(a, stream, num_sms, pl.tm, 0, n_mid, pl.ksplit);
+  if (e != cudaSuccess || n_mid == a.N) return e;
+  return launch_mx_cols(a, stream, num_sms, 128, n_mid, a.N, 1);
 }
 
 }  // namespace atom
