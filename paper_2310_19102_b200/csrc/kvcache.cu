@@ -98,6 +98,25 @@ __device__ __forceinline__ void code_pairs(uint32_t w, float2 (&c)[4]) {
   }
 }
 
+// The nibbles at bits 4i and 4i + 16 of w as an exact half2 (n_lo, n_hi): the nibbles land in
+// the low mantissa bits under the exponent of 1024 (0x6400 = 1024 + n), one HSUB2 removes 1024.
+__device__ __forceinline__ uint32_t nibble_h2(uint32_t w, int i) {
+  uint32_t x = ((w >> (4 * i)) & 0x000F000Fu) | 0x64006400u;
+  const __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&x),
+                            __half2half2(__ushort_as_half(static_cast<unsigned short>(0x6400))));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// D (16 x 8, fp32) += A (16 x 16, f16, row) * B (16 x 8, f16, col) on the tensor cores
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 // CTA (b, h, chunk): tokens [c0, c1) of sequence b.  splits > 1: writes the chunk's (max, sum,
 // unnormalised output) to the workspace; splits == 1: the normalised output.
 __global__ void __launch_bounds__(kAttThreads)
@@ -117,58 +136,81 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
   const int c0 = split * chunk, c1 = min(L, c0 + chunk);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tj = lane >> 2, part4 = lane & 3;         // token slot within 8, dimension quarter
-  // q of this lane's 32 dimensions, scaled by 1/sqrt(d), and their sum
-  float qv[32];     // dims 32 part4 + j; used as 16 float2 pairs (2k, 2k+1)
+  // sum of q over this lane's 32 dimensions (the (s, mn) form of a dequantized dot product:
+  // q . (s n + mn) = s (q . n) + mn sum(q))
+  float qsum = 0.0f;
   {
-    const uint4* qp = reinterpret_cast<const uint4*>(q + static_cast<int64_t>(bh) * kKvD + 32 * part4);
+    const __half2* qp = reinterpret_cast<const __half2*>(q + static_cast<int64_t>(bh) * kKvD +
+                                                         32 * part4);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint4 r = qp[i];
-      const __half2* hp = reinterpret_cast<const __half2*>(&r);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __half22float2(hp[k]);
-        qv[8 * i + 2 * k] = f.x;
-        qv[8 * i + 2 * k + 1] = f.y;
-      }
+    for (int i = 0; i < 16; ++i) {
+      const float2 f = __half22float2(qp[i]);
+      qsum += f.x;
+      qsum += f.y;
     }
   }
   constexpr float kRsqrtD = 0.08838834764831845f;     // 1 / sqrt(128)
-  float qsum = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) qsum += qv[i];
   const int32_t* bt = block_table + static_cast<int64_t>(b) * max_pages;
   // the 16 tokens t0 .. t0+15 of a warp step lie in one page (t0 % 16 == 0): one table lookup
   auto vec0 = [&](int t0) {                           // (page, head, offset) index of token t0
     return (static_cast<int64_t>(__ldg(bt + t0 / kKvPage)) * H + h) * kKvPage + t0 % kKvPage;
   };
-  const float2* q2 = reinterpret_cast<const float2*>(qv);
+  // q as the B operand of m16n8k16 (column 0 = lanes tj == 0; the other columns zero): k-tile
+  // kt = 2 wi + e, slots (2 part4, +1) <-> dims 32 part4 + 8 wi + 2e + (0, 4), slots
+  // (2 part4 + 8, +9) <-> dims 32 part4 + 8 wi + 2e + (1, 5) -- the pairs nibble_h2 makes
+  uint32_t qb[8][2];
+  {
+    const __half* qh = q + static_cast<int64_t>(bh) * kKvD + 32 * part4;
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int dm = 8 * wi + 2 * e + r;
+          const __half2 v = __halves2half2(qh[dm], qh[dm + 4]);
+          qb[2 * wi + e][r] = tj == 0 ? *reinterpret_cast<const uint32_t*>(&v) : 0u;
+        }
+  }
+  float qsum_all = qsum + __shfl_xor_sync(0xffffffffu, qsum, 1);
+  qsum_all += __shfl_xor_sync(0xffffffffu, qsum_all, 2);
 
-  // A warp step covers 16 tokens of one page: lane (tj, part4) takes tokens t0 + tj and
-  // t0 + 8 + tj (two independent loads and FMA chains per lane); every step's codes and (s, mn)
-  // are loaded one step ahead.
-  constexpr int kTpl = 2;                             // tokens per lane per step
+  // A warp step covers 8 kTpl tokens (kTpl / 2 whole pages): lane (tj, part4) loads dims
+  // 32 part4 .. +31 of tokens t0 + 8 u + tj, u < kTpl -- in pass 1 exactly its A fragment of
+  // the page's m16n8k16 (rows tj, tj + 8); every step's codes and (s, mn) are loaded one step
+  // ahead.
+  constexpr int kTpl = 2;     // tokens per lane per step (4: 191.6 vs 183.2 us at B=128 L=1024)
+  static_assert(kTpl % 2 == 0, "a warp step covers whole pages");
   constexpr int kStep = 8 * kTpl * (kAttThreads / 32);
   auto load = [&](const uint8_t* codes, const float* prm, int t0, uint4 (&w)[kTpl],
                   float2 (&sm)[kTpl]) {
-    if (t0 < c1) {
-      const int64_t v0 = vec0(t0) + tj;
 #pragma unroll
-      for (int u = 0; u < kTpl; ++u)
-        if (t0 + 8 * u + tj < c1) {
-          const int64_t v = v0 + 8 * u;
-          w[u] = __ldg(reinterpret_cast<const uint4*>(codes + v * (kKvD / 2) + 16 * part4));
-          sm[u] = __ldg(reinterpret_cast<const float2*>(prm) + v);
-        }
+    for (int pg = 0; pg < kTpl / 2; ++pg) {
+      const int tp = t0 + 16 * pg;
+      if (tp < c1) {
+        const int64_t v0 = vec0(tp) + tj;
+#pragma unroll
+        for (int u = 2 * pg; u < 2 * pg + 2; ++u)
+          if (t0 + 8 * u + tj < c1) {
+            const int64_t v = v0 + 8 * (u - 2 * pg);
+            w[u] = __ldg(reinterpret_cast<const uint4*>(codes + v * (kKvD / 2) + 16 * part4));
+            sm[u] = __ldg(reinterpret_cast<const float2*>(prm) + v);
+          }
+      }
     }
   };
 
   // ---- pass 1: scores of the chunk into shared memory ----
   float wmax = -INFINITY;
-  uint4 wn[kTpl] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-  float2 smn[kTpl] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
-  load(kc, kp, c0 + 16 * warp, wn, smn);
-  for (int t0 = c0 + 16 * warp; t0 < c1; t0 += kStep) {
+  uint4 wn[kTpl];
+  float2 smn[kTpl];
+#pragma unroll
+  for (int u = 0; u < kTpl; ++u) {
+    wn[u] = make_uint4(0, 0, 0, 0);
+    smn[u] = make_float2(0.0f, 0.0f);
+  }
+  load(kc, kp, c0 + 8 * kTpl * warp, wn, smn);
+  for (int t0 = c0 + 8 * kTpl * warp; t0 < c1; t0 += kStep) {
     uint4 w[kTpl];
     float2 sm[kTpl];
 #pragma unroll
@@ -177,32 +219,33 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
       sm[u] = smn[u];
     }
     load(kc, kp, t0 + kStep, wn, smn);
-    float part[kTpl];
+    // one m16n8k16 chain per page: A = the page's codes (row = token t0 + 16 pt + tj (+8),
+    // k-slots = this lane's dimensions, see qb), B = q in column 0; column 0 of D holds the
+    // exact-product fp32 dot products sum_i q_i n_ti of tokens tj and tj + 8 (lanes part4 == 0)
 #pragma unroll
-    for (int u = 0; u < kTpl; ++u) {
-      part[u] = 0.0f;
-      if (t0 + 8 * u + tj < c1) {
-        const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-        float2 d2 = make_float2(0.0f, 0.0f);
+    for (int pt = 0; pt < kTpl / 2; ++pt) {
+      float d[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      const uint32_t r0[4] = {w[2 * pt].x, w[2 * pt].y, w[2 * pt].z, w[2 * pt].w};
+      const uint32_t r1[4] = {w[2 * pt + 1].x, w[2 * pt + 1].y, w[2 * pt + 1].z, w[2 * pt + 1].w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float2 c[4];
-          code_pairs(ww[i], c);
+      for (int wi = 0; wi < 4; ++wi) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) d2 = __ffma2_rn(q2[4 * i + k], c[k], d2);
-        }
-        part[u] = fmaf(sm[u].x, d2.x + d2.y, sm[u].y * qsum);
+        for (int e = 0; e < 2; ++e)
+          mma_16816(d, nibble_h2(r0[wi], 2 * e), nibble_h2(r1[wi], 2 * e),
+                    nibble_h2(r0[wi], 2 * e + 1), nibble_h2(r1[wi], 2 * e + 1), qb[2 * wi + e][0],
+                    qb[2 * wi + e][1]);
       }
-    }
+      if (part4 == 0) {
 #pragma unroll
-    for (int u = 0; u < kTpl; ++u) {
-      part[u] += __shfl_xor_sync(0xffffffffu, part[u], 1);
-      part[u] += __shfl_xor_sync(0xffffffffu, part[u], 2);
-      const int t = t0 + 8 * u + tj;
-      if (t < c1) {
-        const float score = part[u] * kRsqrtD;
-        if (part4 == 0) sc[t - c0] = score;
-        wmax = fmaxf(wmax, score);
+        for (int u2 = 0; u2 < 2; ++u2) {
+          const int t = t0 + 16 * pt + 8 * u2 + tj;
+          if (t < c1) {
+            const float2 m = sm[2 * pt + u2];
+            const float score = fmaf(m.x, d[2 * u2], m.y * qsum_all) * kRsqrtD;
+            sc[t - c0] = score;
+            wmax = fmaxf(wmax, score);
+          }
+        }
       }
     }
   }
@@ -221,8 +264,8 @@ decode_attention_kernel(const __half* __restrict__ q, int32_t H,
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.0f;
   float psum = 0.0f, pmn = 0.0f;                      // sum p_t, sum p_t mn_t (this lane's tokens)
-  load(vc, vp, c0 + 16 * warp, wn, smn);
-  for (int t0 = c0 + 16 * warp; t0 < c1; t0 += kStep) {
+  load(vc, vp, c0 + 8 * kTpl * warp, wn, smn);
+  for (int t0 = c0 + 8 * kTpl * warp; t0 < c1; t0 += kStep) {
     uint4 w[kTpl];
     float2 sm[kTpl];
 #pragma unroll

@@ -18,7 +18,9 @@ timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k re
   -s 3 -c 1 -o $O/prof_gemm_cfg5 python bench.py --steps 4 --warmup 3 --no-e2e \
   --no-cpu-baseline --spinup 0 --no-peak --no-mx > $O/prof_gemm.log 2>&1; echo "ncu gemm rc=$?"
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:mx_gemm \
-  -s 3 -c 1 -o $O/prof_mx_cfg5 python tools/mx_time.py "1024,28672,8192" > $O/prof_mx.log 2>&1; echo "ncu mx rc=$?"
+  -s 6 -c 2 -o $O/prof_mx_cfg5 python tools/mx_time.py "1024,28672,8192" > $O/prof_mx.log 2>&1; echo "ncu mx rc=$?"
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:reorder_quantize \
   -s 3 -c 1 -o $O/prof_quant_cfg5 python bench.py --steps 4 --warmup 3 --no-e2e \
   --no-cpu-baseline --spinup 0 --no-peak --no-mx > $O/prof_quant.log 2>&1; echo "ncu quant rc=$?"
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:decode_attention_kernel \
+  -s 3 -c 1 -o $O/prof_kv python tools/kv_time.py "128,1024,32" > $O/prof_kv.log 2>&1; echo "ncu kv rc=$?"
