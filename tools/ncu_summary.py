@@ -29,7 +29,8 @@ for k in keys:
 st = sorted([(float(d[k][0].replace(",", "") or 0), k) for k in d
              if "pcsamp_warps_issue_stalled" in k and not k.endswith("not_issued")], reverse=True)
 print("stalls:", ", ".join(f"{k.split('stalled_')[1]}={int(a)}" for a, k in st[:8]))
-src = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source=sass"))))[2:]
+src = [r for r in csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source=sass")))
+       if len(r) > 2 and r[2].strip().isdigit()]
 tot = sum(int(r[2]) for r in src)
 print("samples", tot)
 for r in sorted(src, key=lambda r: -int(r[2]))[:top]:
