@@ -22,43 +22,43 @@ FLAGS = [
 ]
 
 
-STAMP = LIB.with_name("libatom.so.flags")
+# Debug library: identical kernels whose wait loops trap (with a message naming the CTA and the
+# barrier) after 2 s instead of hanging -- ptx.cuh ATOM_WAIT_LOOP; tests/test_debug_lib.py
+LIB_DEBUG = PKG / "libatom_debug.so"
+DEBUG_FLAGS = ["-DATOM_MBAR_TIMEOUT_NS=2000000000"]
 
 
 def _extra() -> list:
     return os.environ.get("ATOM_NVCC_EXTRA", "").split()   # development variants (A/B runs)
 
 
-def _stale() -> bool:
-    if not LIB.exists() or not STAMP.exists():
+def _stale(lib: Path, flags: list) -> bool:
+    stamp = lib.with_name(lib.name + ".flags")
+    if not lib.exists() or not stamp.exists():
         return True
-    if STAMP.read_text() != " ".join(FLAGS + _extra()):     # built with other flags
+    if stamp.read_text() != " ".join(flags):               # built with other flags
         return True
-    mt = LIB.stat().st_mtime
+    mt = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + \
         [ROOT / "include" / "atom.h"]
     return any(d.stat().st_mtime > mt for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB.with_name(f"libatom.so.tmp{os.getpid()}")
-    extra = _extra()
-    cmd = [NVCC, *FLAGS, *extra, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> Path:
+    lib = LIB_DEBUG if debug else LIB
+    flags = FLAGS + (DEBUG_FLAGS if debug else []) + _extra()
+    if not force and not _stale(lib, flags):
+        return lib
+    tmp = lib.with_name(f"{lib.name}.tmp{os.getpid()}")
+    cmd = [NVCC, *flags, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = PKG / "build.log"
+    log = PKG / ("build_debug.log" if debug else "build.log")
     log.write_text(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    STAMP.write_text(" ".join(FLAGS + extra))
-    return LIB
-
-
-if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    os.replace(tmp, lib)
+    lib.with_name(lib.name + ".flags").write_text(" ".join(flags))
+    return lib

@@ -722,7 +722,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
           const int first = cta_of(p, static_cast<int64_t>(w.tile) * p.G);
           const int nseg = static_cast<int>(blockIdx.x) - first;
           if (e == 0 && lane == 0) {
-            while (ld_acquire(p.counters + blockIdx.x) < nseg) __nanosleep(64);
+            flag_wait_ge(p.counters + blockIdx.x, nseg);
             p.counters[blockIdx.x] = 0;
           }
           named_bar_sync(1, kEpiThreads);
@@ -969,7 +969,7 @@ w4a4_gemm_kernel(const __grid_constant__ CUtensorMap tm_wq4,
             p.trace[29 * kTraceN + blockIdx.x] = nseg;
           }
 #endif
-          while (ld_acquire(p.counters + blockIdx.x) < nseg) __nanosleep(64);
+          flag_wait_ge(p.counters + blockIdx.x, nseg);
 #ifdef ATOM_DEV_PROBES
           if (p.trace != nullptr && blockIdx.x < kTraceN) p.trace[28 * kTraceN + blockIdx.x] = gtimer();
 #endif

@@ -63,17 +63,37 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return done != 0;
 }
 
+// Debug builds (-DATOM_MBAR_TIMEOUT_NS=<ns>, build.py build(debug=True) -> libatom_debug.so):
+// every wait loop (mbarrier phases, stream-K counters) traps after ATOM_MBAR_TIMEOUT_NS / 64
+// unsuccessful polls, so a pipeline-protocol bug fails the launch loudly (cudaErrorLaunchFailure
+// / illegal instruction at the next synchronisation) instead of hanging the GPU.  Release builds
+// compile the plain loops.
+#ifdef ATOM_MBAR_TIMEOUT_NS
+// a poll of a hinted try_wait suspends up to ~1 us, a counter poll sleeps 64 ns: the limit in
+// polls is a lower bound of the timeout; one 32-bit counter keeps the register cost to one
+// register (the INT GEMM's epilogue warps run at their 216-register cap)
+#define ATOM_WAIT_LOOP(cond)                                                                \
+  do {                                                                                      \
+    for (uint32_t n_ = 0; !(cond);)                                                         \
+      if (++n_ > static_cast<uint32_t>(ATOM_MBAR_TIMEOUT_NS / 64)) asm volatile("trap;");   \
+  } while (0)
+#else
+#define ATOM_WAIT_LOOP(cond) \
+  do {                       \
+    while (!(cond)) {        \
+    }                        \
+  } while (0)
+#endif
+
 // Spin on the non-blocking probe (no suspend): lowest latency when the phase is usually
 // already complete.
 __device__ __forceinline__ void mbar_wait_test(uint64_t* bar, uint32_t parity) {
-  while (!mbar_test(bar, parity)) {
-  }
+  ATOM_WAIT_LOOP(mbar_test(bar, parity));
 }
 
 // Wait until the phase with the given parity has completed.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
+  ATOM_WAIT_LOOP(mbar_try_wait(bar, parity));
 }
 
 // Same, with the default (short) hardware suspend: spins with try_wait.
@@ -89,8 +109,7 @@ __device__ __forceinline__ bool mbar_try_wait_nohint(uint64_t* bar, uint32_t par
   return done != 0;
 }
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait_nohint(bar, parity)) {
-  }
+  ATOM_WAIT_LOOP(mbar_try_wait_nohint(bar, parity));
 }
 
 // Programmatic dependent launch.  griddep_wait: block until the grids this one depends on
@@ -148,6 +167,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Wait (sleeping 64 ns between polls) until the global counter *p reaches `target`.
+__device__ __forceinline__ void flag_wait_ge(const int* p, int target) {
+  ATOM_WAIT_LOOP(ld_acquire(p) >= target || (__nanosleep(64), false));
 }
 
 // ---------------------------------------------------------------------------------------------
